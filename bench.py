@@ -1,0 +1,357 @@
+"""Benchmark: signal-timesteps/s, forward + backward (robustness trace + gradients).
+
+Workload (BASELINE.json configs[1]): Eventually[10,100](||p - g|| < 0.5),
+LogSumExp(temp=10), p = fp32 2-D random walks, B = 1024 signals x T = 10,000 samples
+per GPU.  One step = the full robustness trace [B, T] (masking.trace_var semantics)
+plus the VJP of that trace with the ones cotangent (tape.backward default) into
+d p (both channels).  `value` = B*T*N / step time with inputs resident in HBM;
+`e2e` = the same through the public API with pinned-host inputs copied in and the
+trace + gradients copied out every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun): every rank runs its own B rows (weak scaling); there is no
+data-path collective for this workload; time = max over ranks.
+`--impl reference` times the CPU reference path (the oracle port of the
+reference algorithm, oracle/stl_oracle.py) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "signal-timesteps/sec fwd+bwd (robustness+grads) at T=10k; % HBM/SFU roofline"
+UNIT = "signal-timesteps/s"
+B_PER_GPU, T_LEN = 1024, 10_000
+WINDOW = (10, 100)
+TEMP = 10.0
+RADIUS = 0.5
+
+
+def _config(n):
+    return {"workload": "C2: F[10,100](||p-g||<0.5) LSE(temp=10), 2-D random walks",
+            "global_batch": B_PER_GPU * n, "seq_len": T_LEN, "channels": 2,
+            "parallelism": f"batch-shard dp{n}" if n > 1 else "single",
+            "cotangent": "ones (full-trace VJP)",
+            "l2": "rotating 3 input/output sets (3 x 205 MB > 126 MB L2)"}
+
+
+def _walk(B, T, seed):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    p0 = rng.uniform(-1, 1, (B, 1, 2))
+    return np.asarray(p0 + np.cumsum(0.05 * rng.normal(0, 1, (B, T, 2)), axis=1), dtype=np.float32)
+
+
+def _formula(P):
+    return P.Eventually(P.NormPred(("px", "py"), "<", RADIUS, (0.0, 0.0)),
+                        P.StepInterval(*WINDOW))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+def _cpu_rows(args):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import stl_oracle
+    import paper_2501_04194_b200.core as C
+    import paper_2501_04194_b200.formula as F
+    rows, seed = args
+    p = _walk(rows, T_LEN, seed).astype(np.float64)
+    f = F.Eventually(F.NormPred(("px", "py"), "<", RADIUS, (0.0, 0.0)), C.StepInterval(*WINDOW))
+    cfg = C.SemanticsConfig(mode=C.LogSumExp(TEMP))
+    t0 = time.perf_counter()
+    for r in range(0, rows, 16):  # 16-row chunks bound the (rows, T, K) window arrays
+        q = p[r:r + 16]
+        stl_oracle.trace_and_grad(f, {"px": q[..., 0], "py": q[..., 1]}, cfg)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(rows=8, cores=1):
+    """Time the oracle port on `rows` x T signals; returns signal-timesteps/s."""
+    if cores <= 1:
+        _cpu_rows((2, 99))  # warm-up (imports, allocator)
+        t0 = time.perf_counter()
+        _cpu_rows((rows, 1))
+        dt = time.perf_counter() - t0
+        return rows * T_LEN / dt, dt
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_rows, [(1, 99)] * cores)
+        t0 = time.perf_counter()
+        pool.map(_cpu_rows, [(max(rows // cores, 1), i) for i in range(cores)])
+        dt = time.perf_counter() - t0
+    return max(rows // cores, 1) * cores * T_LEN / dt, dt
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    rows = 2 * cores
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_baseline(rows=cores, cores=cores)
+    for _ in range(args.steps):
+        v, _ = cpu_baseline(rows=rows, cores=cores)
+        vals.append(v)
+    value = statistics.median(vals)
+    sample = f"{rows} rows x T={T_LEN} per step (of B={B_PER_GPU}), row-parallel over {cores} processes"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B_PER_GPU * T_LEN / value * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world):
+    import numpy as np
+    import torch
+    import paper_2501_04194_b200 as P
+    from paper_2501_04194_b200 import _lib
+    from paper_2501_04194_b200.engine import compile_formula
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B, T = B_PER_GPU, T_LEN
+    f = _formula(P)
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(TEMP))
+    comp = compile_formula(f, ["px", "py"], cfg)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+    sptr = __import__("ctypes").c_void_p(stream.cuda_stream)
+
+    NSET = 3
+    host = _walk(B, T, 1 + rank)
+    sets = []
+    for s in range(NSET):
+        p = torch.tensor(np.roll(host, s * 17, axis=1), device=dev)  # [B, T, 2] interleaved
+        sets.append({"px": p[..., 0], "py": p[..., 1], "p": p,
+                     "out": torch.empty(B, T, device=dev),
+                     "dp": torch.zeros(B, T, 2, device=dev)})
+    fb, bb = comp.workspace_bytes(B, T)
+    fws = torch.empty(fb, dtype=torch.uint8, device=dev)
+    bws = torch.empty(bb, dtype=torch.uint8, device=dev)
+    ones = torch.ones(B, T, device=dev)
+    params = comp.smooth_params()
+
+    def step(s, ev=None):
+        d = sets[s]
+        if ev:
+            ev[0].record(stream)
+        comp.forward([d["px"], d["py"]], params, d["out"], fws, sptr)
+        if ev:
+            ev[1].record(stream)
+        d["dp"].zero_()
+        comp.backward([d["px"], d["py"]], params, d["out"], ones,
+                      [d["dp"][..., 0], d["dp"][..., 1]], None, fws, bws, sptr)
+        if ev:
+            ev[2].record(stream)
+
+    for i in range(max(args.warmup, 3)):
+        step(i % NSET)
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib.stlg_launch_count(1)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(i % NSET, evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.stlg_launch_count(1)
+    ms = start.elapsed_time(stop)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    bwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    ms_step = ms / args.steps
+    value = B * T * world / (ms_step / 1e3)
+
+    # ---- e2e through the public API: pinned host -> device -> host ----------
+    hp = torch.tensor(host).pin_memory()
+    h_tr = torch.empty(B, T).pin_memory()
+    h_dp = torch.empty(B, T, 2).pin_memory()
+    e2e_steps = max(2, min(args.steps, 10))
+
+    def e2e_step():
+        p = hp.to(dev, non_blocking=True)
+        px = p[..., 0].detach().requires_grad_(True)
+        py = p[..., 1].detach().requires_grad_(True)
+        out = P.trace(f, {"px": px, "py": py}, cfg)
+        out.backward(ones)
+        h_tr.copy_(out.detach(), non_blocking=True)
+        h_dp[..., 0].copy_(px.grad, non_blocking=True)
+        h_dp[..., 1].copy_(py.grad, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = B * T * world / (e2e_ms / 1e3)
+
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+        # algorithmic bytes: fwd reads px, py (8 B) and writes the
+        # trace (4 B); bwd reads the cotangent (4 B) and writes d px, d py (8 B)
+        alg = {"fwd": 12.0 * B * T, "bwd": 12.0 * B * T}
+        kern = {"fwd": fwd_ms, "bwd": bwd_ms}
+        dom = max(kern, key=kern.get)
+        achieved = alg[dom] / (kern[dom] / 1e3) / 1e9
+        step_ach = (alg["fwd"] + alg["bwd"]) / ((fwd_ms + bwd_ms) / 1e3) / 1e9
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(dom)
+        except Exception:
+            pass
+        cores = 1
+        cpu_v, cpu_dt = cpu_baseline(rows=96, cores=cores)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": _config(world),
+                "roofline": {"bound": "hbm", "kernel": f"stlg {dom} (timed F/G LSE)",
+                             "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": achieved / hbm, "peak_source": hbm_src,
+                             "traffic": traffic,
+                             "alg_bytes_per_launch": alg[dom],
+                             "step_achieved_gbs": step_ach, "step_frac": step_ach / hbm,
+                             "fwd_ms": fwd_ms, "bwd_ms": bwd_ms},
+                "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": cores, "kind": "port",
+                                 "sample": f"96 rows x T={T_LEN} fwd+bwd, oracle/stl_oracle.py "
+                                           f"(numpy f64, single process), {cpu_dt:.1f}s"},
+                "e2e": {"value": e2e_val, "unit": UNIT,
+                        "h2d_bytes_per_step": B * T * 2 * 4,
+                        "d2h_bytes_per_step": B * T * 4 + B * T * 2 * 4,
+                        "ms_per_step": e2e_ms, "path": "paper_2501_04194_b200.trace + autograd"},
+                "gpu_launches": int(launches),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

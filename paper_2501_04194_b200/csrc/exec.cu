@@ -1,0 +1,588 @@
+// exec.cu — the C ABI (include/stlg.h): node-program compiler and executor.
+//
+// stlg_compile lowers the formula DAG (formula.py:65-135 node classes,
+// flattened by the Python host in topological order) into a schedule of
+// entries, one per temporal operator (Eventually / Always / Until) plus a
+// pointwise entry for an elementwise root.  Each entry carries its child
+// sub-formula(s) as a fused DExpr: every Pred / NormPred / Not / And / Or /
+// TRUE below a temporal operator is evaluated inside that operator's load,
+// and temporal children are read from their materialised traces ("slots").
+// This replaces the recursive evaluator masking.trace_var (masking.py:308-343)
+// which materialises one full array per AST node.
+//
+// stlg_forward runs the entries in order; stlg_backward runs them in reverse,
+// each consuming the cotangent of its own output (user cotangent for the
+// root, else its slot's accumulated cotangent) — the schedule equivalent of
+// tape.backward's reverse topological walk (tape.py:114-134).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/stlg.h"
+#include "kernels.cuh"
+
+using namespace stlg;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+enum EntryKind { E_POINTWISE, E_FG_TIMED, E_FG_UNTIMED, E_FG_SMOOTH, E_UNTIL };
+
+struct HLeaf {
+  int kind;
+  int src, src2;  // global source ids: [0, n_ch) channels, n_ch + s slots
+  float s_in, s_out, c, cx, cy;
+};
+struct HExpr {
+  std::vector<HLeaf> leaf;
+  std::vector<DStep> step;
+};
+struct Entry {
+  int kind;
+  float sg;
+  int a, b;
+  int untimed;
+  int smooth_slot;
+  HExpr e1, e2;
+  int out_slot;  // -1: the caller's trace buffer
+  int aux_slot;  // softmax window-LSE buffer, -1 if none
+};
+
+bool is_temporal(int op) { return op == STLG_EVENTUALLY || op == STLG_ALWAYS || op == STLG_UNTIL; }
+bool is_elementwise(int op) {
+  return op == STLG_TRUE || op == STLG_PRED || op == STLG_NOT || op == STLG_AND || op == STLG_OR ||
+         op == STLG_NORM_PRED;
+}
+
+}  // namespace
+
+struct stlg_plan {
+  stlg_cfg cfg;
+  int n_ch = 0, n_smooth = 0, n_slots = 0, n_aux = 0;
+  int root_temporal = 0;
+  std::vector<Entry> entries;
+};
+
+namespace stlg {
+void count_launch(int n) { g_launches += n; }
+}  // namespace stlg
+
+namespace {
+
+// --------------------------------------------------------------------------
+// compiler
+// --------------------------------------------------------------------------
+struct Compiler {
+  const stlg_node* nodes;
+  int n;
+  stlg_plan* plan;
+  std::vector<int> slot_of;   // temporal / materialised node -> slot
+  std::vector<int> weight_;   // leaf weight of elementwise subtrees (memo)
+
+  int new_slot() { return plan->n_slots++; }
+
+  int weight(int i) {
+    if (weight_[i] >= 0) return weight_[i];
+    const stlg_node& nd = nodes[i];
+    int w;
+    if (is_temporal(nd.op) || slot_of[i] >= 0) w = 1;
+    else if (nd.op == STLG_NORM_PRED) w = 2;
+    else if (nd.op == STLG_NOT) w = weight(nd.left);
+    else if (nd.op == STLG_AND || nd.op == STLG_OR) w = weight(nd.left) + weight(nd.right);
+    else w = 1;
+    weight_[i] = w;
+    return w;
+  }
+
+  // Materialise an elementwise sub-formula into its own slot (pointwise entry).
+  int materialise(int i) {
+    if (slot_of[i] >= 0) return slot_of[i];
+    Entry e{};
+    e.kind = E_POINTWISE;
+    e.sg = 1.f;
+    e.aux_slot = -1;
+    build(i, 1.f, e.e1);
+    e.out_slot = new_slot();
+    slot_of[i] = e.out_slot;
+    plan->entries.push_back(e);
+    weight_.assign(n, -1);
+    return e.out_slot;
+  }
+
+  int push_leaf(HExpr& ex, const HLeaf& lf) {
+    ex.leaf.push_back(lf);
+    DStep s{(unsigned char)ST_LEAF, (unsigned char)(ex.leaf.size() - 1), 0, 0};
+    ex.step.push_back(s);
+    return (int)ex.step.size() - 1;
+  }
+
+  // Build node i scaled by `sign` (+1 / -1) into ex; returns the SSA step index.
+  int build(int i, float sign, HExpr& ex) {
+    const stlg_node& nd = nodes[i];
+    const float top = (float)plan->cfg.top_value;
+    if (slot_of[i] >= 0) {
+      HLeaf lf{LEAF_SRC, plan->n_ch + slot_of[i], 0, 1.f, sign, 0.f, 0.f, 0.f};
+      return push_leaf(ex, lf);
+    }
+    switch (nd.op) {
+      case STLG_TRUE: {
+        HLeaf lf{LEAF_CONST, 0, 0, 1.f, 1.f, sign * top, 0.f, 0.f};
+        return push_leaf(ex, lf);
+      }
+      case STLG_PRED:
+      case STLG_NORM_PRED: {
+        float thr = (float)nd.threshold;
+        // '>' : x + (-c)    '<' : (-x) + c     (masking.py:319-323)
+        HLeaf lf{nd.op == STLG_PRED ? LEAF_AFFINE : LEAF_NORM, nd.chan,
+                 nd.op == STLG_PRED ? 0 : nd.chan2, nd.cmp == 0 ? 1.f : -1.f, sign,
+                 nd.cmp == 0 ? -thr : thr, (float)nd.center0, (float)nd.center1};
+        return push_leaf(ex, lf);
+      }
+      case STLG_NOT:
+        return build(nd.left, -sign, ex);
+      case STLG_AND:
+      case STLG_OR: {
+        // sign * min(l, r) == max(-l, -r) exactly (the reference's min is -max(-x))
+        bool is_min = (nd.op == STLG_AND) == (sign > 0);
+        int ka, kb;
+        int l = nd.left, r = nd.right;
+        if (is_elementwise(nodes[l].op) && slot_of[l] < 0 && weight(l) > 7) materialise(l);
+        if (is_elementwise(nodes[r].op) && slot_of[r] < 0 && weight(r) > 7) materialise(r);
+        ka = build(l, sign, ex);
+        kb = build(r, sign, ex);
+        DStep s{(unsigned char)(is_min ? ST_MIN : ST_MAX), (unsigned char)ka, (unsigned char)kb, 0};
+        ex.step.push_back(s);
+        return (int)ex.step.size() - 1;
+      }
+      default:
+        return -1;  // temporal without a slot: impossible after ordering
+    }
+  }
+
+  bool fits(const HExpr& ex) {
+    if ((int)ex.leaf.size() > MAX_LEAF || (int)ex.step.size() > MAX_STEP) return false;
+    std::vector<int> srcs;
+    for (auto& lf : ex.leaf) {
+      if (lf.kind == LEAF_CONST) continue;
+      srcs.push_back(lf.src);
+      if (lf.kind == LEAF_NORM) srcs.push_back(lf.src2);
+    }
+    std::sort(srcs.begin(), srcs.end());
+    srcs.erase(std::unique(srcs.begin(), srcs.end()), srcs.end());
+    return (int)srcs.size() <= MAX_SRC;
+  }
+};
+
+int validate_nodes(const stlg_node* nodes, int n, int n_ch, int n_smooth) {
+  if (n <= 0) return fail(STLG_E_INVALID, "empty node program");
+  for (int i = 0; i < n; ++i) {
+    const stlg_node& nd = nodes[i];
+    auto child_ok = [&](int c) { return c >= 0 && c < i; };
+    switch (nd.op) {
+      case STLG_TRUE:
+        break;
+      case STLG_PRED:
+        if (nd.chan < 0 || nd.chan >= n_ch) return fail(STLG_E_INVALID, "pred channel out of range");
+        break;
+      case STLG_NORM_PRED:
+        if (nd.chan < 0 || nd.chan >= n_ch || nd.chan2 < 0 || nd.chan2 >= n_ch)
+          return fail(STLG_E_INVALID, "norm channel out of range");
+        break;
+      case STLG_NOT:
+        if (!child_ok(nd.left)) return fail(STLG_E_INVALID, "bad child index");
+        break;
+      case STLG_AND:
+      case STLG_OR:
+        if (!child_ok(nd.left) || !child_ok(nd.right)) return fail(STLG_E_INVALID, "bad child index");
+        break;
+      case STLG_EVENTUALLY:
+      case STLG_ALWAYS:
+      case STLG_UNTIL:
+        if (!child_ok(nd.left)) return fail(STLG_E_INVALID, "bad child index");
+        if (nd.op == STLG_UNTIL && !child_ok(nd.right)) return fail(STLG_E_INVALID, "bad child index");
+        if (nd.itv_kind == STLG_ITV_STEP) {
+          if (nd.a < 0 || nd.b < nd.a) return fail(STLG_E_INVALID, "need 0 <= a <= b");
+        } else if (nd.itv_kind == STLG_ITV_SMOOTH) {
+          if (nd.op == STLG_UNTIL)
+            return fail(STLG_E_UNSUPPORTED, "until does not support smooth intervals");
+          if (nd.smooth_slot < 0 || nd.smooth_slot >= n_smooth)
+            return fail(STLG_E_INVALID, "smooth slot out of range");
+        } else if (nd.itv_kind != STLG_ITV_NONE) {
+          return fail(STLG_E_INVALID, "bad interval kind");
+        }
+        break;
+      default:
+        return fail(STLG_E_INVALID, "unknown opcode");
+    }
+  }
+  return STLG_OK;
+}
+
+// --------------------------------------------------------------------------
+// executor helpers
+// --------------------------------------------------------------------------
+struct Bufs {
+  float* slots;   // n_slots * B * T
+  float* aux;     // n_aux * B * T
+  float* gslots;  // n_slots * B * T (backward)
+  float* scratch; // 3 * B * T (backward)
+  long long BT;
+  float* slot(int s) const { return slots + (long long)s * BT; }
+  float* gslot(int s) const { return gslots + (long long)s * BT; }
+  float* auxp(int s) const { return aux + (long long)s * BT; }
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+void fwd_layout(const stlg_plan* p, long long BT, size_t* slots_b, size_t* aux_b) {
+  *slots_b = align256(sizeof(float) * (size_t)p->n_slots * BT);
+  *aux_b = align256(sizeof(float) * (size_t)p->n_aux * BT);
+}
+
+int resolve(const stlg_plan* p, const HExpr& h, const stlg_channel* ch, const stlg_grad* dch,
+            const Bufs& bf, long long T, bool with_dst, DExpr& d) {
+  std::memset(&d, 0, sizeof(d));
+  std::map<int, int> local;
+  auto map_src = [&](int gid) -> int {
+    auto it = local.find(gid);
+    if (it != local.end()) return it->second;
+    int k = (int)local.size();
+    if (k >= MAX_SRC) return -1;
+    local[gid] = k;
+    if (gid < p->n_ch) {
+      d.src[k] = {ch[gid].ptr, ch[gid].row_stride, ch[gid].elem_stride};
+      if (with_dst && dch != nullptr && dch[gid].ptr != nullptr)
+        d.dst[k] = {dch[gid].ptr, dch[gid].row_stride, dch[gid].elem_stride};
+      else
+        d.dst[k] = {nullptr, 0, 0};
+    } else {
+      int s = gid - p->n_ch;
+      d.src[k] = {bf.slot(s), T, 1};
+      d.dst[k] = with_dst ? DDst{bf.gslot(s), T, 1} : DDst{nullptr, 0, 0};
+    }
+    return k;
+  };
+  if ((int)h.leaf.size() > MAX_LEAF || (int)h.step.size() > MAX_STEP)
+    return fail(STLG_E_INVALID, "expression too large");
+  for (size_t i = 0; i < h.leaf.size(); ++i) {
+    const HLeaf& lf = h.leaf[i];
+    DLeaf& o = d.leaf[i];
+    o.kind = lf.kind;
+    o.s_in = lf.s_in;
+    o.s_out = lf.s_out;
+    o.c = lf.c;
+    o.cx = lf.cx;
+    o.cy = lf.cy;
+    if (lf.kind != LEAF_CONST) {
+      o.src = map_src(lf.src);
+      if (o.src < 0) return fail(STLG_E_INVALID, "too many sources");
+      if (lf.kind == LEAF_NORM) {
+        o.src2 = map_src(lf.src2);
+        if (o.src2 < 0) return fail(STLG_E_INVALID, "too many sources");
+      }
+    }
+  }
+  for (size_t k = 0; k < h.step.size(); ++k) d.step[k] = h.step[k];
+  d.n_step = (int)h.step.size();
+  d.n_leaf = (int)h.leaf.size();
+  d.n_src = (int)local.size();
+  return STLG_OK;
+}
+
+ModeP mode_params(const stlg_cfg& c) {
+  ModeP m;
+  double tau = c.mode == STLG_MODE_HARD ? 1.0 : c.temp;
+  m.tau = (float)tau;
+  m.tau2 = (float)(tau * 1.4426950408889634);
+  m.inv_tau2 = (float)(1.0 / (tau * 1.4426950408889634));
+  return m;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return STLG_OK;
+  return fail(STLG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+// ==========================================================================
+// C ABI
+// ==========================================================================
+extern "C" {
+
+int stlg_abi_version(void) { return STLG_ABI_VERSION; }
+
+const char* stlg_last_error(void) { return g_err.c_str(); }
+
+int64_t stlg_launch_count(int reset) {
+  long long v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, int32_t n_smooth,
+                 const stlg_cfg* cfg, stlg_plan** out_plan) {
+  if (!nodes || !cfg || !out_plan) return fail(STLG_E_INVALID, "null argument");
+  *out_plan = nullptr;
+  if (n_channels < 0 || n_smooth < 0) return fail(STLG_E_INVALID, "negative counts");
+  if (cfg->mode < 0 || cfg->mode > 2) return fail(STLG_E_UNSUPPORTED, "unsupported mode");
+  if (cfg->mode != STLG_MODE_HARD && !(cfg->temp > 0)) return fail(STLG_E_INVALID, "temp <= 0");
+  int rc = validate_nodes(nodes, n_nodes, n_channels, n_smooth);
+  if (rc != STLG_OK) return rc;
+
+  stlg_plan* plan = new stlg_plan();
+  plan->cfg = *cfg;
+  plan->n_ch = n_channels;
+  plan->n_smooth = n_smooth;
+  Compiler C{nodes, n_nodes, plan, std::vector<int>(n_nodes, -1), std::vector<int>(n_nodes, -1)};
+  const int root = n_nodes - 1;
+  for (int i = 0; i < n_nodes; ++i) {
+    const stlg_node& nd = nodes[i];
+    if (!is_temporal(nd.op)) continue;
+    Entry e{};
+    e.sg = (nd.op == STLG_ALWAYS) ? -1.f : 1.f;
+    e.a = nd.a;
+    e.b = nd.b;
+    e.untimed = nd.itv_kind == STLG_ITV_NONE;
+    e.smooth_slot = nd.smooth_slot;
+    e.aux_slot = -1;
+    if (nd.op == STLG_UNTIL) {
+      e.kind = E_UNTIL;
+    } else if (nd.itv_kind == STLG_ITV_SMOOTH) {
+      e.kind = E_FG_SMOOTH;
+    } else {
+      e.kind = e.untimed ? E_FG_UNTIMED : E_FG_TIMED;
+    }
+    if (nd.op != STLG_UNTIL && cfg->masked_fill) {
+      // masked_fill compat reduces sentinel-filled columns (masking.py:195-202)
+      if (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) e.kind = E_FG_TIMED;
+    }
+    C.build(nd.left, 1.f, e.e1);
+    if (nd.op == STLG_UNTIL) C.build(nd.right, 1.f, e.e2);
+    if (!C.fits(e.e1) || (nd.op == STLG_UNTIL && !C.fits(e.e2))) {
+      delete plan;
+      return fail(STLG_E_UNSUPPORTED, "sub-formula too large for one fused expression");
+    }
+    if (cfg->mode == STLG_MODE_SOFTMAX && (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED))
+      e.aux_slot = plan->n_aux++;
+    e.out_slot = (i == root) ? -1 : C.new_slot();
+    C.slot_of[i] = e.out_slot;
+    plan->entries.push_back(e);
+  }
+  if (is_temporal(nodes[root].op)) {
+    plan->root_temporal = 1;
+  } else {
+    Entry e{};
+    e.kind = E_POINTWISE;
+    e.sg = 1.f;
+    e.aux_slot = -1;
+    C.build(root, 1.f, e.e1);
+    if (!C.fits(e.e1)) {
+      delete plan;
+      return fail(STLG_E_UNSUPPORTED, "root formula too large for one fused expression");
+    }
+    e.out_slot = -1;
+    plan->entries.push_back(e);
+  }
+  if (cfg->masked_fill) {
+    for (auto& e : plan->entries)
+      if (e.kind != E_POINTWISE) {
+        delete plan;
+        return fail(STLG_E_UNSUPPORTED, "masked_fill is not supported on the device path yet");
+      }
+  }
+  *out_plan = plan;
+  return STLG_OK;
+}
+
+void stlg_free(stlg_plan* plan) { delete plan; }
+
+int stlg_plan_info(const stlg_plan* plan, int32_t* n_temporal, int32_t* n_slots,
+                   int32_t* root_is_temporal) {
+  if (!plan) return fail(STLG_E_INVALID, "null plan");
+  int nt = 0;
+  for (auto& e : plan->entries) nt += e.kind != E_POINTWISE;
+  if (n_temporal) *n_temporal = nt;
+  if (n_slots) *n_slots = plan->n_slots;
+  if (root_is_temporal) *root_is_temporal = plan->root_temporal;
+  return STLG_OK;
+}
+
+int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fwd_bytes,
+                         size_t* bwd_bytes) {
+  if (!plan) return fail(STLG_E_INVALID, "null plan");
+  if (B <= 0 || T <= 0) return fail(STLG_E_SHAPE, "empty signal batch");
+  long long BT = (long long)B * T;
+  size_t sb, ab;
+  fwd_layout(plan, BT, &sb, &ab);
+  if (fwd_bytes) *fwd_bytes = sb + ab + 256;
+  if (bwd_bytes)
+    *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
+                 align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * 4 * (size_t)T) +
+                 align256(sizeof(float) * 1024 * (size_t)T) + 256;
+  return STLG_OK;
+}
+
+static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws, size_t fwd_bytes,
+                      void* bwd_ws, size_t bwd_bytes, Bufs& bf) {
+  long long BT = (long long)B * T;
+  size_t need_f, need_b;
+  stlg_workspace_bytes(plan, B, T, &need_f, &need_b);
+  if (fwd_bytes < need_f) return fail(STLG_E_INVALID, "forward workspace too small");
+  size_t sb, ab;
+  fwd_layout(plan, BT, &sb, &ab);
+  uintptr_t base = ((uintptr_t)fwd_ws + 255) & ~(uintptr_t)255;
+  bf.BT = BT;
+  bf.slots = (float*)base;
+  bf.aux = (float*)(base + sb);
+  bf.gslots = nullptr;
+  bf.scratch = nullptr;
+  if (bwd_ws) {
+    if (bwd_bytes < need_b) return fail(STLG_E_INVALID, "backward workspace too small");
+    uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
+    bf.gslots = (float*)bb;
+    bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
+  }
+  return STLG_OK;
+}
+
+static void fill_fg(const stlg_plan* plan, const Entry& e, int64_t B, int64_t T, FGParams& p) {
+  std::memset(&p, 0, sizeof(p));
+  p.B = B;
+  p.L = T;
+  p.a = e.a;
+  p.b = e.b;
+  p.K = e.b - e.a + 1;
+  p.sg = e.sg;
+  p.pad_last = plan->cfg.pad_last;
+  p.pad_value = (float)plan->cfg.pad_value;
+  p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
+  p.mp = mode_params(plan->cfg);
+}
+
+int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B, int64_t T,
+                 const stlg_smooth* smooth_params, float* trace_out, void* fwd_ws,
+                 size_t fwd_ws_bytes, void* stream) {
+  if (!plan || !trace_out) return fail(STLG_E_INVALID, "null argument");
+  if (B <= 0 || T <= 0) return fail(STLG_E_SHAPE, "empty signal batch");
+  if (B > 65535) return fail(STLG_E_SHAPE, "batch rows per call must be <= 65535");
+  if (plan->n_ch > 0 && !channels) return fail(STLG_E_INVALID, "null channels");
+  if (plan->n_slots + plan->n_aux > 0 && !fwd_ws) return fail(STLG_E_INVALID, "null workspace");
+  Bufs bf{};
+  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, nullptr, 0, bf);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int mode = plan->cfg.mode;
+  for (const Entry& e : plan->entries) {
+    float* out = e.out_slot < 0 ? trace_out : bf.slot(e.out_slot);
+    cudaError_t ce = cudaSuccess;
+    if (e.kind == E_POINTWISE || e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) {
+      FGParams p;
+      fill_fg(plan, e, B, T, p);
+      if ((rc = resolve(plan, e.e1, channels, nullptr, bf, T, false, p.child))) return rc;
+      p.out = out;
+      p.aux = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
+      if (e.kind == E_POINTWISE) ce = launch_pointwise_fwd(mode, p, st);
+      else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_fwd(mode, p, st);
+      else ce = launch_fg_untimed_fwd(mode, p, st);
+    } else if (e.kind == E_UNTIL) {
+      UParams p;
+      std::memset(&p, 0, sizeof(p));
+      if ((rc = resolve(plan, e.e1, channels, nullptr, bf, T, false, p.left))) return rc;
+      if ((rc = resolve(plan, e.e2, channels, nullptr, bf, T, false, p.right))) return rc;
+      p.out = out;
+      p.B = B;
+      p.L = T;
+      p.a = e.untimed ? 0 : e.a;
+      p.b = e.untimed ? 0 : e.b;
+      p.K = e.untimed ? (int)T : e.b - e.a + 1;
+      p.untimed = e.untimed;
+      p.pad_last = plan->cfg.pad_last;
+      p.pad_value = (float)plan->cfg.pad_value;
+      p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
+      p.mp = mode_params(plan->cfg);
+      ce = launch_until_fwd(mode, p, st);
+    } else {
+      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
+    }
+    if ((rc = cuda_status(ce, "forward launch"))) return rc;
+  }
+  (void)smooth_params;
+  return STLG_OK;
+}
+
+int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B, int64_t T,
+                  const stlg_smooth* smooth_params, const float* trace, const float* cot,
+                  const stlg_grad* d_channels, double* d_smooth, void* fwd_ws,
+                  size_t fwd_ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, void* stream) {
+  if (!plan || !trace || !cot) return fail(STLG_E_INVALID, "null argument");
+  if (B <= 0 || T <= 0) return fail(STLG_E_SHAPE, "empty signal batch");
+  if (B > 65535) return fail(STLG_E_SHAPE, "batch rows per call must be <= 65535");
+  if (!bwd_ws) return fail(STLG_E_INVALID, "null backward workspace");
+  Bufs bf{};
+  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, bwd_ws, bwd_ws_bytes, bf);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int mode = plan->cfg.mode;
+  if (plan->n_slots > 0) {
+    cudaError_t ce = cudaMemsetAsync(bf.gslots, 0, sizeof(float) * (size_t)plan->n_slots * bf.BT, st);
+    if ((rc = cuda_status(ce, "memset"))) return rc;
+  }
+  for (auto it = plan->entries.rbegin(); it != plan->entries.rend(); ++it) {
+    const Entry& e = *it;
+    const float* g = e.out_slot < 0 ? cot : bf.gslot(e.out_slot);
+    const float* out_in = e.out_slot < 0 ? trace : bf.slot(e.out_slot);
+    cudaError_t ce = cudaSuccess;
+    if (e.kind == E_POINTWISE || e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) {
+      FGParams p;
+      fill_fg(plan, e, B, T, p);
+      if ((rc = resolve(plan, e.e1, channels, d_channels, bf, T, true, p.child))) return rc;
+      p.out_in = out_in;
+      p.aux_in = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
+      p.cot = g;
+      p.gbuf = bf.scratch;
+      if (e.kind == E_POINTWISE) ce = launch_pointwise_vjp(mode, p, g, st);
+      else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_bwd(mode, p, st);
+      else ce = launch_fg_untimed_bwd(mode, p, st);
+    } else if (e.kind == E_UNTIL) {
+      UParams p;
+      std::memset(&p, 0, sizeof(p));
+      if ((rc = resolve(plan, e.e1, channels, d_channels, bf, T, true, p.left))) return rc;
+      if ((rc = resolve(plan, e.e2, channels, d_channels, bf, T, true, p.right))) return rc;
+      p.out_in = out_in;
+      p.cot = g;
+      p.gl = bf.scratch;
+      p.gr = bf.scratch + bf.BT;
+      p.B = B;
+      p.L = T;
+      p.a = e.untimed ? 0 : e.a;
+      p.b = e.untimed ? 0 : e.b;
+      p.K = e.untimed ? (int)T : e.b - e.a + 1;
+      p.untimed = e.untimed;
+      p.pad_last = plan->cfg.pad_last;
+      p.pad_value = (float)plan->cfg.pad_value;
+      p.mp = mode_params(plan->cfg);
+      ce = launch_until_bwd(mode, p, st);
+    } else {
+      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
+    }
+    if ((rc = cuda_status(ce, "backward launch"))) return rc;
+  }
+  (void)smooth_params;
+  (void)d_smooth;
+  return STLG_OK;
+}
+
+}  // extern "C"

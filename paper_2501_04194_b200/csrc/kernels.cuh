@@ -1,0 +1,77 @@
+// kernels.cuh — parameter blocks and launch entry points of the stlg kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace stlg {
+
+// Eventually / Always (timed [a,b], untimed) and pointwise expression kernels.
+struct FGParams {
+  DExpr child;
+  const float* out_in;  // backward: this node's forward trace (v-space)
+  const float* aux_in;  // backward, softmax: window LSE L_t (u-space)
+  const float* cot;     // backward: cotangent of this node's trace
+  float* out;           // forward: trace (v-space); pointwise: output
+  float* aux;           // forward, softmax: L_t
+  float* gbuf;          // backward scratch [B, L] (hard untimed / brute force)
+  long long B, L;
+  int a, b, K, Kp, NB;
+  float sg;       // +1 Eventually (max), -1 Always (min)
+  int pad_last;   // PaddingPolicy('last')
+  float pad_value;
+  int canon;      // reproduce masking.py:192's `+ 0.0` (b > 0 and some window fits)
+  ModeP mp;
+};
+
+// Until (timed [a,b] and untimed).
+struct UParams {
+  DExpr left, right;
+  const float* out_in;
+  const float* cot;
+  float* out;
+  float* gl;  // backward scratch: cotangent of the left child  [B, L]
+  float* gr;  // backward scratch: cotangent of the right child [B, L]
+  long long B, L;
+  int a, b, K;
+  int untimed;
+  int pad_last;
+  float pad_value;
+  int canon;
+  ModeP mp;
+};
+
+// Smooth-interval F / G (weighted window of length L over the padded child).
+struct SParams {
+  DExpr child;
+  const float* out_in;
+  const float* cot;
+  float* out;
+  const double* w;    // weights w_i, i = 0..L-1 (fp64)
+  const float* lw;    // log-weights ln w_i (fp32; -inf where w_i == 0)
+  float* dw;          // backward: per-weight gradient partial sums [n_part, L] (fp32)
+  double* dw64;       // backward: reduced d/dw_i (fp64) [L]
+  float* gbuf;        // backward scratch: cotangent of the child [B, L]
+  long long B, L;
+  int i_lo, i_hi;     // kept index range {i : w_i > 0}
+  float sg;
+  int pad_last;
+  float pad_value;
+  ModeP mp;
+};
+
+// launchers (return cudaError_t)
+cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st);
+cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cudaStream_t st);
+cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st);
+cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st);
+cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st);
+cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st);
+cudaError_t launch_until_fwd(int mode, UParams& p, cudaStream_t st);
+cudaError_t launch_until_bwd(int mode, UParams& p, cudaStream_t st);
+cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st);
+cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st);
+
+// launch accounting (exec.cu)
+void count_launch(int n = 1);
+
+}  // namespace stlg

@@ -1,0 +1,166 @@
+"""Device path (libstlg.so via the public API) against the reference and the oracle.
+
+Tolerances (BASELINE.json north star):
+  * hard mode: trace bit-exact against float32(reference), including signed
+    zeros; gradients exact for the ones cotangent (they are small integers),
+    1e-6 relative otherwise (fp32 sums of fp32 cotangents);
+  * smooth modes (LSE / softmax): |gpu - ref| / max(1, |ref|) <= 1e-5 for the
+    trace and every gradient (the reference's own FD convention,
+    autodiff.py:126).
+"""
+
+import numpy as np
+import pytest
+
+import golden_io
+import stl_oracle
+from devhelp import assert_hard_equal, device_supports, rel_err, run_device
+
+import paper_2501_04194_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+SMOOTH_TOL = 1e-5
+CASES = [c for c in golden_io.load_all()]
+
+
+def _check(case_mode, tr, g, ref_tr, ref_g, cot, dabc=None, ref_dabc=None):
+    if case_mode == "Hard":
+        assert_hard_equal(tr, np.asarray(ref_tr).astype(np.float32))
+        ones = np.all(np.asarray(cot) == 1.0)
+        for k in ref_g:
+            if ones:
+                np.testing.assert_array_equal(g[k], ref_g[k])
+            else:
+                assert rel_err(g[k], ref_g[k]) <= 1e-6, k
+    else:
+        assert rel_err(tr, ref_tr) <= SMOOTH_TOL
+        for k in ref_g:
+            assert rel_err(g[k], ref_g[k]) <= SMOOTH_TOL, (k, rel_err(g[k], ref_g[k]))
+    if ref_dabc is not None:
+        assert rel_err(dabc, ref_dabc) <= SMOOTH_TOL, (dabc, ref_dabc)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_golden_reference_vectors(cuda, case):
+    if not device_supports(case.formula, case.cfg):
+        pytest.skip("operator not on the device path in this build")
+    binding = (case.si.a, case.si.b, case.si.c) if case.dabc is not None else None
+    tr, g, dabc = run_device(case.formula, case.arrays, case.cfg, case.cot, binding)
+    _check(case.mode, tr, g, case.trace, case.grads, case.cot, dabc, case.dabc)
+
+
+# --- random corpus at moderate sizes against the oracle --------------------------
+
+def _rand_formula(rng, depth, chans=("x", "y"), until_ok=True, max_a=40, max_w=120):
+    ops = ["pred", "not", "and", "or", "F", "G"] + (["U"] if until_ok else [])
+    w = np.array([0.3, 0.08, 0.12, 0.12, 0.14, 0.14] + ([0.1] if until_ok else []))
+    op = "pred" if depth == 0 else rng.choice(ops, p=w / w.sum())
+
+    def iv():
+        if rng.random() < 0.3:
+            return None
+        a = int(rng.integers(0, max_a))
+        return P.StepInterval(a, a + int(rng.integers(0, max_w)))
+    if op == "pred":
+        if rng.random() < 0.05:
+            return P.TRUE
+        return P.Pred(str(rng.choice(chans)), str(rng.choice([">", "<"])),
+                      float(np.float32(rng.normal(0, 1))))
+    if op == "not":
+        return P.Not(_rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w))
+    if op in ("and", "or"):
+        cls = P.And if op == "and" else P.Or
+        return cls(_rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w),
+                   _rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w))
+    if op in ("F", "G"):
+        cls = P.Eventually if op == "F" else P.Always
+        return cls(_rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w), iv())
+    return P.Until(_rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w),
+                   _rand_formula(rng, depth - 1, chans, until_ok, max_a, max_w), iv())
+
+
+MODES = [P.Hard(), P.LogSumExp(1.0), P.LogSumExp(10.0), P.SoftMax(3.0)]
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_formulas_vs_oracle(cuda, seed):
+    rng = np.random.default_rng(1000 + seed)
+    mode = MODES[seed % len(MODES)]
+    pad = P.PaddingPolicy.last_value() if seed % 3 else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(mode=mode, padding=pad, top_value=100.0)
+    f = _rand_formula(rng, int(rng.integers(1, 4)))
+    if not device_supports(f, cfg):
+        pytest.skip("operator not on the device path in this build")
+    B, L = 3, int(rng.integers(20, 400))
+    arrays = {c: np.asarray(rng.normal(0, 1.5, (B, L)), dtype=np.float32).astype(np.float64)
+              for c in ("x", "y")}
+    cot = np.ones((B, L)) if seed % 2 == 0 else \
+        np.asarray(rng.normal(0, 1, (B, L)), dtype=np.float32).astype(np.float64)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, arrays, cfg, cot)
+    tr, g, _ = run_device(f, arrays, cfg, cot)
+    _check(type(mode).__name__, tr, {k: g[k] for k in ref_g}, ref_tr, ref_g, cot)
+
+
+# --- headline shapes: full size on device, rows sampled for the oracle ----------------
+
+def _walk(B, T, seed):
+    rng = np.random.default_rng(seed)
+    p0 = rng.uniform(-1, 1, (B, 1, 2))
+    p = p0 + np.cumsum(0.05 * rng.normal(0, 1, (B, T, 2)), axis=1)
+    return np.asarray(p, dtype=np.float32)
+
+
+@pytest.mark.parametrize("mode", [P.LogSumExp(10.0), P.Hard(), P.SoftMax(10.0)])
+def test_c2_full_size_rows_vs_oracle(cuda, mode):
+    import torch
+    B, T = 1024, 10_000
+    p = _walk(B, T, 1)
+    f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
+    cfg = P.SemanticsConfig(mode=mode)
+    dev = torch.device("cuda", 0)
+    pt = torch.tensor(p, device=dev)
+    px = pt[..., 0].clone().requires_grad_(True)
+    py = pt[..., 1].clone().requires_grad_(True)
+    out = P.trace(f, {"px": px, "py": py}, cfg)
+    out.backward(torch.ones_like(out))
+    rows = [0, 517, 1023]
+    for r in rows:
+        arrays = {"px": p[r:r + 1, :, 0].astype(np.float64), "py": p[r:r + 1, :, 1].astype(np.float64)}
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, arrays, cfg)
+        tr = out[r:r + 1].detach().double().cpu().numpy()
+        assert rel_err(tr, ref_tr) <= SMOOTH_TOL
+        assert rel_err(px.grad[r:r + 1].double().cpu().numpy(), ref_g["px"]) <= SMOOTH_TOL
+        assert rel_err(py.grad[r:r + 1].double().cpu().numpy(), ref_g["py"]) <= SMOOTH_TOL
+
+
+def test_hard_window_full_size_bit_exact(cuda):
+    import torch
+    B, T = 1024, 10_000
+    rng = np.random.default_rng(5)
+    x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    f = P.Eventually(P.Pred("x", ">", 0.5), P.StepInterval(10, 100))
+    xt = torch.tensor(x, device="cuda").requires_grad_(True)
+    out = P.trace(f, {"x": xt}, P.SemanticsConfig())
+    out.backward(torch.ones_like(out))
+    for r in (0, 333, 1023):
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x[r:r + 1].astype(np.float64)},
+                                                     P.SemanticsConfig())
+        assert_hard_equal(out[r:r + 1].detach().cpu().numpy(), ref_tr.astype(np.float32))
+        np.testing.assert_array_equal(xt.grad[r:r + 1].cpu().numpy(), ref_g["x"])
+    # size-independent property: the ones-cotangent gradient of a hard window
+    # sums to the number of outputs per row (each output routes one unit)
+    assert torch.all(xt.grad.sum(dim=1) == T)
+
+
+def test_duality_exact_on_device(cuda):
+    """G(phi) == -F(~phi) bit for bit (test_masking.py:255-268), full-size batch."""
+    import torch
+    rng = np.random.default_rng(7)
+    x = torch.tensor(np.asarray(rng.normal(0, 1, (256, 4000)), dtype=np.float32), device="cuda")
+    for mode in (P.Hard(), P.LogSumExp(4.0)):
+        cfg = P.SemanticsConfig(mode=mode)
+        for iv in (P.StepInterval(3, 40), None):
+            a = P.trace(P.Always(P.Pred("x", ">", 0.2), iv), {"x": x}, cfg)
+            b = P.trace(P.Eventually(P.Not(P.Pred("x", ">", 0.2)), iv), {"x": x}, cfg)
+            assert torch.equal(a, -b)

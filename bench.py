@@ -224,7 +224,6 @@ def run_b200(args, rank, world):
         comp.forward([d["px"], d["py"]], params, d["out"], fws, sptr)
         if ev:
             ev[1].record(stream)
-        d["dp"].zero_()
         comp.backward([d["px"], d["py"]], params, d["out"], ones,
                       [d["dp"][..., 0], d["dp"][..., 1]], None, fws, bws, sptr)
         if ev:

@@ -112,9 +112,12 @@ typedef struct stlg_channel {
 } stlg_channel;
 
 typedef struct stlg_grad {
-  float* ptr;          /* accumulated into (+=); caller zero-fills  */
+  float* ptr;
   int64_t row_stride;
   int64_t elem_stride;
+  int32_t accumulate;  /* 1: add into the existing contents (+=);
+                          0: overwrite — every element is written (zeros where the
+                          formula does not depend on it); no zero-fill needed */
 } stlg_grad;
 
 /* per-call parameters of smooth-interval node slot s: a, b, c, eps (fp64) */

@@ -44,7 +44,8 @@ class StlgChannel(ctypes.Structure):
 
 
 class StlgGrad(ctypes.Structure):
-    _fields_ = [("ptr", c_void_p), ("row_stride", c_int64), ("elem_stride", c_int64)]
+    _fields_ = [("ptr", c_void_p), ("row_stride", c_int64), ("elem_stride", c_int64),
+                ("accumulate", c_int32)]
 
 
 class StlgSmooth(ctypes.Structure):

@@ -40,7 +40,9 @@ struct DDst {
 // value = s_out * x                (LEAF_SRC:    a materialised trace, no rounding step)
 // value = c                        (LEAF_CONST:  +/- top_value, masking.py:316-318)
 struct DLeaf {
-  int kind, src, src2, pad_;
+  int kind, src, src2;
+  int st1, st2;  // gradient write of src / src2: 1 = store (first writer), 0 = accumulate
+  int pad_;
   float s_in, s_out, c, cx, cy, pad2_;
 };
 struct DStep {
@@ -103,10 +105,11 @@ __device__ __forceinline__ float leaf_val(const DExpr& e, const DLeaf& L, long l
   return L.s_out * t;
 }
 
-__device__ __forceinline__ void acc_dst(const DDst& d, long long b, long long j, float g) {
+__device__ __forceinline__ void acc_dst(const DDst& d, long long b, long long j, float g, int st) {
   if (d.p != nullptr) {
     float* q = d.p + b * d.rs + j * d.es;
-    *q += g;
+    if (st) *q = g;
+    else *q += g;
   }
 }
 
@@ -114,20 +117,20 @@ __device__ __forceinline__ void leaf_vjp(const DExpr& e, const DLeaf& L, long lo
                                          float g) {
   if (L.kind == LEAF_CONST) return;
   if (L.kind == LEAF_SRC) {
-    acc_dst(e.dst[L.src], b, j, g * L.s_out);
+    acc_dst(e.dst[L.src], b, j, g * L.s_out, L.st1);
     return;
   }
   float gx = g * L.s_out * L.s_in;
   if (L.kind == LEAF_AFFINE) {
-    acc_dst(e.dst[L.src], b, j, gx);
+    acc_dst(e.dst[L.src], b, j, gx, L.st1);
     return;
   }
   float dx = ld_src(e.src[L.src], b, j) - L.cx;
   float dy = ld_src(e.src[L.src2], b, j) - L.cy;
   float d = sqrtf(fmaf(dx, dx, dy * dy));
   float inv = d > 0.f ? 1.f / d : 0.f;
-  acc_dst(e.dst[L.src], b, j, gx * dx * inv);
-  acc_dst(e.dst[L.src2], b, j, gx * dy * inv);
+  acc_dst(e.dst[L.src], b, j, gx * dx * inv, L.st1);
+  acc_dst(e.dst[L.src2], b, j, gx * dy * inv, L.st2);
 }
 
 // Two-element reduction (And / Or), masking.py:326-330 -> tape.smooth_max/min.
@@ -182,7 +185,6 @@ __device__ __forceinline__ float expr_eval(const DExpr& e, long long b, long lon
 template <int MODE>
 __device__ __forceinline__ void expr_vjp(const DExpr& e, long long b, long long j, float g,
                                          const ModeP& mp) {
-  if (g == 0.f) return;
   if (e.n_step == 1) {
     leaf_vjp(e, e.leaf[0], b, j, g);
     return;
@@ -203,9 +205,9 @@ __device__ __forceinline__ void expr_vjp(const DExpr& e, long long b, long long 
   for (int k = e.n_step - 1; k >= 0; --k) {
     DStep s = e.step[k];
     float a = adj[k];
-    if (a == 0.f) continue;
     if (s.op == ST_LEAF) {
-      leaf_vjp(e, e.leaf[s.a], b, j, a);
+      const DLeaf& L = e.leaf[s.a];
+      if (a != 0.f || L.st1 || L.st2) leaf_vjp(e, L, b, j, a);
     } else {
       adj[s.a] += a * w1[k];
       adj[s.b] += a * w2[k];
@@ -296,5 +298,191 @@ __device__ __forceinline__ GSoft gsoft_comb(GSoft x, GSoft y, float tau2) {
   float f = ex2f(tau2 * (x.mu - y.mu));
   return {x.mu, fmaf(y.A, f, x.A), fmaf(f, fmaf(y.c - x.c, y.A, y.Bc), x.Bc), x.c};
 }
+
+
+// ---------------------------------------------------------------------------
+// branch-free single-MUFU monoid updates (used by the v2 window kernels)
+// ---------------------------------------------------------------------------
+// LSE state (m, s): s = sum exp(tau (u - m)); push one sample u.
+__device__ __forceinline__ void lse_add(float& m, float& s, float u, float tau2) {
+  float d = u - m;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool up = d > 0.f;
+  s = up ? fmaf(s, e, 1.f) : s + e;
+  m = up ? u : m;
+}
+// merge (m2, s2) into (m, s)
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2, float tau2) {
+  float d = m2 - m;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool up = d > 0.f;
+  s = up ? fmaf(s, e, s2) : fmaf(s2, e, s);
+  m = up ? m2 : m;
+}
+// softmax state (m, s, q): q = sum (u - m) exp(tau (u - m)); value m + q / s
+__device__ __forceinline__ void soft_add(float& m, float& s, float& q, float u, float tau2) {
+  float d = u - m;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool up = d > 0.f;
+  float s_up = fmaf(s, e, 1.f), q_up = e * fmaf(-d, s, q);
+  float s_dn = s + e, q_dn = fmaf(d, e, q);
+  s = up ? s_up : s_dn;
+  q = up ? q_up : q_dn;
+  m = up ? u : m;
+}
+__device__ __forceinline__ void soft_merge(float& m, float& s, float& q, float m2, float s2, float q2,
+                                           float tau2) {
+  float d = m2 - m;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool up = d > 0.f;
+  float s_up = fmaf(s, e, s2), q_up = fmaf(e, fmaf(-d, s, q), q2);
+  float s_dn = fmaf(s2, e, s), q_dn = fmaf(e, fmaf(d, s2, q2), q);
+  s = up ? s_up : s_dn;
+  q = up ? q_up : q_dn;
+  m = up ? m2 : m;
+}
+// backward window sums (gather form), state (mu, A): sum_t A_t exp(-tau (mu_t - mu)), mu = min
+__device__ __forceinline__ void gl_add(float& mu, float& A, float mu2, float A2, float tau2) {
+  float d = mu2 - mu;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool dn = d < 0.f;
+  float A_new = dn ? fmaf(A, e, A2) : fmaf(A2, e, A);
+  float mu_new = dn ? mu2 : mu;
+  bool skip = A2 == 0.f, empty = A == 0.f;
+  A = skip ? A : (empty ? A2 : A_new);
+  mu = skip ? mu : (empty ? mu2 : mu_new);
+}
+// softmax backward state (mu, A, Bc, c): Bc = sum A_t w_t (M_t - c), re-centred on the min-mu term
+__device__ __forceinline__ void gs_add(float& mu, float& A, float& Bc, float& c, float mu2, float A2,
+                                       float B2, float c2, float tau2) {
+  bool skip = (A2 == 0.f && B2 == 0.f), empty = (A == 0.f && Bc == 0.f);
+  float d = mu2 - mu;
+  float e = ex2f(-tau2 * fabsf(d));
+  bool dn = d < 0.f;
+  // dn: the new term dominates (reference c2); else keep c
+  float A_dn = fmaf(A, e, A2), B_dn = fmaf(e, fmaf(c - c2, A, Bc), B2);
+  float A_up = fmaf(A2, e, A), B_up = fmaf(e, fmaf(c2 - c, A2, B2), Bc);
+  float nA = dn ? A_dn : A_up, nB = dn ? B_dn : B_up, nmu = dn ? mu2 : mu, nc = dn ? c2 : c;
+  A = skip ? A : (empty ? A2 : nA);
+  Bc = skip ? Bc : (empty ? B2 : nB);
+  mu = skip ? mu : (empty ? mu2 : nmu);
+  c = skip ? c : (empty ? c2 : nc);
+}
+
+// ---------------------------------------------------------------------------
+// evaluators: EK_LEAF hoists a single-leaf expression into registers (the
+// common case: Pred / NormPred / a materialised trace under a temporal op);
+// EK_GEN interprets any fused expression.
+// ---------------------------------------------------------------------------
+enum ExprKind { EK_GEN = 0, EK_LEAF = 1 };
+
+template <int MODE, int EK>
+struct Ev;
+
+template <int MODE>
+struct Ev<MODE, EK_LEAF> {
+  struct Raw {
+    float x, y;
+  };
+  const float* p1;
+  const float* p2;
+  long long es1, es2;
+  float* g1;
+  float* g2;
+  long long ges1, ges2;
+  int kind, st1, st2;
+  float s_in, s_out, c, cx, cy;
+
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) {
+    const DLeaf& L = e.leaf[0];
+    kind = L.kind;
+    st1 = L.st1;
+    st2 = L.st2;
+    s_in = L.s_in;
+    s_out = L.s_out;
+    c = L.c;
+    cx = L.cx;
+    cy = L.cy;
+    p1 = p2 = nullptr;
+    g1 = g2 = nullptr;
+    es1 = es2 = ges1 = ges2 = 0;
+    if (kind != LEAF_CONST) {
+      const DSrc& s = e.src[L.src];
+      p1 = s.p + row * s.rs;
+      es1 = s.es;
+      const DDst& d = e.dst[L.src];
+      if (d.p) {
+        g1 = d.p + row * d.rs;
+        ges1 = d.es;
+      }
+    }
+    if (kind == LEAF_NORM) {
+      const DSrc& s = e.src[L.src2];
+      p2 = s.p + row * s.rs;
+      es2 = s.es;
+      const DDst& d = e.dst[L.src2];
+      if (d.p) {
+        g2 = d.p + row * d.rs;
+        ges2 = d.es;
+      }
+    }
+  }
+  __device__ __forceinline__ Raw load(long long j) const {
+    Raw r{0.f, 0.f};
+    if (kind != LEAF_CONST) r.x = __ldg(p1 + j * es1);
+    if (kind == LEAF_NORM) r.y = __ldg(p2 + j * es2);
+    return r;
+  }
+  __device__ __forceinline__ float value(long long, Raw r) const {
+    if (kind == LEAF_CONST) return c;
+    if (kind == LEAF_SRC) return s_out * r.x;
+    float x = r.x;
+    if (kind == LEAF_NORM) {
+      float dx = r.x - cx, dy = r.y - cy;
+      x = sqrtf(fmaf(dx, dx, dy * dy));
+    }
+    return s_out * __fadd_rn(s_in * x, c);
+  }
+  __device__ __forceinline__ static void put(float* p, long long es, long long j, float g, int st) {
+    if (p) {
+      float* q = p + j * es;
+      if (st) *q = g;
+      else *q += g;
+    }
+  }
+  __device__ __forceinline__ void grad(long long j, Raw r, float g) const {
+    if (kind == LEAF_CONST) return;
+    if (kind == LEAF_SRC) {
+      put(g1, ges1, j, g * s_out, st1);
+      return;
+    }
+    float gx = g * s_out * s_in;
+    if (kind == LEAF_AFFINE) {
+      put(g1, ges1, j, gx, st1);
+      return;
+    }
+    float dx = r.x - cx, dy = r.y - cy;
+    float d = sqrtf(fmaf(dx, dx, dy * dy));
+    float inv = d > 0.f ? gx / d : 0.f;
+    put(g1, ges1, j, dx * inv, st1);
+    put(g2, ges2, j, dy * inv, st2);
+  }
+};
+
+template <int MODE>
+struct Ev<MODE, EK_GEN> {
+  struct Raw {};
+  const DExpr* e;
+  long long row;
+  ModeP mp;
+  __device__ __forceinline__ Ev(const DExpr& ex, long long r, const ModeP& m) : e(&ex), row(r), mp(m) {}
+  __device__ __forceinline__ Raw load(long long) const { return Raw{}; }
+  __device__ __forceinline__ float value(long long j, Raw) const {
+    return expr_eval<MODE>(*e, row, j, mp);
+  }
+  __device__ __forceinline__ void grad(long long j, Raw, float g) const {
+    expr_vjp<MODE>(*e, row, j, g, mp);
+  }
+};
 
 }  // namespace stlg

@@ -44,6 +44,7 @@ struct HLeaf {
   int kind;
   int src, src2;  // global source ids: [0, n_ch) channels, n_ch + s slots
   float s_in, s_out, c, cx, cy;
+  int st1 = 0, st2 = 0;  // first writer of the gradient of src / src2 in backward order
 };
 struct HExpr {
   std::vector<HLeaf> leaf;
@@ -73,6 +74,7 @@ struct stlg_plan {
   int n_ch = 0, n_smooth = 0, n_slots = 0, n_aux = 0;
   int root_temporal = 0;
   std::vector<Entry> entries;
+  std::vector<int> ch_touched;  // channel referenced by some leaf (else zero-filled on overwrite)
 };
 
 namespace stlg {
@@ -185,6 +187,35 @@ struct Compiler {
   }
 };
 
+// Backward runs the entries in reverse; inside a kernel the left expression's
+// VJP runs before the right one's, and a generic expression visits its leaves
+// in reverse step order.  The first leaf (in that order) to write a gradient
+// destination stores; later ones accumulate.  Every VJP kernel writes every
+// element of its destinations, so stored buffers need no zero-fill.
+void mark_first_writers(stlg_plan* plan) {
+  std::map<int, bool> touched;
+  auto visit = [&](HExpr& ex) {
+    for (int k = (int)ex.step.size() - 1; k >= 0; --k) {
+      if (ex.step[k].op != ST_LEAF) continue;
+      HLeaf& lf = ex.leaf[ex.step[k].a];
+      if (lf.kind == LEAF_CONST) continue;
+      lf.st1 = touched[lf.src] ? 0 : 1;
+      touched[lf.src] = true;
+      if (lf.kind == LEAF_NORM) {
+        lf.st2 = touched[lf.src2] ? 0 : 1;
+        touched[lf.src2] = true;
+      }
+    }
+  };
+  for (auto it = plan->entries.rbegin(); it != plan->entries.rend(); ++it) {
+    visit(it->e1);
+    if (it->kind == E_UNTIL) visit(it->e2);
+  }
+  plan->ch_touched.assign(plan->n_ch, 0);
+  for (auto& kv : touched)
+    if (kv.first < plan->n_ch) plan->ch_touched[kv.first] = 1;
+}
+
 int validate_nodes(const stlg_node* nodes, int n, int n_ch, int n_smooth) {
   if (n <= 0) return fail(STLG_E_INVALID, "empty node program");
   for (int i = 0; i < n; ++i) {
@@ -285,6 +316,12 @@ int resolve(const stlg_plan* p, const HExpr& h, const stlg_channel* ch, const st
     o.c = lf.c;
     o.cx = lf.cx;
     o.cy = lf.cy;
+    auto may_store = [&](int gid) {
+      if (gid >= p->n_ch) return true;  // slot cotangents: owned by the library
+      return dch != nullptr && dch[gid].ptr != nullptr && dch[gid].accumulate == 0;
+    };
+    o.st1 = (with_dst && lf.kind != LEAF_CONST && lf.st1 && may_store(lf.src)) ? 1 : 0;
+    o.st2 = (with_dst && lf.kind == LEAF_NORM && lf.st2 && may_store(lf.src2)) ? 1 : 0;
     if (lf.kind != LEAF_CONST) {
       o.src = map_src(lf.src);
       if (o.src < 0) return fail(STLG_E_INVALID, "too many sources");
@@ -362,6 +399,8 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
       e.kind = E_UNTIL;
     } else if (nd.itv_kind == STLG_ITV_SMOOTH) {
       e.kind = E_FG_SMOOTH;
+      delete plan;
+      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
     } else {
       e.kind = e.untimed ? E_FG_UNTIMED : E_FG_TIMED;
     }
@@ -403,6 +442,7 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
         return fail(STLG_E_UNSUPPORTED, "masked_fill is not supported on the device path yet");
       }
   }
+  mark_first_writers(plan);
   *out_plan = plan;
   return STLG_OK;
 }
@@ -536,9 +576,12 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int mode = plan->cfg.mode;
-  if (plan->n_slots > 0) {
-    cudaError_t ce = cudaMemsetAsync(bf.gslots, 0, sizeof(float) * (size_t)plan->n_slots * bf.BT, st);
-    if ((rc = cuda_status(ce, "memset"))) return rc;
+  for (int c = 0; c < plan->n_ch && d_channels; ++c) {
+    const stlg_grad& g = d_channels[c];
+    if (g.ptr && !g.accumulate && !plan->ch_touched[c]) {
+      cudaError_t ce = launch_fill_strided(g.ptr, B, T, g.row_stride, g.elem_stride, 0.f, st);
+      if ((rc = cuda_status(ce, "zero-fill"))) return rc;
+    }
   }
   for (auto it = plan->entries.rbegin(); it != plan->entries.rend(); ++it) {
     const Entry& e = *it;

@@ -53,6 +53,25 @@ __global__ void __launch_bounds__(256) k_pointwise_vjp(const __grid_constant__ F
   }
 }
 
+__global__ void k_fill_strided(float* p, long long B, long long T, long long rs, long long es,
+                               float v) {
+  const long long n = B * T;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / T, t = i - b * T;
+    p[b * rs + t * es] = v;
+  }
+}
+
+static int grid_for(long long n, int threads);
+
+cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs, long long es,
+                                float v, cudaStream_t st) {
+  k_fill_strided<<<grid_for(B * T, 256), 256, 0, st>>>(p, B, T, rs, es, v);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   long long cap = 148LL * 16;
@@ -80,349 +99,448 @@ cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cu
 // ===========================================================================
 // timed F / G — forward (vHGW)
 // ===========================================================================
-// shared layout: NB blocks, row stride Kp (odd => conflict-free per-thread walks)
-//   u[NB*Kp]                 child in max space; overwritten in place by outputs
-//   P0, P1 [, P2]            prefix states (hard: value, index; lse: m, s; soft: m, s, d)
-//   AX (soft)                window LSE (aux output)
-template <int MODE>
-__global__ void __launch_bounds__(256) k_fg_timed_fwd(const __grid_constant__ FGParams p) {
+// Shared layout: NB blocks of K samples, row stride Kp = K | 1 (odd, so the
+// per-thread block walks are bank-conflict free):
+//   U  [NB*Kp]  child in max space; overwritten in place by the outputs
+//   P1 [NB*Kp]  prefix state: hard = running max; lse = log-domain prefix LSE;
+//               soft = prefix softmax value M
+//   P2 [NB*Kp]  soft: prefix LSE L
+//   AX [NB*Kp]  soft: window LSE (aux output for the backward)
+// Loads and stores run warp-per-block (coalesced, no integer division);
+// the scans run one thread per block.
+constexpr int FG_THREADS = 256;
+
+template <int MODE, int EK>
+__global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float padv_sh;
   const int NB = p.NB, K = p.K, Kp = p.Kp;
+  const int nsm = NB * Kp;
   const long long row = blockIdx.y, L = p.L;
   const long long J = (long long)(NB - 1) * K;
   const long long t0 = (long long)blockIdx.x * J;
   const long long nvalid = L - p.b;
   const long long s0 = t0 + p.a;
-  const int nsm = NB * Kp;
-  float* u = sm;
-  float* P0 = sm + nsm;
-  float* P1 = sm + 2 * nsm;
-  float* P2 = sm + 3 * nsm;
-  float* AX = sm + 4 * nsm;
-  const float tau2 = p.mp.tau2;
+  float* U = sm;
+  float* P1 = sm + nsm;
+  float* P2 = sm + 2 * nsm;
+  float* AX = sm + 3 * nsm;
+  const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  Ev<MODE, EK> ev(p.child, row, p.mp);
   const bool any = t0 < nvalid;
 
-  if (threadIdx.x == 0)
-    padv_sh = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+  if (threadIdx.x == 0) padv_sh = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   if (any) {
-    const int n = NB * K;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      int blk = i / K, off = i - blk * K;
-      long long idx = s0 + i;
-      u[blk * Kp + off] = idx < L ? p.sg * expr_eval<MODE>(p.child, row, idx, p.mp) : -INFINITY;
+    for (int blk = warp; blk < NB; blk += nw) {
+      const long long base = s0 + (long long)blk * K;
+      float* ub = U + blk * Kp;
+      for (int o0 = 0; o0 < K; o0 += 128) {
+        typename Ev<MODE, EK>::Raw r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int off = o0 + lane + 32 * k;
+          long long idx = base + off;
+          if (off < K && idx < L) r[k] = ev.load(idx);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int off = o0 + lane + 32 * k;
+          long long idx = base + off;
+          if (off < K) ub[off] = idx < L ? sg * ev.value(idx, r[k]) : -INFINITY;
+        }
+      }
     }
   }
   __syncthreads();
   if (any && threadIdx.x < NB) {  // prefix scan of own block
-    const int base = threadIdx.x * Kp;
+    const float* u = U + threadIdx.x * Kp;
+    float* q1 = P1 + threadIdx.x * Kp;
     if (MODE == M_HARD) {
-      float bv = u[base];
-      P0[base] = bv;
+      float bv = u[0];
+      q1[0] = bv;
+#pragma unroll 4
       for (int i = 1; i < K; ++i) {
-        float x = u[base + i];
-        if (x > bv) bv = x;
-        P0[base + i] = bv;
+        float x = u[i];
+        bv = (x > bv) ? x : bv;
+        q1[i] = bv;
       }
     } else if (MODE == M_LSE) {
-      LseAcc a = {u[base], 1.f};
-      P0[base] = a.m;
-      P1[base] = a.s;
+      float m = u[0], s = 1.f;
+      q1[0] = m;
+#pragma unroll 4
       for (int i = 1; i < K; ++i) {
-        a = lse_push(a, u[base + i], tau2);
-        P0[base + i] = a.m;
-        P1[base + i] = a.s;
+        lse_add(m, s, u[i], tau2);
+        q1[i] = fmaf(lg2f(s), itau2, m);
       }
     } else {
-      SoftAcc a = {u[base], 1.f, 0.f};
-      P0[base] = a.m;
-      P1[base] = a.s;
-      P2[base] = a.d;
+      float* q2 = P2 + threadIdx.x * Kp;
+      float m = u[0], s = 1.f, q = 0.f;
+      q1[0] = m;
+      q2[0] = m;
+#pragma unroll 2
       for (int i = 1; i < K; ++i) {
-        a = soft_push(a, u[base + i], tau2);
-        P0[base + i] = a.m;
-        P1[base + i] = a.s;
-        P2[base + i] = a.d;
+        soft_add(m, s, q, u[i], tau2);
+        q1[i] = m + q / s;
+        q2[i] = fmaf(lg2f(s), itau2, m);
       }
     }
   }
   __syncthreads();
-  if (any && threadIdx.x < NB - 1) {  // suffix walk + combine with next block's prefix
-    const int base = threadIdx.x * Kp, nb = base + Kp;
+  if (any && threadIdx.x < NB - 1) {  // suffix walk + combine with the next block's prefix
+    float* u = U + threadIdx.x * Kp;
+    const float* n1 = P1 + (threadIdx.x + 1) * Kp - 1;  // n1[i] = next block prefix at i-1
     if (MODE == M_HARD) {
-      float acc = -INFINITY;
+      float acc = u[K - 1];
+#pragma unroll 4
       for (int i = K - 1; i >= 0; --i) {
-        float x = u[base + i];
-        if (x >= acc) acc = x;  // value only; ties keep the earlier element (same value)
+        float x = u[i];
+        acc = (x >= acc) ? x : acc;  // walking backwards: ties keep the earlier sample
         float r = acc;
         if (i > 0) {
-          float pv = P0[nb + i - 1];
-          if (pv > r) r = pv;
+          float pv = n1[i];
+          r = (pv > r) ? pv : r;
         }
-        u[base + i] = r;
+        u[i] = r;
       }
     } else if (MODE == M_LSE) {
-      LseAcc acc = {0.f, 0.f};
+      float m = u[K - 1], s = 1.f;
+#pragma unroll 4
       for (int i = K - 1; i >= 0; --i) {
-        acc = lse_push(acc, u[base + i], tau2);
-        LseAcc r = acc;
-        if (i > 0) r = lse_comb(acc, LseAcc{P0[nb + i - 1], P1[nb + i - 1]}, tau2);
-        u[base + i] = fmaf(lg2f(r.s), p.mp.inv_tau2, r.m);
+        if (i < K - 1) lse_add(m, s, u[i], tau2);
+        float mm = m, ss = s;
+        if (i > 0) lse_merge(mm, ss, n1[i], 1.f, tau2);
+        u[i] = fmaf(lg2f(ss), itau2, mm);
       }
     } else {
-      SoftAcc acc = {0.f, 0.f, 0.f};
+      const float* n2 = P2 + (threadIdx.x + 1) * Kp - 1;
+      float* ax = AX + threadIdx.x * Kp;
+      float m = u[K - 1], s = 1.f, q = 0.f;
+#pragma unroll 2
       for (int i = K - 1; i >= 0; --i) {
-        acc = soft_push(acc, u[base + i], tau2);
-        SoftAcc r = acc;
-        if (i > 0) r = soft_comb(acc, SoftAcc{P0[nb + i - 1], P1[nb + i - 1], P2[nb + i - 1]}, tau2);
-        u[base + i] = r.m + r.d / r.s;
-        AX[base + i] = fmaf(lg2f(r.s), p.mp.inv_tau2, r.m);
+        if (i < K - 1) soft_add(m, s, q, u[i], tau2);
+        float mm = m, ss = s, qq = q;
+        if (i > 0) {
+          float Lp = n2[i];
+          soft_merge(mm, ss, qq, Lp, 1.f, n1[i] - Lp, tau2);
+        }
+        u[i] = mm + qq / ss;
+        ax[i] = fmaf(lg2f(ss), itau2, mm);
       }
     }
   }
   __syncthreads();
-  const long long tend = t0 + J < L ? t0 + J : L;
   const float padv = padv_sh;
-  for (long long t = t0 + threadIdx.x; t < tend; t += blockDim.x) {
-    int i = (int)(t - t0);
-    int blk = i / K, off = i - blk * K;
-    float v = (t < nvalid) ? p.sg * u[blk * Kp + off] : padv;
-    if (p.canon) v = __fadd_rn(v, 0.f);
-    p.out[row * L + t] = v;
-    if (MODE == M_SOFT && t < nvalid) p.aux[row * L + t] = AX[blk * Kp + off];
+  for (int blk = warp; blk < NB - 1; blk += nw) {
+    for (int off = lane; off < K; off += 32) {
+      long long t = t0 + (long long)blk * K + off;
+      if (t >= L) break;
+      float v = (t < nvalid) ? sg * U[blk * Kp + off] : padv;
+      if (p.canon) v = __fadd_rn(v, 0.f);
+      p.out[row * L + t] = v;
+      if (MODE == M_SOFT && t < nvalid) p.aux[row * L + t] = AX[blk * Kp + off];
+    }
   }
 }
 
 // ===========================================================================
 // timed F / G — backward, LSE and softmax (window sum over the cotangent)
 // ===========================================================================
-// CTA owns child elements j in [j0, j0 + J); it needs outputs t in
-// [j0 - b, j0 + J - 1 - a] (NB blocks of K).  h_t = (mu_t, g_t [, Bc]) with
-//   LSE:  mu_t = M_t (u-space output);           g_child[j] = A e^{tau (u_j - mu)}
-//   soft: mu_t = L_t (window LSE), c_t = M_t;     g_child[j] = e^{tau (u_j - mu)} (A (1 + tau (u_j - c)) - tau Bc)
-template <int MODE>
-__global__ void __launch_bounds__(256) k_fg_timed_bwd_smooth(const __grid_constant__ FGParams p) {
+// The CTA owns child elements j in [j0, j0 + J), J = (NB-1) K; element j
+// receives from outputs t in [j - b, j - a], a window of K over the output
+// sequence starting at tb = j0 - b.  Shared layout (stride Kp):
+//   LSE:  HM = M_t (u-space output), HG = g_t; prefix PM, PA
+//   soft: HM = L_t (window LSE), HG = g_t, HC = M_t; prefix PM, PA, PB, PC
+// Gradient: LSE  g_child[j] = sum_t g_t exp(tau (u_j - M_t))
+//           soft g_child[j] = sum_t g_t exp(tau (u_j - L_t)) (1 + tau (u_j - M_t))
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
+template <int MODE, int EK>
+__global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red_sh[32];
-  __shared__ float padsum_sh;
   const int NB = p.NB, K = p.K, Kp = p.Kp;
+  const int nsm = NB * Kp;
   const long long row = blockIdx.y, L = p.L;
   const long long J = (long long)(NB - 1) * K;
   const long long j0 = (long long)blockIdx.x * J;
   const long long tb = j0 - p.b;
   const long long nvalid = L - p.b;
-  const int nsm = NB * Kp;
-  const int NW = (MODE == M_SOFT) ? 4 : 2;  // words per state
-  float* H = sm;                 // NW arrays of nsm
-  float* P = sm + NW * nsm;      // NW arrays of nsm
-  const float tau2 = p.mp.tau2;
+  float* HM = sm;
+  float* HG = sm + nsm;
+  float* HC = sm + 2 * nsm;                                  // soft only
+  float* HB = sm + 3 * nsm;                                  // soft only
+  float* PM = sm + (MODE == M_SOFT ? 4 : 2) * nsm;
+  float* PA = PM + nsm;
+  float* PB = PA + nsm;                                      // soft only
+  float* PC = PB + nsm;                                      // soft only
+  const float tau2 = p.mp.tau2, tau = p.mp.tau, sg = p.sg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
+  const float* auxr = (MODE == M_SOFT) ? p.aux_in + row * L : nullptr;
 
-  {
-    const int n = NB * K;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      int blk = i / K, off = i - blk * K, pos = blk * Kp + off;
-      long long t = tb + i;
-      float g = 0.f;
-      if (t >= 0 && t < nvalid) g = cot[t];
-      if (MODE == M_LSE) {
-        H[pos] = g != 0.f ? p.sg * outr[t] : 0.f;
-        H[nsm + pos] = g;
-      } else {
-        if (g != 0.f) {
-          H[pos] = p.aux_in[row * L + t];
-          H[2 * nsm + pos] = 0.f;
-          H[3 * nsm + pos] = p.sg * outr[t];
+  for (int blk = warp; blk < NB; blk += nw) {
+    const long long base = tb + (long long)blk * K;
+    for (int o0 = 0; o0 < K; o0 += 64) {
+      float gv[2], ov[2], av[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long t = base + off;
+        bool v = off < K && t >= 0 && t < nvalid;
+        gv[k] = v ? cot[t] : 0.f;
+        ov[k] = v ? outr[t] : 0.f;
+        if (MODE == M_SOFT) av[k] = v ? auxr[t] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        if (off >= K) continue;
+        int q = blk * Kp + off;
+        HG[q] = gv[k];
+        if (MODE == M_LSE) {
+          HM[q] = sg * ov[k];
         } else {
-          H[pos] = 0.f;
-          H[2 * nsm + pos] = 0.f;
-          H[3 * nsm + pos] = 0.f;
+          HM[q] = av[k];
+          HC[q] = sg * ov[k];
         }
-        H[nsm + pos] = g;
       }
     }
   }
-  // pad contribution: overrun outputs route their cotangent to c[L-1] (last pad)
+  // pad contribution: overrun outputs route their cotangent to c[L-1] ('last' padding)
   const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J);
-  if (own_last) {
+  float padsum = 0.f;
+  if (own_last) {  // block-uniform branch
     float s = 0.f;
     long long t_lo = nvalid > 0 ? nvalid : 0;
     for (long long t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red_sh[threadIdx.x >> 5] = s;
+    padsum = block_sum(s, red_sh);
   }
   __syncthreads();
-  if (own_last && threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red_sh[w];
-    padsum_sh = s;
-  }
   if (threadIdx.x < NB) {  // prefix scans
-    const int base = threadIdx.x * Kp;
+    const int b0 = threadIdx.x * Kp;
     if (MODE == M_LSE) {
-      GLse a = {0.f, 0.f};
-      for (int i = 0; i < K; ++i) {
-        a = glse_comb(a, GLse{H[base + i], H[nsm + base + i]}, tau2);
-        P[base + i] = a.mu;
-        P[nsm + base + i] = a.A;
+      float mu = HM[b0], A = HG[b0];
+      PM[b0] = mu;
+      PA[b0] = A;
+#pragma unroll 4
+      for (int i = 1; i < K; ++i) {
+        gl_add(mu, A, HM[b0 + i], HG[b0 + i], tau2);
+        PM[b0 + i] = mu;
+        PA[b0 + i] = A;
       }
     } else {
-      GSoft a = {0.f, 0.f, 0.f, 0.f};
-      for (int i = 0; i < K; ++i) {
-        int q = base + i;
-        a = gsoft_comb(a, GSoft{H[q], H[nsm + q], H[2 * nsm + q], H[3 * nsm + q]}, tau2);
-        P[q] = a.mu;
-        P[nsm + q] = a.A;
-        P[2 * nsm + q] = a.Bc;
-        P[3 * nsm + q] = a.c;
+      float mu = HM[b0], A = HG[b0], Bc = 0.f, c = HC[b0];
+      PM[b0] = mu;
+      PA[b0] = A;
+      PB[b0] = Bc;
+      PC[b0] = c;
+#pragma unroll 2
+      for (int i = 1; i < K; ++i) {
+        int q = b0 + i;
+        gs_add(mu, A, Bc, c, HM[q], HG[q], 0.f, HC[q], tau2);
+        PM[q] = mu;
+        PA[q] = A;
+        PB[q] = Bc;
+        PC[q] = c;
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x < NB - 1) {  // suffix walk + combine, result in place into H
-    const int base = threadIdx.x * Kp, nb = base + Kp;
+  if (threadIdx.x < NB - 1) {  // suffix walk + combine; results in place into H*
+    const int b0 = threadIdx.x * Kp, nb = b0 + Kp - 1;  // nb + i = next block prefix at i - 1
     if (MODE == M_LSE) {
-      GLse acc = {0.f, 0.f};
+      float mu = HM[b0 + K - 1], A = HG[b0 + K - 1];
+#pragma unroll 4
       for (int i = K - 1; i >= 0; --i) {
-        acc = glse_comb(GLse{H[base + i], H[nsm + base + i]}, acc, tau2);
-        GLse r = acc;
-        if (i > 0) r = glse_comb(acc, GLse{P[nb + i - 1], P[nsm + nb + i - 1]}, tau2);
-        H[base + i] = r.mu;
-        H[nsm + base + i] = r.A;
+        if (i < K - 1) gl_add(mu, A, HM[b0 + i], HG[b0 + i], tau2);
+        float m2 = mu, a2 = A;
+        if (i > 0) gl_add(m2, a2, PM[nb + i], PA[nb + i], tau2);
+        HM[b0 + i] = m2;
+        HG[b0 + i] = a2;
       }
     } else {
-      GSoft acc = {0.f, 0.f, 0.f, 0.f};
+      int q = b0 + K - 1;
+      float mu = HM[q], A = HG[q], Bc = 0.f, c = HC[q];
+#pragma unroll 2
       for (int i = K - 1; i >= 0; --i) {
-        int q = base + i;
-        acc = gsoft_comb(GSoft{H[q], H[nsm + q], H[2 * nsm + q], H[3 * nsm + q]}, acc, tau2);
-        GSoft r = acc;
-        if (i > 0) {
-          int pq = nb + i - 1;
-          r = gsoft_comb(acc, GSoft{P[pq], P[nsm + pq], P[2 * nsm + pq], P[3 * nsm + pq]}, tau2);
+        q = b0 + i;
+        if (i < K - 1) gs_add(mu, A, Bc, c, HM[q], HG[q], 0.f, HC[q], tau2);
+        float m2 = mu, a2 = A, b2 = Bc, c2 = c;
+        if (i > 0) gs_add(m2, a2, b2, c2, PM[nb + i], PA[nb + i], PB[nb + i], PC[nb + i], tau2);
+        HM[q] = m2;
+        HG[q] = a2;
+        HC[q] = c2;
+        HB[q] = b2;
+      }
+    }
+  }
+  __syncthreads();
+  Ev<MODE, EK> ev(p.child, row, p.mp);
+  for (int blk = warp; blk < NB - 1; blk += nw) {
+    const long long base = j0 + (long long)blk * K;
+    for (int o0 = 0; o0 < K; o0 += 64) {
+      typename Ev<MODE, EK>::Raw r[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long j = base + off;
+        if (off < K && j < L) r[k] = ev.load(j);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long j = base + off;
+        if (off >= K || j >= L) continue;
+        int q = blk * Kp + off;
+        float A = HG[q];
+        float g = 0.f;
+        if (MODE == M_LSE) {
+          if (A != 0.f) {
+            float uj = sg * ev.value(j, r[k]);
+            g = A * ex2f(tau2 * (uj - HM[q]));
+          }
+        } else {
+          float Bc = HB[q];
+          if (A != 0.f || Bc != 0.f) {
+            float uj = sg * ev.value(j, r[k]);
+            g = ex2f(tau2 * (uj - HM[q])) * (A * fmaf(tau, uj - HC[q], 1.f) - tau * Bc);
+          }
         }
-        H[q] = r.mu;
-        H[nsm + q] = r.A;
-        H[2 * nsm + q] = r.Bc;
-        H[3 * nsm + q] = r.c;
+        if (own_last && j == L - 1) g += padsum;
+        ev.grad(j, r[k], g);
       }
     }
-  }
-  __syncthreads();
-  const long long jend = j0 + J < L ? j0 + J : L;
-  for (long long j = j0 + threadIdx.x; j < jend; j += blockDim.x) {
-    int i = (int)(j - j0);
-    int blk = i / K, off = i - blk * K, q = blk * Kp + off;
-    float g = 0.f;
-    float A = H[nsm + q];
-    if (MODE == M_LSE) {
-      if (A != 0.f) {
-        float uj = p.sg * expr_eval<MODE>(p.child, row, j, p.mp);
-        g = A * ex2f(tau2 * (uj - H[q]));
-      }
-    } else {
-      float Bc = H[2 * nsm + q];
-      if (A != 0.f || Bc != 0.f) {
-        float uj = p.sg * expr_eval<MODE>(p.child, row, j, p.mp);
-        float c = H[3 * nsm + q];
-        g = ex2f(tau2 * (uj - H[q])) * (A * fmaf(p.mp.tau, uj - c, 1.f) - p.mp.tau * Bc);
-      }
-    }
-    if (own_last && j == L - 1) g += padsum_sh;
-    expr_vjp<MODE>(p.child, row, j, g, p.mp);
   }
 }
 
 // ===========================================================================
-// timed F / G — backward, hard (recompute arg-max, scatter in shared memory)
+// timed F / G — backward, hard (recompute the first arg-max, scatter in smem)
 // ===========================================================================
-template <int MODE>
-__global__ void __launch_bounds__(256) k_fg_timed_bwd_hard(const __grid_constant__ FGParams p) {
+// Inputs cover NB+1 blocks from s0 = j0 - K + 1 (the start of the window of
+// output t = j0 - b); outputs t = s - a for starts s in blocks 0..NB-1.
+//   U [(NB+1)Kp] child, PV/PI prefix (value, tile-local index), GT[NB*Kp] cotangent,
+//   G [J] accumulated child cotangent for the owned range
+template <int EK>
+__global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red_sh[32];
-  __shared__ float padsum_sh;
   const int NB = p.NB, K = p.K, Kp = p.Kp;
-  const int NBi = NB + 1;  // input blocks
+  const int NBi = NB + 1;
+  const int nsi = NBi * Kp;
   const long long row = blockIdx.y, L = p.L;
   const long long J = (long long)(NB - 1) * K;
   const long long j0 = (long long)blockIdx.x * J;
-  const long long s0 = j0 - K + 1;  // first input index (start of window of t = j0 - b)
+  const long long s0 = j0 - K + 1;
   const long long nvalid = L - p.b;
-  const int nsm = NBi * Kp;
-  float* u = sm;
-  float* PV = sm + nsm;
-  int* PI = reinterpret_cast<int*>(sm + 2 * nsm);
-  float* G = sm + 3 * nsm;  // J accumulators
+  float* U = sm;
+  float* PV = sm + nsi;
+  int* PI = reinterpret_cast<int*>(sm + 2 * nsi);
+  float* GT = sm + 3 * nsi;
+  float* G = GT + NB * Kp;
+  const float sg = p.sg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const float* cot = p.cot + row * L;
+  Ev<M_HARD, EK> ev(p.child, row, p.mp);
 
-  {
-    const int n = NBi * K;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      int blk = i / K, off = i - blk * K;
-      long long idx = s0 + i;
-      u[blk * Kp + off] =
-          (idx >= 0 && idx < L) ? p.sg * expr_eval<MODE>(p.child, row, idx, p.mp) : -INFINITY;
+  for (int blk = warp; blk < NBi; blk += nw) {
+    const long long base = s0 + (long long)blk * K;
+    for (int o0 = 0; o0 < K; o0 += 128) {
+      typename Ev<M_HARD, EK>::Raw r[4];
+      float gv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long idx = base + off;
+        if (off < K && idx >= 0 && idx < L) r[k] = ev.load(idx);
+        long long t = idx - p.a;
+        gv[k] = (blk < NB && off < K && t >= 0 && t < nvalid) ? cot[t] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long idx = base + off;
+        if (off >= K) continue;
+        U[blk * Kp + off] = (idx >= 0 && idx < L) ? sg * ev.value(idx, r[k]) : -INFINITY;
+        if (blk < NB) GT[blk * Kp + off] = gv[k];
+      }
     }
-    for (int i = threadIdx.x; i < (int)J; i += blockDim.x) G[i] = 0.f;
   }
+  for (int i = threadIdx.x; i < (int)J; i += blockDim.x) G[i] = 0.f;
   const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J);
+  float padsum = 0.f;
   if (own_last) {
     float s = 0.f;
     long long t_lo = nvalid > 0 ? nvalid : 0;
     for (long long t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red_sh[threadIdx.x >> 5] = s;
+    padsum = block_sum(s, red_sh);
   }
   __syncthreads();
-  if (own_last && threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red_sh[w];
-    padsum_sh = s;
-  }
   if (threadIdx.x < NBi) {  // prefix (value, first arg-max)
-    const int base = threadIdx.x * Kp;
-    float bv = u[base];
-    int bi = threadIdx.x * K;
-    PV[base] = bv;
-    PI[base] = bi;
+    const int b0 = threadIdx.x * Kp;
+    const int l0 = threadIdx.x * K;
+    float bv = U[b0];
+    int bi = l0;
+    PV[b0] = bv;
+    PI[b0] = bi;
+#pragma unroll 4
     for (int i = 1; i < K; ++i) {
-      float x = u[base + i];
-      if (x > bv) {
-        bv = x;
-        bi = threadIdx.x * K + i;
-      }
-      PV[base + i] = bv;
-      PI[base + i] = bi;
+      float x = U[b0 + i];
+      bool up = x > bv;
+      bv = up ? x : bv;
+      bi = up ? l0 + i : bi;
+      PV[b0 + i] = bv;
+      PI[b0 + i] = bi;
     }
   }
   __syncthreads();
   if (threadIdx.x < NB) {
     const int qb = threadIdx.x;
-    const int base = qb * Kp, nb = base + Kp;
-    HardAcc acc = {-INFINITY, 0};
+    const int b0 = qb * Kp, nb = b0 + Kp - 1;
+    float av = U[b0 + K - 1];
+    int ai = qb * K + K - 1;
+#pragma unroll 4
     for (int i = K - 1; i >= 0; --i) {
-      float x = u[base + i];
-      if (x >= acc.v) acc = {x, qb * K + i};  // walking backwards: the new element is earlier
-      HardAcc r = acc;
-      if (i > 0) {
-        float pv = PV[nb + i - 1];
-        if (pv > r.v) r = {pv, PI[nb + i - 1]};
-      }
-      long long s = s0 + (long long)qb * K + i;
-      long long t = s - p.a;
-      if (t >= 0 && t < nvalid) {
-        float g = cot[t];
-        long long jj = s0 + r.i;
-        if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
-      }
+      float x = U[b0 + i];
+      bool up = x >= av;  // walking backwards: the new sample is earlier
+      av = up ? x : av;
+      ai = up ? qb * K + i : ai;
+      int ri = ai;
+      if (i > 0 && PV[nb + i] > av) ri = PI[nb + i];
+      float g = GT[b0 + i];
+      long long jj = s0 + ri;
+      if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
     }
   }
   __syncthreads();
-  const long long jend = j0 + J < L ? j0 + J : L;
-  for (long long j = j0 + threadIdx.x; j < jend; j += blockDim.x) {
-    float g = G[j - j0];
-    if (own_last && j == L - 1) g += padsum_sh;
-    expr_vjp<MODE>(p.child, row, j, g, p.mp);
+  for (int blk = warp; blk < NB - 1; blk += nw) {
+    const long long base = j0 + (long long)blk * K;
+    for (int o0 = 0; o0 < K; o0 += 64) {
+      typename Ev<M_HARD, EK>::Raw r[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long j = base + off;
+        if (off < K && j < L) r[k] = ev.load(j);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        int off = o0 + lane + 32 * k;
+        long long j = base + off;
+        if (off >= K || j >= L) continue;
+        float g = G[blk * K + off];
+        if (own_last && j == L - 1) g += padsum;
+        ev.grad(j, r[k], g);
+      }
+    }
   }
 }
 
@@ -515,28 +633,41 @@ static cudaError_t set_smem(KernT k, size_t bytes) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-static const size_t kSmemBudget = 72 * 1024;   // per CTA target (3 CTAs / SM)
+static const size_t kSmemBudget = 72 * 1024;  // per CTA: 3 CTAs x 256 threads per SM
 static const size_t kSmemMax = 200 * 1024;
 
-// words per element of each kernel's shared layout
-static int fwd_words(int mode) { return mode == M_SOFT ? 5 : 3; }
-static int bwd_words(int mode) { return mode == M_HARD ? 4 : (mode == M_SOFT ? 8 : 4); }
+static int fwd_words(int mode) { return mode == M_SOFT ? 4 : 2; }
+static int bwd_words(int mode) { return mode == M_SOFT ? 8 : (mode == M_HARD ? 5 : 4); }
 
-static int pick_nb(int K, int words, int extra_blocks) {
-  int Kp = odd_stride(K);
-  long long per_block = (long long)words * Kp * 4;
-  long long nb = (long long)(kSmemBudget / per_block) - extra_blocks;
-  if (nb > 256 - extra_blocks) nb = 256 - extra_blocks;
+static int pick_nb(int K, int words) {
+  long long per_block = (long long)words * odd_stride(K) * 4;
+  long long nb = (long long)(kSmemBudget / per_block);
+  if (nb > 255) nb = 255;
   if (nb < 2) nb = 2;
   return (int)nb;
 }
 
 static bool use_direct(int K, int mode) {
   if (K < 4) return true;
-  int Kp = odd_stride(K);
-  // two blocks (+1 input block for hard backward) must fit
-  size_t need = (size_t)bwd_words(mode) * 3 * Kp * 4;
+  size_t need = (size_t)bwd_words(mode) * 3 * odd_stride(K) * 4;
   return need > kSmemMax;
+}
+
+#define DISPATCH_EK(EKV, ...)          \
+  if ((EKV) == EK_LEAF) {              \
+    constexpr int EK = EK_LEAF;        \
+    __VA_ARGS__;                       \
+  } else {                             \
+    constexpr int EK = EK_GEN;         \
+    __VA_ARGS__;                       \
+  }
+
+template <int MODE, int EK>
+static cudaError_t fwd_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t st) {
+  cudaError_t e = set_smem(k_fgt_fwd<MODE, EK>, smem);
+  if (e != cudaSuccess) return e;
+  k_fgt_fwd<MODE, EK><<<grid, FG_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
@@ -549,25 +680,36 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   p.Kp = odd_stride(p.K);
-  p.NB = pick_nb(p.K, fwd_words(mode), 0);
+  p.NB = pick_nb(p.K, fwd_words(mode));
   long long J = (long long)(p.NB - 1) * p.K;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
-  int threads = ((p.NB + 31) / 32) * 32;
-  if (threads < 128) threads = 128;
-  if (threads > 256) threads = 256;
   size_t smem = (size_t)fwd_words(mode) * p.NB * p.Kp * 4;
+  const int ek = p.child.n_step == 1 ? EK_LEAF : EK_GEN;
   cudaError_t e;
   if (mode == M_HARD) {
-    if ((e = set_smem(k_fg_timed_fwd<M_HARD>, smem)) != cudaSuccess) return e;
-    k_fg_timed_fwd<M_HARD><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (fwd_v2<M_HARD, EK>(p, smem, grid, st)))
   } else if (mode == M_LSE) {
-    if ((e = set_smem(k_fg_timed_fwd<M_LSE>, smem)) != cudaSuccess) return e;
-    k_fg_timed_fwd<M_LSE><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (fwd_v2<M_LSE, EK>(p, smem, grid, st)))
   } else {
-    if ((e = set_smem(k_fg_timed_fwd<M_SOFT>, smem)) != cudaSuccess) return e;
-    k_fg_timed_fwd<M_SOFT><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (fwd_v2<M_SOFT, EK>(p, smem, grid, st)))
   }
   count_launch();
+  return e;
+}
+
+template <int MODE, int EK>
+static cudaError_t bwd_sm_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t st) {
+  cudaError_t e = set_smem(k_fgt_bwd_sm<MODE, EK>, smem);
+  if (e != cudaSuccess) return e;
+  k_fgt_bwd_sm<MODE, EK><<<grid, FG_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int EK>
+static cudaError_t bwd_hard_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t st) {
+  cudaError_t e = set_smem(k_fgt_bwd_hard<EK>, smem);
+  if (e != cudaSuccess) return e;
+  k_fgt_bwd_hard<EK><<<grid, FG_THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -584,39 +726,32 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
     return launch_pointwise_vjp(mode, p, p.gbuf, st);
   }
   p.Kp = odd_stride(p.K);
-  const int words = bwd_words(mode);
+  const int ek = p.child.n_step == 1 ? EK_LEAF : EK_GEN;
   if (mode == M_HARD) {
-    // (NB+1) input blocks * 3 words + J accumulators
-    int nb = pick_nb(p.K, 4, 1);
+    // U, PV, PI over NB+1 blocks + GT over NB blocks + J accumulators
+    int nb = pick_nb(p.K, 5);
+    if (nb > 254) nb = 254;
     p.NB = nb;
-    size_t smem = (size_t)3 * (nb + 1) * p.Kp * 4 + (size_t)(nb - 1) * p.K * 4;
+    size_t smem = (size_t)3 * (nb + 1) * p.Kp * 4 + (size_t)nb * p.Kp * 4 + (size_t)(nb - 1) * p.K * 4;
     long long J = (long long)(nb - 1) * p.K;
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
-    int threads = ((nb + 1 + 31) / 32) * 32;
-    if (threads < 128) threads = 128;
-    if (threads > 256) threads = 256;
-    if ((e = set_smem(k_fg_timed_bwd_hard<M_HARD>, smem)) != cudaSuccess) return e;
-    k_fg_timed_bwd_hard<M_HARD><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (bwd_hard_v2<EK>(p, smem, grid, st)))
     count_launch();
-    return cudaGetLastError();
+    return e;
   }
-  int nb = pick_nb(p.K, words, 0);
+  const int words = bwd_words(mode);
+  int nb = pick_nb(p.K, words);
   p.NB = nb;
   size_t smem = (size_t)words * nb * p.Kp * 4;
   long long J = (long long)(nb - 1) * p.K;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
-  int threads = ((nb + 31) / 32) * 32;
-  if (threads < 128) threads = 128;
-  if (threads > 256) threads = 256;
   if (mode == M_LSE) {
-    if ((e = set_smem(k_fg_timed_bwd_smooth<M_LSE>, smem)) != cudaSuccess) return e;
-    k_fg_timed_bwd_smooth<M_LSE><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (bwd_sm_v2<M_LSE, EK>(p, smem, grid, st)))
   } else {
-    if ((e = set_smem(k_fg_timed_bwd_smooth<M_SOFT>, smem)) != cudaSuccess) return e;
-    k_fg_timed_bwd_smooth<M_SOFT><<<grid, threads, smem, st>>>(p);
+    DISPATCH_EK(ek, e = (bwd_sm_v2<M_SOFT, EK>(p, smem, grid, st)))
   }
   count_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 // ===========================================================================

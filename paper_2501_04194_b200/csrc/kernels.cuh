@@ -71,6 +71,9 @@ cudaError_t launch_until_bwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st);
 cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st);
 
+cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs, long long es,
+                                float v, cudaStream_t st);
+
 // launch accounting (exec.cu)
 void count_launch(int n = 1);
 

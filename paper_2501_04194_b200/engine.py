@@ -117,6 +117,7 @@ class Compiled:
                 gt[i].ptr = d.data_ptr()
                 gt[i].row_stride = d.stride(0)
                 gt[i].elem_stride = d.stride(1)
+                gt[i].accumulate = 0  # the library writes every element
         _lib.check(self.lib.stlg_backward(
             self.plan, self._channel_table(chans), B, T, self._smooth_table(params),
             trace.data_ptr(), cot.data_ptr(), gt,
@@ -171,7 +172,7 @@ class _TraceFn(torch.autograd.Function):
         B, T = out.shape
         dev = out.device
         g = g.to(torch.float32).contiguous()
-        dch = [torch.zeros((B, T), dtype=torch.float32, device=dev)
+        dch = [torch.empty((B, T), dtype=torch.float32, device=dev)
                if ctx.needs_input_grad[3 + i] else None for i in range(len(chans))]
         d_smooth = None
         if comp.n_smooth:

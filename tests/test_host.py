@@ -141,6 +141,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.StlgNode) == 64
     assert ctypes.sizeof(_lib.StlgCfg) == 56
     assert ctypes.sizeof(_lib.StlgChannel) == 24
+    assert ctypes.sizeof(_lib.StlgGrad) == 32
     assert ctypes.sizeof(_lib.StlgSmooth) == 32
 
 

@@ -259,7 +259,8 @@ def run_b200(args, rank, world):
     # ---- e2e through the public API: pinned host -> device -> host ----------
     hp = torch.tensor(host).pin_memory()
     h_tr = torch.empty(B, T).pin_memory()
-    h_dp = torch.empty(B, T, 2).pin_memory()
+    h_dx = torch.empty(B, T).pin_memory()
+    h_dy = torch.empty(B, T).pin_memory()
     e2e_steps = max(2, min(args.steps, 10))
 
     def e2e_step():
@@ -269,8 +270,8 @@ def run_b200(args, rank, world):
         out = P.trace(f, {"px": px, "py": py}, cfg)
         out.backward(ones)
         h_tr.copy_(out.detach(), non_blocking=True)
-        h_dp[..., 0].copy_(px.grad, non_blocking=True)
-        h_dp[..., 1].copy_(py.grad, non_blocking=True)
+        h_dx.copy_(px.grad, non_blocking=True)
+        h_dy.copy_(py.grad, non_blocking=True)
 
     for _ in range(2):
         e2e_step()

@@ -98,7 +98,9 @@ __device__ __forceinline__ float leaf_val(const DExpr& e, const DLeaf& L, long l
   } else {
     float dx = ld_src(e.src[L.src], b, j) - L.cx;
     float dy = ld_src(e.src[L.src2], b, j) - L.cy;
-    x = sqrtf(fmaf(dx, dx, dy * dy));
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fmaf(dx, dx, dy * dy)));
+    x = y;
   }
   // one rounding, exactly as x + (-c) / (-x) + c in the reference
   float t = __fadd_rn(L.s_in * x, L.c);
@@ -370,32 +372,34 @@ __device__ __forceinline__ void gs_add(float& mu, float& A, float& Bc, float& c,
 }
 
 // ---------------------------------------------------------------------------
-// evaluators: EK_LEAF hoists a single-leaf expression into registers (the
-// common case: Pred / NormPred / a materialised trace under a temporal op);
-// EK_GEN interprets any fused expression.
+// evaluators.  The single-leaf kinds (the common case: a Pred / NormPred / a
+// materialised trace directly under a temporal operator) are compile-time
+// specialisations with the row's pointers hoisted into registers; EK_GEN
+// interprets any fused expression.  Element indices are row-relative ints.
 // ---------------------------------------------------------------------------
-enum ExprKind { EK_GEN = 0, EK_LEAF = 1 };
+enum ExprKind { EK_GEN = 0, EK_AFF = 1, EK_NORM = 2, EK_SRC = 3 };
 
-template <int MODE, int EK>
-struct Ev;
+__device__ __forceinline__ float sqrt_fast(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
-template <int MODE>
-struct Ev<MODE, EK_LEAF> {
-  struct Raw {
-    float x, y;
-  };
+struct LeafRegs {
   const float* p1;
   const float* p2;
-  long long es1, es2;
   float* g1;
   float* g2;
-  long long ges1, ges2;
-  int kind, st1, st2;
+  int es1, es2, ges1, ges2;
+  int st1, st2;
   float s_in, s_out, c, cx, cy;
-
-  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) {
+  __device__ __forceinline__ LeafRegs(const DExpr& e, long long row) {
     const DLeaf& L = e.leaf[0];
-    kind = L.kind;
     st1 = L.st1;
     st2 = L.st2;
     s_in = L.s_in;
@@ -406,66 +410,80 @@ struct Ev<MODE, EK_LEAF> {
     p1 = p2 = nullptr;
     g1 = g2 = nullptr;
     es1 = es2 = ges1 = ges2 = 0;
-    if (kind != LEAF_CONST) {
+    if (L.kind != LEAF_CONST) {
       const DSrc& s = e.src[L.src];
       p1 = s.p + row * s.rs;
-      es1 = s.es;
+      es1 = (int)s.es;
       const DDst& d = e.dst[L.src];
       if (d.p) {
         g1 = d.p + row * d.rs;
-        ges1 = d.es;
+        ges1 = (int)d.es;
       }
     }
-    if (kind == LEAF_NORM) {
+    if (L.kind == LEAF_NORM) {
       const DSrc& s = e.src[L.src2];
       p2 = s.p + row * s.rs;
-      es2 = s.es;
+      es2 = (int)s.es;
       const DDst& d = e.dst[L.src2];
       if (d.p) {
         g2 = d.p + row * d.rs;
-        ges2 = d.es;
+        ges2 = (int)d.es;
       }
     }
   }
-  __device__ __forceinline__ Raw load(long long j) const {
-    Raw r{0.f, 0.f};
-    if (kind != LEAF_CONST) r.x = __ldg(p1 + j * es1);
-    if (kind == LEAF_NORM) r.y = __ldg(p2 + j * es2);
-    return r;
-  }
-  __device__ __forceinline__ float value(long long, Raw r) const {
-    if (kind == LEAF_CONST) return c;
-    if (kind == LEAF_SRC) return s_out * r.x;
-    float x = r.x;
-    if (kind == LEAF_NORM) {
-      float dx = r.x - cx, dy = r.y - cy;
-      x = sqrtf(fmaf(dx, dx, dy * dy));
-    }
-    return s_out * __fadd_rn(s_in * x, c);
-  }
-  __device__ __forceinline__ static void put(float* p, long long es, long long j, float g, int st) {
+  __device__ __forceinline__ static void put(float* p, int es, int j, float g, int st) {
     if (p) {
-      float* q = p + j * es;
+      float* q = p + (long long)j * es;
       if (st) *q = g;
       else *q += g;
     }
   }
-  __device__ __forceinline__ void grad(long long j, Raw r, float g) const {
-    if (kind == LEAF_CONST) return;
-    if (kind == LEAF_SRC) {
-      put(g1, ges1, j, g * s_out, st1);
-      return;
-    }
-    float gx = g * s_out * s_in;
-    if (kind == LEAF_AFFINE) {
-      put(g1, ges1, j, gx, st1);
-      return;
-    }
+};
+
+template <int MODE, int EK>
+struct Ev;
+
+template <int MODE>
+struct Ev<MODE, EK_AFF> : LeafRegs {
+  struct Raw {
+    float x;
+  };
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
+  __device__ __forceinline__ Raw load(int j) const { return Raw{__ldg(p1 + (long long)j * es1)}; }
+  __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
+  __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * (s_out * s_in), st1); }
+};
+
+template <int MODE>
+struct Ev<MODE, EK_SRC> : LeafRegs {
+  struct Raw {
+    float x;
+  };
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
+  __device__ __forceinline__ Raw load(int j) const { return Raw{__ldg(p1 + (long long)j * es1)}; }
+  __device__ __forceinline__ float value(int, Raw r) const { return s_out * r.x; }
+  __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * s_out, st1); }
+};
+
+template <int MODE>
+struct Ev<MODE, EK_NORM> : LeafRegs {
+  struct Raw {
+    float x, y;
+  };
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
+  __device__ __forceinline__ Raw load(int j) const {
+    return Raw{__ldg(p1 + (long long)j * es1), __ldg(p2 + (long long)j * es2)};
+  }
+  __device__ __forceinline__ float value(int, Raw r) const {
     float dx = r.x - cx, dy = r.y - cy;
-    float d = sqrtf(fmaf(dx, dx, dy * dy));
-    float inv = d > 0.f ? gx / d : 0.f;
-    put(g1, ges1, j, dx * inv, st1);
-    put(g2, ges2, j, dy * inv, st2);
+    return s_out * __fadd_rn(s_in * sqrt_fast(fmaf(dx, dx, dy * dy)), c);
+  }
+  __device__ __forceinline__ void grad(int j, Raw r, float g) const {
+    float dx = r.x - cx, dy = r.y - cy;
+    float d2 = fmaf(dx, dx, dy * dy);
+    float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
+    put(g1, ges1, j, dx * sc, st1);
+    put(g2, ges2, j, dy * sc, st2);
   }
 };
 
@@ -476,13 +494,28 @@ struct Ev<MODE, EK_GEN> {
   long long row;
   ModeP mp;
   __device__ __forceinline__ Ev(const DExpr& ex, long long r, const ModeP& m) : e(&ex), row(r), mp(m) {}
-  __device__ __forceinline__ Raw load(long long) const { return Raw{}; }
-  __device__ __forceinline__ float value(long long j, Raw) const {
-    return expr_eval<MODE>(*e, row, j, mp);
-  }
-  __device__ __forceinline__ void grad(long long j, Raw, float g) const {
-    expr_vjp<MODE>(*e, row, j, g, mp);
-  }
+  __device__ __forceinline__ Raw load(int) const { return Raw{}; }
+  __device__ __forceinline__ float value(int j, Raw) const { return expr_eval<MODE>(*e, row, j, mp); }
+  __device__ __forceinline__ void grad(int j, Raw, float g) const { expr_vjp<MODE>(*e, row, j, g, mp); }
 };
+
+// host-side choice of the evaluator for an expression
+__host__ __device__ inline int expr_kind(const DExpr& e) {
+  if (e.n_step != 1) return EK_GEN;
+  int k = e.leaf[0].kind;
+  if (k == LEAF_AFFINE) return EK_AFF;
+  if (k == LEAF_NORM) return EK_NORM;
+  if (k == LEAF_SRC) return EK_SRC;
+  return EK_GEN;
+}
+
+// floor(i / K) for 0 <= i < 2^24 with a float reciprocal (exact after correction)
+__device__ __forceinline__ int div_k(int i, int K, float invK) {
+  int q = __float2int_rz((float)i * invK);
+  int r = i - q * K;
+  q += (r >= K) ? 1 : 0;
+  q -= (r < 0) ? 1 : 0;
+  return q;
+}
 
 }  // namespace stlg

@@ -100,54 +100,54 @@ cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cu
 // timed F / G — forward (vHGW)
 // ===========================================================================
 // Shared layout: NB blocks of K samples, row stride Kp = K | 1 (odd, so the
-// per-thread block walks are bank-conflict free):
-//   U  [NB*Kp]  child in max space; overwritten in place by the outputs
-//   P1 [NB*Kp]  prefix state: hard = running max; lse = log-domain prefix LSE;
-//               soft = prefix softmax value M
-//   P2 [NB*Kp]  soft: prefix LSE L
-//   AX [NB*Kp]  soft: window LSE (aux output for the backward)
-// Loads and stores run warp-per-block (coalesced, no integer division);
-// the scans run one thread per block.
+// per-thread block walks are bank-conflict free); flat index i of the tile
+// lives at i + (i / K) * (Kp - K):
+//   U  child in max space; overwritten in place by the outputs
+//   P1 prefix state: hard = running max; lse = log-domain prefix LSE;
+//      soft = prefix softmax value M
+//   P2 soft: prefix LSE L
+//   AX soft: window LSE (aux output for the backward)
+// Loads / stores are flat and coalesced (4 independent loads in flight per
+// thread); the scans run one thread per block.
 constexpr int FG_THREADS = 256;
 
 template <int MODE, int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float padv_sh;
-  const int NB = p.NB, K = p.K, Kp = p.Kp;
+  const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
   const int nsm = NB * Kp;
-  const long long row = blockIdx.y, L = p.L;
-  const long long J = (long long)(NB - 1) * K;
-  const long long t0 = (long long)blockIdx.x * J;
-  const long long nvalid = L - p.b;
-  const long long s0 = t0 + p.a;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = (NB - 1) * K;
+  const int t0 = blockIdx.x * J;
+  const int nvalid = L - p.b;
+  const int s0 = t0 + p.a;
+  const float invK = 1.f / (float)K;
   float* U = sm;
   float* P1 = sm + nsm;
   float* P2 = sm + 2 * nsm;
   float* AX = sm + 3 * nsm;
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const bool any = t0 < nvalid;
 
   if (threadIdx.x == 0) padv_sh = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   if (any) {
-    for (int blk = warp; blk < NB; blk += nw) {
-      const long long base = s0 + (long long)blk * K;
-      float* ub = U + blk * Kp;
-      for (int o0 = 0; o0 < K; o0 += 128) {
-        typename Ev<MODE, EK>::Raw r[4];
+    const int n = NB * K;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * FG_THREADS) {
+      typename Ev<MODE, EK>::Raw r[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          int off = o0 + lane + 32 * k;
-          long long idx = base + off;
-          if (off < K && idx < L) r[k] = ev.load(idx);
-        }
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * FG_THREADS;
+        if (i < n && s0 + i < L) r[u] = ev.load(s0 + i);
+      }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          int off = o0 + lane + 32 * k;
-          long long idx = base + off;
-          if (off < K) ub[off] = idx < L ? sg * ev.value(idx, r[k]) : -INFINITY;
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * FG_THREADS;
+        if (i < n) {
+          int idx = s0 + i;
+          U[i + div_k(i, K, invK) * dK] = idx < L ? sg * ev.value(idx, r[u]) : -INFINITY;
         }
       }
     }
@@ -231,15 +231,16 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
   }
   __syncthreads();
   const float padv = padv_sh;
-  for (int blk = warp; blk < NB - 1; blk += nw) {
-    for (int off = lane; off < K; off += 32) {
-      long long t = t0 + (long long)blk * K + off;
-      if (t >= L) break;
-      float v = (t < nvalid) ? sg * U[blk * Kp + off] : padv;
-      if (p.canon) v = __fadd_rn(v, 0.f);
-      p.out[row * L + t] = v;
-      if (MODE == M_SOFT && t < nvalid) p.aux[row * L + t] = AX[blk * Kp + off];
-    }
+  float* outr = p.out + row * L;
+  float* auxr = (MODE == M_SOFT) ? p.aux + row * L : nullptr;
+  const int tend = (t0 + J < L ? t0 + J : L) - t0;
+  for (int i = threadIdx.x; i < tend; i += FG_THREADS) {
+    int t = t0 + i;
+    int q = i + div_k(i, K, invK) * dK;
+    float v = (t < nvalid) ? sg * U[q] : padv;
+    if (p.canon) v = __fadd_rn(v, 0.f);
+    outr[t] = v;
+    if (MODE == M_SOFT && t < nvalid) auxr[t] = AX[q];
   }
 }
 
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
 // receives from outputs t in [j - b, j - a], a window of K over the output
 // sequence starting at tb = j0 - b.  Shared layout (stride Kp):
 //   LSE:  HM = M_t (u-space output), HG = g_t; prefix PM, PA
-//   soft: HM = L_t (window LSE), HG = g_t, HC = M_t; prefix PM, PA, PB, PC
+//   soft: HM = L_t (window LSE), HG = g_t, HC = M_t, HB (result Bc); prefix PM, PA, PB, PC
 // Gradient: LSE  g_child[j] = sum_t g_t exp(tau (u_j - M_t))
 //           soft g_child[j] = sum_t g_t exp(tau (u_j - L_t)) (1 + tau (u_j - M_t))
 __device__ __forceinline__ float block_sum(float v, float* red) {
@@ -266,51 +267,52 @@ template <int MODE, int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red_sh[32];
-  const int NB = p.NB, K = p.K, Kp = p.Kp;
+  const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
   const int nsm = NB * Kp;
-  const long long row = blockIdx.y, L = p.L;
-  const long long J = (long long)(NB - 1) * K;
-  const long long j0 = (long long)blockIdx.x * J;
-  const long long tb = j0 - p.b;
-  const long long nvalid = L - p.b;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = (NB - 1) * K;
+  const int j0 = blockIdx.x * J;
+  const int tb = j0 - p.b;
+  const int nvalid = L - p.b;
+  const float invK = 1.f / (float)K;
   float* HM = sm;
   float* HG = sm + nsm;
-  float* HC = sm + 2 * nsm;                                  // soft only
-  float* HB = sm + 3 * nsm;                                  // soft only
+  float* HC = sm + 2 * nsm;  // soft only
+  float* HB = sm + 3 * nsm;  // soft only
   float* PM = sm + (MODE == M_SOFT ? 4 : 2) * nsm;
   float* PA = PM + nsm;
-  float* PB = PA + nsm;                                      // soft only
-  float* PC = PB + nsm;                                      // soft only
+  float* PB = PA + nsm;  // soft only
+  float* PC = PB + nsm;  // soft only
   const float tau2 = p.mp.tau2, tau = p.mp.tau, sg = p.sg;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
   const float* auxr = (MODE == M_SOFT) ? p.aux_in + row * L : nullptr;
 
-  for (int blk = warp; blk < NB; blk += nw) {
-    const long long base = tb + (long long)blk * K;
-    for (int o0 = 0; o0 < K; o0 += 64) {
+  {
+    const int n = NB * K;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 2 * FG_THREADS) {
       float gv[2], ov[2], av[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long t = base + off;
-        bool v = off < K && t >= 0 && t < nvalid;
-        gv[k] = v ? cot[t] : 0.f;
-        ov[k] = v ? outr[t] : 0.f;
-        if (MODE == M_SOFT) av[k] = v ? auxr[t] : 0.f;
+      for (int u = 0; u < 2; ++u) {
+        int i = i0 + u * FG_THREADS;
+        int t = tb + i;
+        bool v = i < n && t >= 0 && t < nvalid;
+        gv[u] = v ? cot[t] : 0.f;
+        ov[u] = v ? outr[t] : 0.f;
+        av[u] = (MODE == M_SOFT && v) ? auxr[t] : 0.f;
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        if (off >= K) continue;
-        int q = blk * Kp + off;
-        HG[q] = gv[k];
+      for (int u = 0; u < 2; ++u) {
+        int i = i0 + u * FG_THREADS;
+        if (i >= n) continue;
+        int q = i + div_k(i, K, invK) * dK;
+        HG[q] = gv[u];
         if (MODE == M_LSE) {
-          HM[q] = sg * ov[k];
+          HM[q] = sg * ov[u];
         } else {
-          HM[q] = av[k];
-          HC[q] = sg * ov[k];
+          HM[q] = av[u];
+          HC[q] = sg * ov[u];
         }
       }
     }
@@ -320,8 +322,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant
   float padsum = 0.f;
   if (own_last) {  // block-uniform branch
     float s = 0.f;
-    long long t_lo = nvalid > 0 ? nvalid : 0;
-    for (long long t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
+    int t_lo = nvalid > 0 ? nvalid : 0;
+    for (int t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
     padsum = block_sum(s, red_sh);
   }
   __syncthreads();
@@ -385,39 +387,36 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant
   }
   __syncthreads();
   Ev<MODE, EK> ev(p.child, row, p.mp);
-  for (int blk = warp; blk < NB - 1; blk += nw) {
-    const long long base = j0 + (long long)blk * K;
-    for (int o0 = 0; o0 < K; o0 += 64) {
-      typename Ev<MODE, EK>::Raw r[2];
+  const int jn = (j0 + J < L ? j0 + J : L) - j0;
+  for (int i0 = threadIdx.x; i0 < jn; i0 += 2 * FG_THREADS) {
+    typename Ev<MODE, EK>::Raw r[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long j = base + off;
-        if (off < K && j < L) r[k] = ev.load(j);
-      }
+    for (int u = 0; u < 2; ++u) {
+      int i = i0 + u * FG_THREADS;
+      if (i < jn) r[u] = ev.load(j0 + i);
+    }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long j = base + off;
-        if (off >= K || j >= L) continue;
-        int q = blk * Kp + off;
-        float A = HG[q];
-        float g = 0.f;
-        if (MODE == M_LSE) {
-          if (A != 0.f) {
-            float uj = sg * ev.value(j, r[k]);
-            g = A * ex2f(tau2 * (uj - HM[q]));
-          }
-        } else {
-          float Bc = HB[q];
-          if (A != 0.f || Bc != 0.f) {
-            float uj = sg * ev.value(j, r[k]);
-            g = ex2f(tau2 * (uj - HM[q])) * (A * fmaf(tau, uj - HC[q], 1.f) - tau * Bc);
-          }
+    for (int u = 0; u < 2; ++u) {
+      int i = i0 + u * FG_THREADS;
+      if (i >= jn) continue;
+      int j = j0 + i;
+      int q = i + div_k(i, K, invK) * dK;
+      float A = HG[q];
+      float g = 0.f;
+      if (MODE == M_LSE) {
+        if (A != 0.f) {
+          float uj = sg * ev.value(j, r[u]);
+          g = A * ex2f(tau2 * (uj - HM[q]));
         }
-        if (own_last && j == L - 1) g += padsum;
-        ev.grad(j, r[k], g);
+      } else {
+        float Bc = HB[q];
+        if (A != 0.f || Bc != 0.f) {
+          float uj = sg * ev.value(j, r[u]);
+          g = ex2f(tau2 * (uj - HM[q])) * (A * fmaf(tau, uj - HC[q], 1.f) - tau * Bc);
+        }
       }
+      if (own_last && j == L - 1) g += padsum;
+      ev.grad(j, r[u], g);
     }
   }
 }
@@ -427,60 +426,62 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant
 // ===========================================================================
 // Inputs cover NB+1 blocks from s0 = j0 - K + 1 (the start of the window of
 // output t = j0 - b); outputs t = s - a for starts s in blocks 0..NB-1.
-//   U [(NB+1)Kp] child, PV/PI prefix (value, tile-local index), GT[NB*Kp] cotangent,
-//   G [J] accumulated child cotangent for the owned range
+//   U [(NB+1)Kp] child, PV/PI prefix (value, tile-local index),
+//   GT [NB*Kp] cotangent by start, G [J] accumulated child cotangent
 template <int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red_sh[32];
-  const int NB = p.NB, K = p.K, Kp = p.Kp;
+  const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
   const int NBi = NB + 1;
   const int nsi = NBi * Kp;
-  const long long row = blockIdx.y, L = p.L;
-  const long long J = (long long)(NB - 1) * K;
-  const long long j0 = (long long)blockIdx.x * J;
-  const long long s0 = j0 - K + 1;
-  const long long nvalid = L - p.b;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = (NB - 1) * K;
+  const int j0 = blockIdx.x * J;
+  const int s0 = j0 - K + 1;
+  const int nvalid = L - p.b;
+  const float invK = 1.f / (float)K;
   float* U = sm;
   float* PV = sm + nsi;
   int* PI = reinterpret_cast<int*>(sm + 2 * nsi);
   float* GT = sm + 3 * nsi;
   float* G = GT + NB * Kp;
   const float sg = p.sg;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const float* cot = p.cot + row * L;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
 
-  for (int blk = warp; blk < NBi; blk += nw) {
-    const long long base = s0 + (long long)blk * K;
-    for (int o0 = 0; o0 < K; o0 += 128) {
+  {
+    const int n = NBi * K;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * FG_THREADS) {
       typename Ev<M_HARD, EK>::Raw r[4];
       float gv[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long idx = base + off;
-        if (off < K && idx >= 0 && idx < L) r[k] = ev.load(idx);
-        long long t = idx - p.a;
-        gv[k] = (blk < NB && off < K && t >= 0 && t < nvalid) ? cot[t] : 0.f;
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * FG_THREADS;
+        int idx = s0 + i;
+        if (i < n && idx >= 0 && idx < L) r[u] = ev.load(idx);
+        int t = idx - p.a;
+        gv[u] = (i < NB * K && t >= 0 && t < nvalid) ? cot[t] : 0.f;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long idx = base + off;
-        if (off >= K) continue;
-        U[blk * Kp + off] = (idx >= 0 && idx < L) ? sg * ev.value(idx, r[k]) : -INFINITY;
-        if (blk < NB) GT[blk * Kp + off] = gv[k];
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * FG_THREADS;
+        if (i >= n) continue;
+        int idx = s0 + i;
+        int q = i + div_k(i, K, invK) * dK;
+        U[q] = (idx >= 0 && idx < L) ? sg * ev.value(idx, r[u]) : -INFINITY;
+        if (i < NB * K) GT[q] = gv[u];
       }
     }
   }
-  for (int i = threadIdx.x; i < (int)J; i += blockDim.x) G[i] = 0.f;
+  for (int i = threadIdx.x; i < J; i += FG_THREADS) G[i] = 0.f;
   const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J);
   float padsum = 0.f;
   if (own_last) {
     float s = 0.f;
-    long long t_lo = nvalid > 0 ? nvalid : 0;
-    for (long long t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
+    int t_lo = nvalid > 0 ? nvalid : 0;
+    for (int t = t_lo + threadIdx.x; t < L; t += blockDim.x) s += cot[t];
     padsum = block_sum(s, red_sh);
   }
   __syncthreads();
@@ -516,30 +517,27 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
       int ri = ai;
       if (i > 0 && PV[nb + i] > av) ri = PI[nb + i];
       float g = GT[b0 + i];
-      long long jj = s0 + ri;
+      int jj = s0 + ri;
       if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
     }
   }
   __syncthreads();
-  for (int blk = warp; blk < NB - 1; blk += nw) {
-    const long long base = j0 + (long long)blk * K;
-    for (int o0 = 0; o0 < K; o0 += 64) {
-      typename Ev<M_HARD, EK>::Raw r[2];
+  const int jn = (j0 + J < L ? j0 + J : L) - j0;
+  for (int i0 = threadIdx.x; i0 < jn; i0 += 2 * FG_THREADS) {
+    typename Ev<M_HARD, EK>::Raw r[2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long j = base + off;
-        if (off < K && j < L) r[k] = ev.load(j);
-      }
+    for (int u = 0; u < 2; ++u) {
+      int i = i0 + u * FG_THREADS;
+      if (i < jn) r[u] = ev.load(j0 + i);
+    }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        int off = o0 + lane + 32 * k;
-        long long j = base + off;
-        if (off >= K || j >= L) continue;
-        float g = G[blk * K + off];
-        if (own_last && j == L - 1) g += padsum;
-        ev.grad(j, r[k], g);
-      }
+    for (int u = 0; u < 2; ++u) {
+      int i = i0 + u * FG_THREADS;
+      if (i >= jn) continue;
+      int j = j0 + i;
+      float g = G[i];
+      if (own_last && j == L - 1) g += padsum;
+      ev.grad(j, r[u], g);
     }
   }
 }
@@ -633,16 +631,18 @@ static cudaError_t set_smem(KernT k, size_t bytes) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-static const size_t kSmemBudget = 72 * 1024;  // per CTA: 3 CTAs x 256 threads per SM
+static const size_t kSmemBudget = 56 * 1024;  // per CTA: 4 CTAs x 256 threads per SM
 static const size_t kSmemMax = 200 * 1024;
 
 static int fwd_words(int mode) { return mode == M_SOFT ? 4 : 2; }
 static int bwd_words(int mode) { return mode == M_SOFT ? 8 : (mode == M_HARD ? 5 : 4); }
 
+// blocks per CTA: a multiple of 32 when it fits (full warps in the scans)
 static int pick_nb(int K, int words) {
   long long per_block = (long long)words * odd_stride(K) * 4;
   long long nb = (long long)(kSmemBudget / per_block);
-  if (nb > 255) nb = 255;
+  if (nb >= 32) nb = (nb / 32) * 32;
+  if (nb > 224) nb = 224;
   if (nb < 2) nb = 2;
   return (int)nb;
 }
@@ -654,8 +654,14 @@ static bool use_direct(int K, int mode) {
 }
 
 #define DISPATCH_EK(EKV, ...)          \
-  if ((EKV) == EK_LEAF) {              \
-    constexpr int EK = EK_LEAF;        \
+  if ((EKV) == EK_AFF) {               \
+    constexpr int EK = EK_AFF;         \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_NORM) {       \
+    constexpr int EK = EK_NORM;        \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_SRC) {        \
+    constexpr int EK = EK_SRC;         \
     __VA_ARGS__;                       \
   } else {                             \
     constexpr int EK = EK_GEN;         \
@@ -684,7 +690,7 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
   long long J = (long long)(p.NB - 1) * p.K;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
   size_t smem = (size_t)fwd_words(mode) * p.NB * p.Kp * 4;
-  const int ek = p.child.n_step == 1 ? EK_LEAF : EK_GEN;
+  const int ek = expr_kind(p.child);
   cudaError_t e;
   if (mode == M_HARD) {
     DISPATCH_EK(ek, e = (fwd_v2<M_HARD, EK>(p, smem, grid, st)))
@@ -726,7 +732,7 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
     return launch_pointwise_vjp(mode, p, p.gbuf, st);
   }
   p.Kp = odd_stride(p.K);
-  const int ek = p.child.n_step == 1 ? EK_LEAF : EK_GEN;
+  const int ek = expr_kind(p.child);
   if (mode == M_HARD) {
     // U, PV, PI over NB+1 blocks + GT over NB blocks + J accumulators
     int nb = pick_nb(p.K, 5);

@@ -59,6 +59,7 @@ struct Entry {
   HExpr e1, e2;
   int out_slot;  // -1: the caller's trace buffer
   int aux_slot;  // softmax window-LSE buffer, -1 if none
+  int table = -1;  // smooth: index of its log2-weight table in the forward workspace
 };
 
 bool is_temporal(int op) { return op == STLG_EVENTUALLY || op == STLG_ALWAYS || op == STLG_UNTIL; }
@@ -71,7 +72,7 @@ bool is_elementwise(int op) {
 
 struct stlg_plan {
   stlg_cfg cfg;
-  int n_ch = 0, n_smooth = 0, n_slots = 0, n_aux = 0;
+  int n_ch = 0, n_smooth = 0, n_slots = 0, n_aux = 0, n_tables = 0;
   int root_temporal = 0;
   std::vector<Entry> entries;
   std::vector<int> ch_touched;  // channel referenced by some leaf (else zero-filled on overwrite)
@@ -267,6 +268,7 @@ int validate_nodes(const stlg_node* nodes, int n, int n_ch, int n_smooth) {
 struct Bufs {
   float* slots;   // n_slots * B * T
   float* aux;     // n_aux * B * T
+  float* tables;  // n_tables * T (log2 smooth weights)
   float* gslots;  // n_slots * B * T (backward)
   float* scratch; // 3 * B * T (backward)
   long long BT;
@@ -280,6 +282,35 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 void fwd_layout(const stlg_plan* p, long long BT, size_t* slots_b, size_t* aux_b) {
   *slots_b = align256(sizeof(float) * (size_t)p->n_slots * BT);
   *aux_b = align256(sizeof(float) * (size_t)p->n_aux * BT);
+}
+size_t tables_bytes(const stlg_plan* p, long long T) {
+  return align256(sizeof(float) * (size_t)p->n_tables * (size_t)T);
+}
+
+// Smooth-interval weights on the host in fp64, exactly as the reference forms
+// them (smoothing.py:85-97 / masking.py:300-305); returns the kept range.
+double sigmoid_h(double z) {
+  if (z >= 0) return 1.0 / (1.0 + std::exp(-z));
+  double ez = std::exp(z);
+  return ez / (1.0 + ez);
+}
+bool smooth_table(const stlg_smooth& sp, long long L, std::vector<float>& lw2, int* i_lo, int* i_hi) {
+  lw2.assign((size_t)L, -INFINITY);
+  int lo = -1, hi = -1;
+  const double Lf = (double)L;
+  for (long long i = 0; i < L; ++i) {
+    double a = sigmoid_h(((double)i - sp.a * Lf) * sp.c);
+    double b = sigmoid_h(((double)i - sp.b * Lf) * sp.c);
+    double w = a - b - sp.eps;
+    if (w > 0) {
+      lw2[(size_t)i] = (float)std::log2(w);
+      if (lo < 0) lo = (int)i;
+      hi = (int)i;
+    }
+  }
+  *i_lo = lo;
+  *i_hi = hi;
+  return lo >= 0;
 }
 
 int resolve(const stlg_plan* p, const HExpr& h, const stlg_channel* ch, const stlg_grad* dch,
@@ -399,8 +430,7 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
       e.kind = E_UNTIL;
     } else if (nd.itv_kind == STLG_ITV_SMOOTH) {
       e.kind = E_FG_SMOOTH;
-      delete plan;
-      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
+      e.table = plan->n_tables++;
     } else {
       e.kind = e.untimed ? E_FG_UNTIMED : E_FG_TIMED;
     }
@@ -414,7 +444,8 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
       delete plan;
       return fail(STLG_E_UNSUPPORTED, "sub-formula too large for one fused expression");
     }
-    if (cfg->mode == STLG_MODE_SOFTMAX && (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED))
+    if (cfg->mode == STLG_MODE_SOFTMAX &&
+        (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED || e.kind == E_FG_SMOOTH))
       e.aux_slot = plan->n_aux++;
     e.out_slot = (i == root) ? -1 : C.new_slot();
     C.slot_of[i] = e.out_slot;
@@ -467,11 +498,10 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   long long BT = (long long)B * T;
   size_t sb, ab;
   fwd_layout(plan, BT, &sb, &ab);
-  if (fwd_bytes) *fwd_bytes = sb + ab + 256;
+  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + 256;
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
-                 align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * 4 * (size_t)T) +
-                 align256(sizeof(float) * 1024 * (size_t)T) + 256;
+                 align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * (size_t)T) + 512;
   return STLG_OK;
 }
 
@@ -487,6 +517,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.BT = BT;
   bf.slots = (float*)base;
   bf.aux = (float*)(base + sb);
+  bf.tables = (float*)(base + sb + ab);
   bf.gslots = nullptr;
   bf.scratch = nullptr;
   if (bwd_ws) {
@@ -510,6 +541,79 @@ static void fill_fg(const stlg_plan* plan, const Entry& e, int64_t B, int64_t T,
   p.pad_value = (float)plan->cfg.pad_value;
   p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
   p.mp = mode_params(plan->cfg);
+}
+
+// Smooth-interval F / G: hard mode is the vHGW window kernel over the kept
+// range with padded-window semantics; LSE / softmax use smooth.cu.
+static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel* channels,
+                      const stlg_grad* d_channels, int64_t B, int64_t T,
+                      const stlg_smooth* smooth_params, const Bufs& bf, float* out,
+                      const float* out_in, const float* cot, double* d_smooth, double* dw64,
+                      cudaStream_t st, bool backward) {
+  if (!smooth_params) return fail(STLG_E_INVALID, "smooth parameters required");
+  const stlg_smooth& sp = smooth_params[e.smooth_slot];
+  std::vector<float> lw2;
+  int i_lo, i_hi;
+  if (!smooth_table(sp, T, lw2, &i_lo, &i_hi))
+    return fail(STLG_E_EMPTY_WINDOW, "smooth interval produced an all-zero weight vector");
+  float* tab = bf.tables + (size_t)e.table * (size_t)T;
+  cudaError_t ce = cudaMemcpyAsync(tab, lw2.data(), sizeof(float) * (size_t)T,
+                                   cudaMemcpyHostToDevice, st);
+  int rc;
+  if ((rc = cuda_status(ce, "weight upload"))) return rc;
+  const int mode = plan->cfg.mode;
+  if (mode == STLG_MODE_HARD) {
+    FGParams p;
+    fill_fg(plan, e, B, T, p);
+    p.a = i_lo;
+    p.b = i_hi;
+    p.K = i_hi - i_lo + 1;
+    p.canon = 0;
+    p.padmode = 1;
+    if ((rc = resolve(plan, e.e1, channels, d_channels, bf, T, backward, p.child))) return rc;
+    if (!backward) {
+      p.out = out;
+      ce = launch_fg_timed_fwd(mode, p, st);
+    } else {
+      p.out_in = out_in;
+      p.cot = cot;
+      p.gbuf = bf.scratch;
+      ce = launch_fg_timed_bwd(mode, p, st);
+    }
+    return cuda_status(ce, "smooth (hard) launch");
+  }
+  SParams p;
+  std::memset(&p, 0, sizeof(p));
+  if ((rc = resolve(plan, e.e1, channels, d_channels, bf, T, backward, p.child))) return rc;
+  p.B = B;
+  p.L = T;
+  p.i_lo = i_lo;
+  p.i_hi = i_hi;
+  p.sg = e.sg;
+  p.pad_last = plan->cfg.pad_last;
+  p.pad_value = (float)plan->cfg.pad_value;
+  p.mp = mode_params(plan->cfg);
+  p.lw2 = tab;
+  if (!backward) {
+    p.out = out;
+    p.aux = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
+    return cuda_status(launch_smooth_fwd(mode, p, st), "smooth launch");
+  }
+  p.out_in = out_in;
+  p.aux_in = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
+  p.cot = cot;
+  p.gbuf = bf.scratch;
+  p.dw64 = d_smooth ? dw64 : nullptr;
+  if (d_smooth) {
+    ce = cudaMemsetAsync(dw64, 0, sizeof(double) * (size_t)T, st);
+    if ((rc = cuda_status(ce, "memset"))) return rc;
+  }
+  if ((rc = cuda_status(launch_smooth_bwd(mode, p, st), "smooth backward launch"))) return rc;
+  if (d_smooth) {
+    ce = launch_smooth_abc(dw64, T, sp.a, sp.b, sp.c, sp.eps, d_smooth + 3 * e.smooth_slot, st);
+    if ((rc = cuda_status(ce, "smooth d(a,b,c)"))) return rc;
+  }
+  return STLG_OK;
 }
 
 int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B, int64_t T,
@@ -554,12 +658,13 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_fwd(mode, p, st);
-    } else {
-      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
+    } else {  // E_FG_SMOOTH
+      if ((rc = run_smooth(plan, e, channels, nullptr, B, T, smooth_params, bf, out, nullptr,
+                           nullptr, nullptr, nullptr, st, false)))
+        return rc;
     }
     if ((rc = cuda_status(ce, "forward launch"))) return rc;
   }
-  (void)smooth_params;
   return STLG_OK;
 }
 
@@ -618,13 +723,13 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.pad_value = (float)plan->cfg.pad_value;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_bwd(mode, p, st);
-    } else {
-      return fail(STLG_E_UNSUPPORTED, "smooth intervals are not implemented on the device yet");
+    } else {  // E_FG_SMOOTH
+      if ((rc = run_smooth(plan, e, channels, d_channels, B, T, smooth_params, bf, nullptr, out_in,
+                           g, d_smooth, (double*)(((uintptr_t)(bf.scratch + 3 * bf.BT) + 7) & ~(uintptr_t)7), st, true)))
+        return rc;
     }
     if ((rc = cuda_status(ce, "backward launch"))) return rc;
   }
-  (void)smooth_params;
-  (void)d_smooth;
   return STLG_OK;
 }
 

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
   const long long row = blockIdx.y;
   const int J = (NB - 1) * K;
   const int t0 = blockIdx.x * J;
-  const int nvalid = L - p.b;
+  const int nvalid = p.padmode ? L : L - p.b;  // padded windows: every output reduces a window
   const int s0 = t0 + p.a;
   const float invK = 1.f / (float)K;
   float* U = sm;
@@ -131,8 +131,10 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const bool any = t0 < nvalid;
+  const float padv0 = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+  const float ufill = p.padmode ? sg * padv0 : -INFINITY;  // samples past the end
 
-  if (threadIdx.x == 0) padv_sh = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+  if (threadIdx.x == 0) padv_sh = padv0;
   if (any) {
     const int n = NB * K;
     for (int i0 = threadIdx.x; i0 < n; i0 += 4 * FG_THREADS) {
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
         int i = i0 + u * FG_THREADS;
         if (i < n) {
           int idx = s0 + i;
-          U[i + div_k(i, K, invK) * dK] = idx < L ? sg * ev.value(idx, r[u]) : -INFINITY;
+          U[i + div_k(i, K, invK) * dK] = idx < L ? sg * ev.value(idx, r[u]) : ufill;
         }
       }
     }
@@ -440,7 +442,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
   const int J = (NB - 1) * K;
   const int j0 = blockIdx.x * J;
   const int s0 = j0 - K + 1;
-  const int nvalid = L - p.b;
+  // padded windows: outputs whose window lies wholly past the end route to c[L-1] via padsum
+  const int nvalid = p.padmode ? L - p.a : L - p.b;
   const float invK = 1.f / (float)K;
   float* U = sm;
   float* PV = sm + nsi;
@@ -450,6 +453,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
   const float sg = p.sg;
   const float* cot = p.cot + row * L;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
+  const float ufill =
+      p.padmode ? sg * (p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value) : -INFINITY;
 
   {
     const int n = NBi * K;
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
         if (i >= n) continue;
         int idx = s0 + i;
         int q = i + div_k(i, K, invK) * dK;
-        U[q] = (idx >= 0 && idx < L) ? sg * ev.value(idx, r[u]) : -INFINITY;
+        U[q] = (idx >= 0 && idx < L) ? sg * ev.value(idx, r[u]) : (idx >= L ? ufill : -INFINITY);
         if (i < NB * K) GT[q] = gv[u];
       }
     }
@@ -518,6 +523,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
       if (i > 0 && PV[nb + i] > av) ri = PI[nb + i];
       float g = GT[b0 + i];
       int jj = s0 + ri;
+      if (jj >= L) jj = p.pad_last ? L - 1 : -1;  // padded samples route to c[L-1] ('last')
       if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
     }
   }
@@ -548,8 +554,12 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
 template <int MODE>
 __global__ void __launch_bounds__(256) k_fg_timed_fwd_direct(const __grid_constant__ FGParams p) {
   const long long row = blockIdx.y, L = p.L;
-  const long long nvalid = L - p.b;
+  const long long nvalid = p.padmode ? L : L - p.b;
   const float tau2 = p.mp.tau2;
+  const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+  auto uval = [&](long long idx) {
+    return p.sg * (idx < L ? expr_eval<MODE>(p.child, row, idx, p.mp) : padv);
+  };
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < L;
        t += (long long)gridDim.x * blockDim.x) {
     float v;
@@ -557,24 +567,22 @@ __global__ void __launch_bounds__(256) k_fg_timed_fwd_direct(const __grid_consta
       if (MODE == M_HARD) {
         float m = -INFINITY;
         for (int k = 0; k < p.K; ++k) {
-          float x = p.sg * expr_eval<MODE>(p.child, row, t + p.a + k, p.mp);
+          float x = uval(t + p.a + k);
           if (x > m) m = x;
         }
         v = p.sg * m;
       } else if (MODE == M_LSE) {
         LseAcc a = {0.f, 0.f};
-        for (int k = 0; k < p.K; ++k)
-          a = lse_push(a, p.sg * expr_eval<MODE>(p.child, row, t + p.a + k, p.mp), tau2);
+        for (int k = 0; k < p.K; ++k) a = lse_push(a, uval(t + p.a + k), tau2);
         v = p.sg * fmaf(lg2f(a.s), p.mp.inv_tau2, a.m);
       } else {
         SoftAcc a = {0.f, 0.f, 0.f};
-        for (int k = 0; k < p.K; ++k)
-          a = soft_push(a, p.sg * expr_eval<MODE>(p.child, row, t + p.a + k, p.mp), tau2);
+        for (int k = 0; k < p.K; ++k) a = soft_push(a, uval(t + p.a + k), tau2);
         v = p.sg * (a.m + a.d / a.s);
         p.aux[row * L + t] = fmaf(lg2f(a.s), p.mp.inv_tau2, a.m);
       }
     } else {
-      v = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+      v = padv;
     }
     if (p.canon) v = __fadd_rn(v, 0.f);
     p.out[row * L + t] = v;
@@ -585,8 +593,12 @@ __global__ void __launch_bounds__(256) k_fg_timed_fwd_direct(const __grid_consta
 template <int MODE>
 __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_constant__ FGParams p) {
   const long long row = blockIdx.y, L = p.L;
-  const long long nvalid = L - p.b;
+  const long long nvalid = p.padmode ? L : L - p.b;
   const float tau2 = p.mp.tau2;
+  const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+  auto uval = [&](long long idx) {
+    return p.sg * (idx < L ? expr_eval<MODE>(p.child, row, idx, p.mp) : padv);
+  };
   float* gb = p.gbuf + row * L;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < L;
        t += (long long)gridDim.x * blockDim.x) {
@@ -598,23 +610,26 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
     }
     if (MODE == M_HARD) {
       float m = -INFINITY;
-      int am = 0;
+      long long am = 0;
       for (int k = 0; k < p.K; ++k) {
-        float x = p.sg * expr_eval<MODE>(p.child, row, t + p.a + k, p.mp);
+        float x = uval(t + p.a + k);
         if (x > m) {
           m = x;
-          am = k;
+          am = t + p.a + k;
         }
       }
-      atomicAdd(gb + t + p.a + am, g);
+      if (am >= L) am = p.pad_last ? L - 1 : -1;
+      if (am >= 0) atomicAdd(gb + am, g);
     } else {
       float M = p.sg * p.out_in[row * L + t];
       float Lt = (MODE == M_SOFT) ? p.aux_in[row * L + t] : M;
       for (int k = 0; k < p.K; ++k) {
-        float x = p.sg * expr_eval<MODE>(p.child, row, t + p.a + k, p.mp);
+        long long idx = t + p.a + k;
+        float x = uval(idx);
         float w = ex2f(tau2 * (x - Lt));
         if (MODE == M_SOFT) w *= fmaf(p.mp.tau, x - M, 1.f);
-        atomicAdd(gb + t + p.a + k, g * w);
+        if (idx >= L) idx = p.pad_last ? L - 1 : -1;
+        if (idx >= 0) atomicAdd(gb + idx, g * w);
       }
     }
   }

@@ -20,6 +20,7 @@ struct FGParams {
   int pad_last;   // PaddingPolicy('last')
   float pad_value;
   int canon;      // reproduce masking.py:192's `+ 0.0` (b > 0 and some window fits)
+  int padmode;    // 1: windows read the padded child (smooth-interval hard path, no overrun rule)
   ModeP mp;
 };
 
@@ -40,24 +41,28 @@ struct UParams {
   ModeP mp;
 };
 
-// Smooth-interval F / G (weighted window of length L over the padded child).
+// Smooth-interval F / G, LSE / softmax (weighted window of length L over the padded child).
 struct SParams {
   DExpr child;
-  const float* out_in;
+  const float* out_in;  // backward: this node's trace
+  const float* aux_in;  // backward, softmax: weighted window LSE
   const float* cot;
   float* out;
-  const double* w;    // weights w_i, i = 0..L-1 (fp64)
-  const float* lw;    // log-weights ln w_i (fp32; -inf where w_i == 0)
-  float* dw;          // backward: per-weight gradient partial sums [n_part, L] (fp32)
-  double* dw64;       // backward: reduced d/dw_i (fp64) [L]
-  float* gbuf;        // backward scratch: cotangent of the child [B, L]
+  float* aux;          // forward, softmax
+  const float* lw2;    // log2 w_i (fp32; -inf where w_i == 0), i = 0..L-1
+  double* dw64;        // backward: d out / d w_i summed over rows and t [L] (fp64, accumulated)
+  float* gbuf;         // backward scratch: cotangent of the child [B, L]
   long long B, L;
-  int i_lo, i_hi;     // kept index range {i : w_i > 0}
+  int i_lo, i_hi;      // kept index range {i : w_i > 0}
   float sg;
   int pad_last;
   float pad_value;
   ModeP mp;
 };
+
+// fp64 weight table and its (a, b, c) partials -> d_abc (one smooth slot)
+cudaError_t launch_smooth_abc(const double* dw64, long long L, double a, double b, double c,
+                              double eps, double* d_abc, cudaStream_t st);
 
 // launchers (return cudaError_t)
 cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st);

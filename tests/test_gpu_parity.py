@@ -171,3 +171,74 @@ def test_duality_exact_on_device(cuda):
             a = P.trace(P.Always(P.Pred("x", ">", 0.2), iv), {"x": x}, cfg)
             b = P.trace(P.Eventually(P.Not(P.Pred("x", ">", 0.2)), iv), {"x": x}, cfg)
             assert torch.equal(a, -b)
+
+
+# --- smooth intervals -----------------------------------------
+
+def _step_dataset(seed, n, length, truth=(0.23, 0.59), noise=0.05):
+    """Noisy step signals as apps.synth_step_dataset (apps.py:252-269)."""
+    import math
+    rng = np.random.default_rng(seed)
+    lo, hi = int(math.ceil(truth[0] * length)), int(math.floor(truth[1] * length))
+    data = np.zeros((n, length))
+    for r in range(n):
+        jlo = lo + int(rng.integers(-1, 2))
+        jhi = hi + int(rng.integers(-1, 2))
+        data[r, max(jlo, 0):min(jhi, length - 1) + 1] = 1.0
+    data += rng.normal(0.0, noise, (n, length))
+    return np.asarray(data, dtype=np.float32)
+
+
+@pytest.mark.parametrize("mode", [P.Hard(), P.LogSumExp(5.0), P.SoftMax(2.0)])
+@pytest.mark.parametrize("pad", [P.PaddingPolicy.last_value(), P.PaddingPolicy.constant(-0.25)])
+def test_smooth_interval_vs_oracle(cuda, mode, pad):
+    rng = np.random.default_rng(77)
+    B, L = 5, 300
+    x = np.asarray(rng.normal(0, 1, (B, L)), dtype=np.float32).astype(np.float64)
+    y = np.asarray(rng.normal(0, 1, (B, L)), dtype=np.float32).astype(np.float64)
+    si = P.SmoothInterval(0.3, 0.65, 9.0)
+    f = P.And(P.Always(P.Pred("x", ">", 0.0), si), P.Eventually(P.Pred("y", ">", -0.5), si))
+    cfg = P.SemanticsConfig(mode=mode, padding=pad)
+    binding = (si.a, si.b, si.c)
+    ref_tr, ref_g, ref_abc = stl_oracle.trace_and_grad(f, {"x": x, "y": y}, cfg,
+                                                       smooth_binding=binding)
+    tr, g, dabc = run_device(f, {"x": x, "y": y}, cfg, None, binding)
+    _check(type(mode).__name__, tr, g, ref_tr, ref_g, np.ones_like(tr), dabc,
+           None if type(mode).__name__ == "Hard" else np.array(ref_abc))
+    if type(mode).__name__ == "Hard":
+        assert np.all(dabc == 0.0)
+
+
+def test_c4_full_size(cuda):
+    """C4: G_smooth(0.3, 0.65, c=9)(x > 0), LSE(5), B=4096, T=2000; rows vs oracle and
+    d(a,b,c) additivity over batch shards (the quantity the multi-GPU path all-reduces)."""
+    import torch
+    B, T = 4096, 2000
+    data = _step_dataset(3, B, T)
+    si = P.SmoothInterval(0.3, 0.65, 9.0)
+    f = P.Always(P.Pred("x", ">", 0.0), si)
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(5.0))
+    dev = torch.device("cuda", 0)
+
+    def run(rows):
+        xt = torch.tensor(data[rows], device=dev).requires_grad_(True)
+        abc = tuple(torch.tensor(v, dtype=torch.float64, device=dev, requires_grad=True)
+                    for v in (si.a, si.b, si.c))
+        out = P.trace(f, {"x": xt}, cfg, smooth_binding=abc)
+        gs = torch.autograd.grad(out, [xt, *abc], torch.ones_like(out))
+        return out.detach(), gs[0], np.array([float(v) for v in gs[1:]])
+
+    out, gx, dabc = run(slice(0, B))
+    for r in (0, 2047, 4095):
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": data[r:r + 1].astype(np.float64)}, cfg,
+                                                     smooth_binding=(si.a, si.b, si.c))
+        assert rel_err(out[r:r + 1].double().cpu().numpy(), ref_tr) <= SMOOTH_TOL
+        assert rel_err(gx[r:r + 1].double().cpu().numpy(), ref_g["x"]) <= SMOOTH_TOL
+    _, _, d1 = run(slice(0, B // 2))
+    _, _, d2 = run(slice(B // 2, B))
+    assert rel_err(d1 + d2, dabc) <= 1e-6
+    # small-batch d(a,b,c) against the oracle
+    ref_tr, ref_g, ref_abc = stl_oracle.trace_and_grad(f, {"x": data[:4].astype(np.float64)}, cfg,
+                                                       smooth_binding=(si.a, si.b, si.c))
+    _, _, d4 = run(slice(0, 4))
+    assert rel_err(d4, np.array(ref_abc)) <= SMOOTH_TOL

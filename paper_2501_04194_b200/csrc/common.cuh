@@ -371,6 +371,33 @@ __device__ __forceinline__ void gs_add(float& mu, float& A, float& Bc, float& c,
   c = skip ? c : (empty ? c2 : nc);
 }
 
+// masked_fill compat (masking.py:195-202): the column holds the window plus
+// nu sentinel entries (-sent in max space), `sent_first` if some sit before the
+// window.  Merges them into the window result M (and its LSE `lse` for
+// softmax); returns false when the sentinel wins in hard mode (no gradient).
+template <int MODE>
+__device__ __forceinline__ bool fill_merge(float& M, float& lse, float nu, float sent,
+                                           bool sent_first, float tau2, float itau2) {
+  if (nu <= 0.f) return true;
+  const float ms = -sent;
+  if (MODE == M_HARD) {
+    if (M > ms || (M == ms && !sent_first)) return true;
+    M = ms;
+    return false;
+  }
+  if (MODE == M_LSE) {
+    float m = M, s = 1.f;
+    lse_merge(m, s, ms, nu, tau2);
+    M = fmaf(lg2f(s), itau2, m);
+    return true;
+  }
+  float m = lse, s = 1.f, q = M - lse;
+  soft_merge(m, s, q, ms, nu, 0.f, tau2);
+  M = m + q / s;
+  lse = fmaf(lg2f(s), itau2, m);
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // evaluators.  The single-leaf kinds (the common case: a Pred / NormPred / a
 // materialised trace directly under a temporal operator) are compile-time

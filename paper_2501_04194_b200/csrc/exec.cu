@@ -434,10 +434,6 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     } else {
       e.kind = e.untimed ? E_FG_UNTIMED : E_FG_TIMED;
     }
-    if (nd.op != STLG_UNTIL && cfg->masked_fill) {
-      // masked_fill compat reduces sentinel-filled columns (masking.py:195-202)
-      if (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) e.kind = E_FG_TIMED;
-    }
     C.build(nd.left, 1.f, e.e1);
     if (nd.op == STLG_UNTIL) C.build(nd.right, 1.f, e.e2);
     if (!C.fits(e.e1) || (nd.op == STLG_UNTIL && !C.fits(e.e2))) {
@@ -468,9 +464,9 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
   }
   if (cfg->masked_fill) {
     for (auto& e : plan->entries)
-      if (e.kind != E_POINTWISE) {
+      if (e.kind == E_UNTIL) {
         delete plan;
-        return fail(STLG_E_UNSUPPORTED, "masked_fill is not supported on the device path yet");
+        return fail(STLG_E_UNSUPPORTED, "masked_fill Until is not supported on the device path yet");
       }
   }
   mark_first_writers(plan);
@@ -541,6 +537,13 @@ static void fill_fg(const stlg_plan* plan, const Entry& e, int64_t B, int64_t T,
   p.pad_value = (float)plan->cfg.pad_value;
   p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
   p.mp = mode_params(plan->cfg);
+  p.sent = (float)plan->cfg.sentinel;
+  if (plan->cfg.masked_fill && (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED)) {
+    // sentinel-filled columns over the b-padded child, no overrun rule (masking.py:229-232)
+    p.fill = 1;
+    p.canon = 0;
+    if (e.kind == E_FG_TIMED) p.padmode = 1;
+  }
 }
 
 // Smooth-interval F / G: hard mode is the vHGW window kernel over the kept

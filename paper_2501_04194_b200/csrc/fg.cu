@@ -239,10 +239,19 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
   for (int i = threadIdx.x; i < tend; i += FG_THREADS) {
     int t = t0 + i;
     int q = i + div_k(i, K, invK) * dK;
-    float v = (t < nvalid) ? sg * U[q] : padv;
+    float v;
+    if (t < nvalid) {
+      float M = U[q];
+      float lse = (MODE == M_SOFT) ? AX[q] : 0.f;
+      if (p.fill)  // columns of L + b rows: K kept, the rest sentinel (t + a of them first)
+        fill_merge<MODE>(M, lse, (float)(L + p.b - K), p.sent, t + p.a > 0, tau2, itau2);
+      v = sg * M;
+      if (MODE == M_SOFT) auxr[t] = lse;
+    } else {
+      v = padv;
+    }
     if (p.canon) v = __fadd_rn(v, 0.f);
     outr[t] = v;
-    if (MODE == M_SOFT && t < nvalid) auxr[t] = AX[q];
   }
 }
 
@@ -481,7 +490,9 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
     }
   }
   for (int i = threadIdx.x; i < J; i += FG_THREADS) G[i] = 0.f;
-  const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J);
+  // all-pad windows route to c[L-1]; in fill mode only if the pad beats the sentinel
+  const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J) &&
+                        !(p.fill && ufill <= -p.sent);
   float padsum = 0.f;
   if (own_last) {
     float s = 0.f;
@@ -520,8 +531,17 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
       av = up ? x : av;
       ai = up ? qb * K + i : ai;
       int ri = ai;
-      if (i > 0 && PV[nb + i] > av) ri = PI[nb + i];
+      float rv = av;
+      if (i > 0 && PV[nb + i] > av) {
+        ri = PI[nb + i];
+        rv = PV[nb + i];
+      }
       float g = GT[b0 + i];
+      if (p.fill) {  // the sentinel wins: no gradient (mask_fill cuts it, tape.py:229-234)
+        float lse0 = 0.f;
+        if (!fill_merge<M_HARD>(rv, lse0, (float)(L + p.b - K), p.sent, s0 + qb * K + i > 0, 0.f, 0.f))
+          g = 0.f;
+      }
       int jj = s0 + ri;
       if (jj >= L) jj = p.pad_last ? L - 1 : -1;  // padded samples route to c[L-1] ('last')
       if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
@@ -584,6 +604,12 @@ __global__ void __launch_bounds__(256) k_fg_timed_fwd_direct(const __grid_consta
     } else {
       v = padv;
     }
+    if (p.fill && t < nvalid) {
+      float M = p.sg * v, lse = (MODE == M_SOFT) ? p.aux[row * L + t] : 0.f;
+      fill_merge<MODE>(M, lse, (float)(L + p.b - p.K), p.sent, t + p.a > 0, tau2, p.mp.inv_tau2);
+      v = p.sg * M;
+      if (MODE == M_SOFT) p.aux[row * L + t] = lse;
+    }
     if (p.canon) v = __fadd_rn(v, 0.f);
     p.out[row * L + t] = v;
   }
@@ -619,6 +645,11 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
         }
       }
       if (am >= L) am = p.pad_last ? L - 1 : -1;
+      if (p.fill) {
+        float lse0 = 0.f;
+        if (!fill_merge<M_HARD>(m, lse0, (float)(L + p.b - p.K), p.sent, t + p.a > 0, 0.f, 0.f))
+          am = -1;
+      }
       if (am >= 0) atomicAdd(gb + am, g);
     } else {
       float M = p.sg * p.out_in[row * L + t];
@@ -835,7 +866,11 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_fwd(const __grid_constant__
       carry = nc;
       for (int k = tid; k < UT_CH; k += UT_T) {
         long long t = c0 + k;
-        if (t < L) p.out[row * L + t] = p.sg * u[upos(k)];
+        if (t < L) {
+          float M = u[upos(k)], lse0 = 0.f;
+          if (p.fill) fill_merge<M_HARD>(M, lse0, (float)t, p.sent, t > 0, 0.f, 0.f);
+          p.out[row * L + t] = p.sg * M;
+        }
       }
       __syncthreads();
     }
@@ -866,7 +901,11 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_fwd(const __grid_constant__
       carry = nc;
       for (int k = tid; k < UT_CH; k += UT_T) {
         long long t = c0 + k;
-        if (t < L) p.out[row * L + t] = p.sg * u[upos(k)];
+        if (t < L) {
+          float M = u[upos(k)], lse0 = 0.f;
+          if (p.fill) fill_merge<M_LSE>(M, lse0, (float)t, p.sent, t > 0, tau2, p.mp.inv_tau2);
+          p.out[row * L + t] = p.sg * M;
+        }
       }
       __syncthreads();
     }
@@ -899,8 +938,10 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_fwd(const __grid_constant__
       for (int k = tid; k < UT_CH; k += UT_T) {
         long long t = c0 + k;
         if (t < L) {
-          p.out[row * L + t] = p.sg * u[upos(k)];
-          p.aux[row * L + t] = ax[upos(k)];
+          float M = u[upos(k)], lse = ax[upos(k)];
+          if (p.fill) fill_merge<M_SOFT>(M, lse, (float)t, p.sent, t > 0, tau2, p.mp.inv_tau2);
+          p.out[row * L + t] = p.sg * M;
+          p.aux[row * L + t] = lse;
         }
       }
       __syncthreads();
@@ -1043,6 +1084,10 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_bwd_hard(const __grid_const
       if (t >= L) continue;
       acc = comb(HardAcc{u[tid * UT_S + e], (int)t}, acc);
       float g = cot[t];
+      if (p.fill) {
+        float M = acc.v, lse0 = 0.f;
+        if (!fill_merge<M_HARD>(M, lse0, (float)t, p.sent, t > 0, 0.f, 0.f)) g = 0.f;
+      }
       if (acc.i != run_idx) {
         if (run_idx >= 0 && run_sum != 0.f) atomicAdd(gb + run_idx, run_sum);
         run_idx = acc.i;

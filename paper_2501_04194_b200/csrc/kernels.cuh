@@ -21,6 +21,8 @@ struct FGParams {
   float pad_value;
   int canon;      // reproduce masking.py:192's `+ 0.0` (b > 0 and some window fits)
   int padmode;    // 1: windows read the padded child (smooth-interval hard path, no overrun rule)
+  int fill;       // masked_fill compat: reduce sentinel-filled full columns (masking.py:195-202)
+  float sent;     // SemanticsConfig.sentinel
   ModeP mp;
 };
 

@@ -84,6 +84,19 @@ __device__ __forceinline__ float rcpf(float x) {
 // ---------------------------------------------------------------------------
 // expression evaluation
 // ---------------------------------------------------------------------------
+// streaming loads that do not allocate in L1: the pipelined kernels give most of
+// the unified L1 to shared memory, and L1-allocating loads then cap the bytes in flight
+__device__ __forceinline__ float ld_na(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ld_na2(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ float ld_src(const DSrc& s, long long b, long long j) {
   return __ldg(s.p + b * s.rs + j * s.es);
 }
@@ -404,7 +417,7 @@ __device__ __forceinline__ bool fill_merge(float& M, float& lse, float nu, float
 // specialisations with the row's pointers hoisted into registers; EK_GEN
 // interprets any fused expression.  Element indices are row-relative ints.
 // ---------------------------------------------------------------------------
-enum ExprKind { EK_GEN = 0, EK_AFF = 1, EK_NORM = 2, EK_SRC = 3 };
+enum ExprKind { EK_GEN = 0, EK_AFF = 1, EK_NORM = 2, EK_SRC = 3, EK_PAIR = 4 };
 
 __device__ __forceinline__ float sqrt_fast(float x) {
   float y;
@@ -476,7 +489,7 @@ struct Ev<MODE, EK_AFF> : LeafRegs {
     float x;
   };
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
-  __device__ __forceinline__ Raw load(int j) const { return Raw{__ldg(p1 + (long long)j * es1)}; }
+  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + (long long)j * es1)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * (s_out * s_in), st1); }
 };
@@ -487,7 +500,7 @@ struct Ev<MODE, EK_SRC> : LeafRegs {
     float x;
   };
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
-  __device__ __forceinline__ Raw load(int j) const { return Raw{__ldg(p1 + (long long)j * es1)}; }
+  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + (long long)j * es1)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * r.x; }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * s_out, st1); }
 };
@@ -497,9 +510,12 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
   struct Raw {
     float x, y;
   };
-  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
+  bool pair;  // (x, y) interleaved in one [.., T, 2] tensor: one 8-byte load per sample
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {
+    pair = (p2 == p1 + 1) && es1 == 2 && es2 == 2 && ((reinterpret_cast<uintptr_t>(p1) & 7) == 0);
+  }
   __device__ __forceinline__ Raw load(int j) const {
-    return Raw{__ldg(p1 + (long long)j * es1), __ldg(p2 + (long long)j * es2)};
+    return Raw{ld_na(p1 + (long long)j * es1), ld_na(p2 + (long long)j * es2)};
   }
   __device__ __forceinline__ float value(int, Raw r) const {
     float dx = r.x - cx, dy = r.y - cy;
@@ -511,6 +527,40 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
     float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
     put(g1, ges1, j, dx * sc, st1);
     put(g2, ges2, j, dy * sc, st2);
+  }
+};
+
+// NormPred over an interleaved (x, y) pair ([.., T, 2] tensor): one 8-byte load
+// per sample and, when both gradients are stored into an interleaved buffer,
+// one 8-byte store.
+template <int MODE>
+struct Ev<MODE, EK_PAIR> : LeafRegs {
+  struct Raw {
+    float x, y;
+  };
+  bool gpair;
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {
+    gpair = g1 != nullptr && g2 == g1 + 1 && ges1 == 2 && ges2 == 2 && st1 && st2 &&
+            ((reinterpret_cast<uintptr_t>(g1) & 7) == 0);
+  }
+  __device__ __forceinline__ Raw load(int j) const {
+    float2 v = ld_na2(reinterpret_cast<const float2*>(p1) + j);
+    return Raw{v.x, v.y};
+  }
+  __device__ __forceinline__ float value(int, Raw r) const {
+    float dx = r.x - cx, dy = r.y - cy;
+    return s_out * __fadd_rn(s_in * sqrt_fast(fmaf(dx, dx, dy * dy)), c);
+  }
+  __device__ __forceinline__ void grad(int j, Raw r, float g) const {
+    float dx = r.x - cx, dy = r.y - cy;
+    float d2 = fmaf(dx, dx, dy * dy);
+    float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
+    if (gpair) {
+      reinterpret_cast<float2*>(g1)[j] = make_float2(dx * sc, dy * sc);
+    } else {
+      put(g1, ges1, j, dx * sc, st1);
+      put(g2, ges2, j, dy * sc, st2);
+    }
   }
 };
 
@@ -531,7 +581,13 @@ __host__ __device__ inline int expr_kind(const DExpr& e) {
   if (e.n_step != 1) return EK_GEN;
   int k = e.leaf[0].kind;
   if (k == LEAF_AFFINE) return EK_AFF;
-  if (k == LEAF_NORM) return EK_NORM;
+  if (k == LEAF_NORM) {
+    const DSrc& a = e.src[e.leaf[0].src];
+    const DSrc& b = e.src[e.leaf[0].src2];
+    bool pair = b.p == a.p + 1 && a.es == 2 && b.es == 2 && a.rs == b.rs && (a.rs % 2 == 0) &&
+                ((reinterpret_cast<uintptr_t>(a.p) & 7) == 0);
+    return pair ? EK_PAIR : EK_NORM;
+  }
   if (k == LEAF_SRC) return EK_SRC;
   return EK_GEN;
 }

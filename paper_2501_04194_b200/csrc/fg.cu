@@ -25,6 +25,8 @@
 // softmax) or by scattering each g_t to its recomputed arg-max in shared
 // memory (hard), then runs the child expression's VJP at j — so the
 // cotangent of an elementwise child is never materialised.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace stlg {
@@ -671,10 +673,31 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
 // ===========================================================================
 static int odd_stride(int K) { return K | 1; }
 
+// STLG_PIPE=0 selects the non-pipelined timed kernels (A/B measurements)
+bool pipe_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("STLG_PIPE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// raise the dynamic shared-memory limit once per (kernel, size)
 template <typename KernT>
 static cudaError_t set_smem(KernT k, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static thread_local const void* done_fn[64];
+  static thread_local size_t done_sz[64];
+  static thread_local int n_done = 0;
+  for (int i = 0; i < n_done; ++i)
+    if (done_fn[i] == (const void*)k && done_sz[i] >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && n_done < 64) {
+    done_fn[n_done] = (const void*)k;
+    done_sz[n_done++] = bytes;
+  }
+  return e;
 }
 
 static const size_t kSmemBudget = 56 * 1024;  // per CTA: 4 CTAs x 256 threads per SM
@@ -709,6 +732,9 @@ static bool use_direct(int K, int mode) {
   } else if ((EKV) == EK_SRC) {        \
     constexpr int EK = EK_SRC;         \
     __VA_ARGS__;                       \
+  } else if ((EKV) == EK_PAIR) {       \
+    constexpr int EK = EK_PAIR;        \
+    __VA_ARGS__;                       \
   } else {                             \
     constexpr int EK = EK_GEN;         \
     __VA_ARGS__;                       \
@@ -731,13 +757,17 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
     count_launch();
     return cudaGetLastError();
   }
+  const int ek = expr_kind(p.child);
+  cudaError_t e;
+  if (pipe_enabled()) {
+    e = launch_fgt_fwd_pipe(mode, ek, p, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
   p.Kp = odd_stride(p.K);
   p.NB = pick_nb(p.K, fwd_words(mode));
   long long J = (long long)(p.NB - 1) * p.K;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
   size_t smem = (size_t)fwd_words(mode) * p.NB * p.Kp * 4;
-  const int ek = expr_kind(p.child);
-  cudaError_t e;
   if (mode == M_HARD) {
     DISPATCH_EK(ek, e = (fwd_v2<M_HARD, EK>(p, smem, grid, st)))
   } else if (mode == M_LSE) {
@@ -790,6 +820,10 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
     DISPATCH_EK(ek, e = (bwd_hard_v2<EK>(p, smem, grid, st)))
     count_launch();
     return e;
+  }
+  if (pipe_enabled()) {
+    e = launch_fgt_bwd_pipe(mode, ek, p, st);
+    if (e != cudaErrorNotSupported) return e;
   }
   const int words = bwd_words(mode);
   int nb = pick_nb(p.K, words);

@@ -1,0 +1,745 @@
+// fg_pipe.cu — persistent, warp-specialised timed Eventually / Always kernels.
+//
+// Same algorithm as fg.cu's k_fgt_fwd / k_fgt_bwd_sm (van Herk / Gil-Werman
+// blocks of K = b - a + 1, one scanner thread per block), restructured so the
+// memory traffic overlaps the sequential block scans:
+//
+//   * CTAs are persistent; each walks the (row, time-tile) list with stride
+//     gridDim.x.
+//   * Warps 0 .. SW-1 ("scanners", one thread per vHGW block) scan tile s in
+//     shared buffer s & 1.
+//   * The other warps ("movers") meanwhile write tile s-1's results out of
+//     buffer (s-1) & 1 (forward: the trace; backward: the child VJP), then
+//     load tile s+1 into that same buffer.
+//   * One CTA barrier per stage; a named barrier among scanners between the
+//     prefix and the suffix pass, one among movers between store and load.
+//
+// The profile of the non-pipelined kernels showed 6 of 8 warps stalled on the
+// CTA barrier while two warps scanned (profiles/r1_c2_ncu_summary.md).
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace stlg {
+
+constexpr int PIPE_THREADS = 256;
+constexpr int PIPE_UNROLL = 8;
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ===========================================================================
+// forward
+// ===========================================================================
+// Shared: U[2][NB*Kp] (child in max space -> outputs), P1[NB*Kp] prefix,
+//         soft: P2[NB*Kp] prefix LSE, AX[2][NB*Kp] window LSE.
+template <int MODE, int EK>
+__global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_fwd_pipe(const __grid_constant__ FGParams p,
+                                                               int tiles_per_row, long long total) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float padv_sh[2];
+  __shared__ float rng_sh[2][2][8];  // per buffer: {max, min} of the tile's samples, per mover warp
+  const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
+  const int nsm = NB * Kp;
+  const int L = (int)p.L;
+  const int J = (NB - 1) * K;
+  const int nvalid = p.padmode ? L : L - p.b;
+  const float invK = 1.f / (float)K;
+  const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
+  const int SWT = ((NB + 31) >> 5) << 5;
+  const int NMOV = PIPE_THREADS - SWT;
+  const bool scanner = (int)threadIdx.x < SWT;
+  const int mid = (int)threadIdx.x - SWT;
+  // buffer b: U at sm + b * nsm, AX at sm + (4 + b) * nsm (arithmetic, so the
+  // compiler keeps shared-memory addressing; a pointer array demotes to generic loads)
+  float* P1 = sm + 2 * nsm;
+  float* P2 = sm + 3 * nsm;
+  const long long n = (total - (long long)blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  auto tile_of = [&](long long s, long long& row, int& t0) {
+    long long tau = (long long)blockIdx.x + s * gridDim.x;
+    row = tau / tiles_per_row;
+    t0 = (int)(tau - row * tiles_per_row) * J;
+  };
+
+  auto load = [&](long long s, int b) {  // movers
+    long long row;
+    int t0;
+    tile_of(s, row, t0);
+    Ev<MODE, EK> ev(p.child, row, p.mp);
+    const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+    if (mid == 0) padv_sh[b] = padv;
+    float hi = -INFINITY, lo = INFINITY;  // dynamic range of the tile (LSE fast path)
+    if (t0 < nvalid) {
+      float* U = sm + b * nsm;
+      const float ufill = p.padmode ? sg * padv : -INFINITY;
+      const int s0 = t0 + p.a, nn = NB * K;
+      int i0 = mid;
+      if (dK == 0 && s0 + nn <= L) {  // interior tile, unpadded layout: no per-sample checks
+        const int step = PIPE_UNROLL * NMOV;
+        const int nmain = (nn / step) * step;
+        for (; i0 < nmain; i0 += step) {
+          typename Ev<MODE, EK>::Raw r[PIPE_UNROLL];
+#pragma unroll
+          for (int u = 0; u < PIPE_UNROLL; ++u) r[u] = ev.load(s0 + i0 + u * NMOV);
+#pragma unroll
+          for (int u = 0; u < PIPE_UNROLL; ++u) {
+            float v = sg * ev.value(s0 + i0 + u * NMOV, r[u]);
+            U[i0 + u * NMOV] = v;
+            if (MODE == M_LSE) {
+              hi = fmaxf(hi, v);
+              lo = fminf(lo, v);
+            }
+          }
+        }
+      }
+      for (; i0 < nn; i0 += PIPE_UNROLL * NMOV) {
+        typename Ev<MODE, EK>::Raw r[PIPE_UNROLL];
+#pragma unroll
+        for (int u = 0; u < PIPE_UNROLL; ++u) {
+          int i = i0 + u * NMOV;
+          if (i < nn && s0 + i < L) r[u] = ev.load(s0 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < PIPE_UNROLL; ++u) {
+          int i = i0 + u * NMOV;
+          if (i < nn) {
+            float v = (s0 + i < L) ? sg * ev.value(s0 + i, r[u]) : ufill;
+            U[dK ? i + div_k(i, K, invK) : i] = v;
+            if (MODE == M_LSE && v > -INFINITY) {
+              hi = fmaxf(hi, v);
+              lo = fminf(lo, v);
+            }
+          }
+        }
+      }
+    }
+    if (MODE == M_LSE) {
+      for (int o = 16; o > 0; o >>= 1) {
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      }
+      if ((mid & 31) == 0) {
+        rng_sh[b][0][mid >> 5] = hi;
+        rng_sh[b][1][mid >> 5] = lo;
+      }
+    }
+  };
+
+  auto store = [&](long long s, int b) {  // movers
+    long long row;
+    int t0;
+    tile_of(s, row, t0);
+    const float padv = padv_sh[b];
+    const float* U = sm + b * nsm;
+    const float* AX = sm + (4 + b) * nsm;
+    const int tend = (t0 + J < L ? t0 + J : L) - t0;
+    float* outr = p.out + row * L;
+    float* auxr = (MODE == M_SOFT) ? p.aux + row * L : nullptr;
+    int i = mid;
+    if (MODE != M_SOFT && dK == 0 && !p.fill && t0 + tend <= nvalid) {  // interior outputs
+      const int canon = p.canon;
+      for (; i + 3 * NMOV < tend; i += 4 * NMOV) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = sg * U[i + u * NMOV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) outr[t0 + i + u * NMOV] = canon ? __fadd_rn(v[u], 0.f) : v[u];
+      }
+    }
+    for (; i < tend; i += NMOV) {
+      const int t = t0 + i;
+      const int q = dK ? i + div_k(i, K, invK) : i;
+      float v;
+      if (t < nvalid) {
+        float M = U[q];
+        float lse = (MODE == M_SOFT) ? AX[q] : 0.f;
+        if (p.fill) fill_merge<MODE>(M, lse, (float)(L + p.b - K), p.sent, t + p.a > 0, tau2, itau2);
+        v = sg * M;
+        if (MODE == M_SOFT) auxr[t] = lse;
+      } else {
+        v = padv;
+      }
+      if (p.canon) v = __fadd_rn(v, 0.f);
+      outr[t] = v;
+    }
+  };
+
+  // Scans load their inputs in register chunks of SC ahead of the stores: the
+  // prefix / output arrays may alias the inputs as far as the compiler knows, so
+  // per-element load-after-store would serialise every step on shared latency.
+  constexpr int SC = 8;
+  auto scan = [&](long long s, int b) {  // scanners
+    long long row;
+    int t0;
+    tile_of(s, row, t0);
+    const bool any = t0 < nvalid;
+    float* U = sm + b * nsm;
+    if (MODE == M_LSE) {
+      // Fast path: one shift c (the tile max) for every window of the tile, so the
+      // block scans are plain sums of E_i = 2^{tau2 (u_i - c)}.  Valid while the
+      // tile's range keeps every E_i a normal float (tau2 * range <= 100); else
+      // the exact max-shifted monoid path below.
+      float c = -INFINITY, lo = INFINITY;
+      for (int w = 0; w < NMOV / 32; ++w) {
+        c = fmaxf(c, rng_sh[b][0][w]);
+        lo = fminf(lo, rng_sh[b][1][w]);
+      }
+      if (c >= lo && (c - lo) * tau2 <= 100.f) {
+        if (any && (int)threadIdx.x < NB) {
+          float* u = U + threadIdx.x * Kp;
+          float* q1 = P1 + threadIdx.x * Kp;
+          float acc = 0.f;
+          for (int i = 0; i < K; i += SC) {
+            float x[SC];
+#pragma unroll
+            for (int k = 0; k < SC; ++k) x[k] = (i + k < K) ? u[i + k] : -INFINITY;
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              if (i + k >= K) break;
+              float e = ex2f(tau2 * (x[k] - c));
+              u[i + k] = e;
+              acc += e;
+              q1[i + k] = acc;
+            }
+          }
+        }
+        named_bar(1, SWT);
+        if (any && (int)threadIdx.x < NB - 1) {
+          float* u = U + threadIdx.x * Kp;
+          const float* n1 = P1 + (threadIdx.x + 1) * Kp - 1;
+          float acc = 0.f;
+          for (int i = K - 1; i >= 0; i -= SC) {
+            float x[SC], y[SC];
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              const int j = i - k;
+              x[k] = (j >= 0) ? u[j] : 0.f;
+              y[k] = (j > 0) ? n1[j] : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              const int j = i - k;
+              if (j < 0) break;
+              acc += x[k];
+              u[j] = fmaf(lg2f(acc + y[k]), itau2, c);
+            }
+          }
+        }
+        return;
+      }
+    }
+    if (any && (int)threadIdx.x < NB) {  // prefix of own block
+      const float* u = U + threadIdx.x * Kp;
+      float* q1 = P1 + threadIdx.x * Kp;
+      float* q2 = P2 + threadIdx.x * Kp;
+      float m = u[0], sacc = 1.f, q = 0.f;
+      q1[0] = m;
+      if (MODE == M_SOFT) q2[0] = m;
+      for (int i = 1; i < K; i += SC) {
+        float x[SC];
+#pragma unroll
+        for (int k = 0; k < SC; ++k) x[k] = (i + k < K) ? u[i + k] : 0.f;
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          if (i + k >= K) break;
+          if (MODE == M_HARD) {
+            m = (x[k] > m) ? x[k] : m;
+            q1[i + k] = m;
+          } else if (MODE == M_LSE) {
+            lse_add(m, sacc, x[k], tau2);
+            q1[i + k] = fmaf(lg2f(sacc), itau2, m);
+          } else {
+            soft_add(m, sacc, q, x[k], tau2);
+            q1[i + k] = m + q / sacc;
+            q2[i + k] = fmaf(lg2f(sacc), itau2, m);
+          }
+        }
+      }
+    }
+    named_bar(1, SWT);
+    if (any && (int)threadIdx.x < NB - 1) {  // suffix walk + combine with the next block's prefix
+      float* u = U + threadIdx.x * Kp;
+      const float* n1 = P1 + (threadIdx.x + 1) * Kp - 1;  // n1[i] = next block prefix at i-1
+      const float* n2 = P2 + (threadIdx.x + 1) * Kp - 1;
+      float* ax = sm + (4 + b) * nsm + threadIdx.x * Kp;
+      float m = u[K - 1], sacc = 1.f, q = 0.f;
+      for (int i = K - 1; i >= 0; i -= SC) {
+        float x[SC], y[SC], z[SC];
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          const int j = i - k;
+          x[k] = (j >= 0) ? u[j] : 0.f;
+          y[k] = (j > 0) ? n1[j] : 0.f;
+          z[k] = (MODE == M_SOFT && j > 0) ? n2[j] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          const int j = i - k;
+          if (j < 0) break;
+          if (MODE == M_HARD) {
+            m = (x[k] >= m) ? x[k] : m;  // walking backwards: ties keep the earlier sample
+            float r = m;
+            if (j > 0) r = (y[k] > r) ? y[k] : r;
+            u[j] = r;
+          } else if (MODE == M_LSE) {
+            if (j < K - 1) lse_add(m, sacc, x[k], tau2);
+            float mm = m, ss = sacc;
+            if (j > 0) lse_merge(mm, ss, y[k], 1.f, tau2);
+            u[j] = fmaf(lg2f(ss), itau2, mm);
+          } else {
+            if (j < K - 1) soft_add(m, sacc, q, x[k], tau2);
+            float mm = m, ss = sacc, qq = q;
+            if (j > 0) soft_merge(mm, ss, qq, z[k], 1.f, y[k] - z[k], tau2);
+            u[j] = mm + qq / ss;
+            ax[j] = fmaf(lg2f(ss), itau2, mm);
+          }
+        }
+      }
+    }
+  };
+
+  const bool do_scan = p.dbg_skip != 1, do_move = p.dbg_skip != 2;
+  if (!scanner && n > 0 && do_move) load(0, 0);
+  __syncthreads();
+  for (long long s = 0; s < n; ++s) {
+    const int b = (int)(s & 1);
+    if (scanner) {
+      if (do_scan) scan(s, b);
+    } else {
+      if (s >= 1 && do_move) store(s - 1, b ^ 1);
+      named_bar(2, NMOV);
+      if (s + 1 < n && do_move) load(s + 1, b ^ 1);
+    }
+    __syncthreads();
+  }
+  if (!scanner && n > 0 && do_move) store(n - 1, (int)((n - 1) & 1));
+}
+
+// ===========================================================================
+// backward, LSE / softmax
+// ===========================================================================
+// Shared (stride Kp): H[2] = {HM, HG[, HC, HB]} per buffer, P = {PM, PA[, PB, PC]}.
+template <int MODE, int EK>
+__global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_bwd_pipe(const __grid_constant__ FGParams p,
+                                                               int tiles_per_row, long long total) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float padsum_sh[2];
+  __shared__ float rng_sh[2][2][8];  // per buffer: {max, min} of M_t over live outputs, per mover warp
+  constexpr int HW = (MODE == M_SOFT) ? 4 : 2;  // words per state
+  const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
+  const int nsm = NB * Kp;
+  const int L = (int)p.L;
+  const int J = (NB - 1) * K;
+  const int nvalid = L - p.b;
+  const float invK = 1.f / (float)K;
+  const float tau2 = p.mp.tau2, tau = p.mp.tau, sg = p.sg;
+  const int SWT = ((NB + 31) >> 5) << 5;
+  const int NMOV = PIPE_THREADS - SWT;
+  const bool scanner = (int)threadIdx.x < SWT;
+  const int mid = (int)threadIdx.x - SWT;
+  float* PM = sm + 2 * HW * nsm;  // buffer b's H arrays start at sm + b * HW * nsm
+  float* PA = PM + nsm;
+  float* PB = PA + nsm;
+  float* PC = PB + nsm;
+  const long long n = (total - (long long)blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  auto tile_of = [&](long long s, long long& row, int& j0) {
+    long long tau_ = (long long)blockIdx.x + s * gridDim.x;
+    row = tau_ / tiles_per_row;
+    j0 = (int)(tau_ - row * tiles_per_row) * J;
+  };
+
+  auto load = [&](long long s, int b) {  // movers: cotangent states of outputs t in [j0 - b, ...)
+    long long row;
+    int j0;
+    tile_of(s, row, j0);
+    float* HM = sm + b * HW * nsm;
+    float* HG = HM + nsm;
+    float* HC = HG + nsm;
+    float* HB = HC + nsm;
+    const float* cot = p.cot + row * L;
+    const float* outr = p.out_in + row * L;
+    const float* auxr = (MODE == M_SOFT) ? p.aux_in + row * L : nullptr;
+    const int tb = j0 - p.b, nn = NB * K;
+    float hi = -INFINITY, lo = INFINITY;
+    for (int i0 = mid; i0 < nn; i0 += 8 * NMOV) {
+      float gv[8], ov[8], av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int i = i0 + u * NMOV;
+        int t = tb + i;
+        bool v = i < nn && t >= 0 && t < nvalid;
+        gv[u] = v ? ld_na(cot + t) : 0.f;
+        ov[u] = v ? ld_na(outr + t) : 0.f;
+        av[u] = (MODE == M_SOFT && v) ? ld_na(auxr + t) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int i = i0 + u * NMOV;
+        if (i >= nn) continue;
+        int q = dK ? i + div_k(i, K, invK) : i;
+        HG[q] = gv[u];
+        if (MODE == M_LSE) {
+          float M = sg * ov[u];
+          HM[q] = M;
+          if (gv[u] != 0.f) {
+            hi = fmaxf(hi, M);
+            lo = fminf(lo, M);
+          }
+        } else {
+          HM[q] = av[u];
+          HC[q] = sg * ov[u];
+          HB[q] = 0.f;
+        }
+      }
+    }
+    if (MODE == M_LSE) {
+      for (int o = 16; o > 0; o >>= 1) {
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      }
+      if ((mid & 31) == 0) {
+        rng_sh[b][0][mid >> 5] = hi;
+        rng_sh[b][1][mid >> 5] = lo;
+      }
+    }
+    // overrun outputs route their cotangent to c[L-1] ('last'); one mover warp sums them
+    if (mid < 32) {
+      float ps = 0.f;
+      if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + J) {
+        int t_lo = nvalid > 0 ? nvalid : 0;
+        for (int t = t_lo + mid; t < L; t += 32) ps += cot[t];
+        for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      }
+      if (mid == 0) padsum_sh[b] = ps;
+    }
+  };
+
+  auto finalize = [&](long long s, int b) {  // movers: child cotangent + fused VJP
+    long long row;
+    int j0;
+    tile_of(s, row, j0);
+    const float* HM = sm + b * HW * nsm;
+    const float* HG = HM + nsm;
+    const float* HC = HG + nsm;
+    const float* HB = HC + nsm;
+    const float padsum = padsum_sh[b];
+    Ev<MODE, EK> ev(p.child, row, p.mp);
+    const int jn = (j0 + J < L ? j0 + J : L) - j0;
+    int i0 = mid;
+    if (MODE == M_LSE && dK == 0 && j0 + jn < L) {  // interior (the pad sum lands on L - 1)
+      for (; i0 + 7 * NMOV < jn; i0 += 8 * NMOV) {
+        typename Ev<MODE, EK>::Raw r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = ev.load(j0 + i0 + u * NMOV);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * NMOV;
+          const float A = HG[i];
+          float g = 0.f;
+          if (A != 0.f) g = A * ex2f(tau2 * (sg * ev.value(j0 + i, r[u]) - HM[i]));
+          ev.grad(j0 + i, r[u], g);
+        }
+      }
+    }
+    for (; i0 < jn; i0 += 4 * NMOV) {
+      typename Ev<MODE, EK>::Raw r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * NMOV;
+        if (i < jn) r[u] = ev.load(j0 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int i = i0 + u * NMOV;
+        if (i >= jn) continue;
+        int j = j0 + i;
+        int q = dK ? i + div_k(i, K, invK) : i;
+        float A = HG[q];
+        float g = 0.f;
+        if (MODE == M_LSE) {
+          if (A != 0.f) {
+            float uj = sg * ev.value(j, r[u]);
+            g = A * ex2f(tau2 * (uj - HM[q]));
+          }
+        } else {
+          float Bc = HB[q];
+          if (A != 0.f || Bc != 0.f) {
+            float uj = sg * ev.value(j, r[u]);
+            g = ex2f(tau2 * (uj - HM[q])) * (A * fmaf(tau, uj - HC[q], 1.f) - tau * Bc);
+          }
+        }
+        if (j == L - 1) g += padsum;
+        ev.grad(j, r[u], g);
+      }
+    }
+  };
+
+  constexpr int SC = 8;
+  auto scan = [&](int b) {  // scanners: prefix, then suffix + combine in place
+    float* HM = sm + b * HW * nsm;
+    float* HG = HM + nsm;
+    float* HC = HG + nsm;
+    float* HB = HC + nsm;
+    if (MODE == M_LSE) {
+      // Fast path: one shift c = min M_t over the tile's live outputs, so the
+      // window sums are plain sums of h_t = g_t 2^{tau2 (c - M_t)}; the result is
+      // written back as (mu = c, A) so the finalize formula is unchanged.
+      float hi = -INFINITY, c = INFINITY;
+      for (int w = 0; w < NMOV / 32; ++w) {
+        hi = fmaxf(hi, rng_sh[b][0][w]);
+        c = fminf(c, rng_sh[b][1][w]);
+      }
+      if (hi < c || (hi - c) * tau2 <= 100.f) {
+        if (hi < c) c = 0.f;  // no live output in the tile
+        if ((int)threadIdx.x < NB) {
+          const int b0 = threadIdx.x * Kp;
+          float acc = 0.f;
+          for (int i = 0; i < K; i += SC) {
+            float xm[SC], xg[SC];
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              bool in = i + k < K;
+              xm[k] = in ? HM[b0 + i + k] : 0.f;
+              xg[k] = in ? HG[b0 + i + k] : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              if (i + k >= K) break;
+              float h = xg[k] != 0.f ? xg[k] * ex2f(tau2 * (c - xm[k])) : 0.f;
+              HM[b0 + i + k] = h;
+              acc += h;
+              PA[b0 + i + k] = acc;
+            }
+          }
+        }
+        named_bar(1, SWT);
+        if ((int)threadIdx.x < NB - 1) {
+          const int b0 = threadIdx.x * Kp, nb = b0 + Kp - 1;
+          float acc = 0.f;
+          for (int i = K - 1; i >= 0; i -= SC) {
+            float xh[SC], ya[SC];
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              const int j = i - k;
+              xh[k] = (j >= 0) ? HM[b0 + j] : 0.f;
+              ya[k] = (j > 0) ? PA[nb + j] : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < SC; ++k) {
+              const int j = i - k;
+              if (j < 0) break;
+              acc += xh[k];
+              HM[b0 + j] = c;
+              HG[b0 + j] = acc + ya[k];
+            }
+          }
+        }
+        return;
+      }
+    }
+    if ((int)threadIdx.x < NB) {
+      const int b0 = threadIdx.x * Kp;
+      float mu = HM[b0], A = HG[b0], Bc = 0.f, c = (MODE == M_SOFT) ? HC[b0] : 0.f;
+      PM[b0] = mu;
+      PA[b0] = A;
+      if (MODE == M_SOFT) {
+        PB[b0] = Bc;
+        PC[b0] = c;
+      }
+      for (int i = 1; i < K; i += SC) {
+        float xm[SC], xa[SC], xc[SC];
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          bool in = i + k < K;
+          xm[k] = in ? HM[b0 + i + k] : 0.f;
+          xa[k] = in ? HG[b0 + i + k] : 0.f;
+          xc[k] = (MODE == M_SOFT && in) ? HC[b0 + i + k] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          if (i + k >= K) break;
+          const int q = b0 + i + k;
+          if (MODE == M_LSE) {
+            gl_add(mu, A, xm[k], xa[k], tau2);
+          } else {
+            gs_add(mu, A, Bc, c, xm[k], xa[k], 0.f, xc[k], tau2);
+            PB[q] = Bc;
+            PC[q] = c;
+          }
+          PM[q] = mu;
+          PA[q] = A;
+        }
+      }
+    }
+    named_bar(1, SWT);
+    if ((int)threadIdx.x < NB - 1) {
+      const int b0 = threadIdx.x * Kp, nb = b0 + Kp - 1;  // nb + i = next block prefix at i - 1
+      float mu = HM[b0 + K - 1], A = HG[b0 + K - 1], Bc = 0.f;
+      float c = (MODE == M_SOFT) ? HC[b0 + K - 1] : 0.f;
+      for (int i = K - 1; i >= 0; i -= SC) {
+        float xm[SC], xa[SC], xc[SC], ym[SC], ya[SC], yb[SC], yc[SC];
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          const int j = i - k;
+          const bool in = j >= 0, nx = j > 0;
+          xm[k] = in ? HM[b0 + j] : 0.f;
+          xa[k] = in ? HG[b0 + j] : 0.f;
+          xc[k] = (MODE == M_SOFT && in) ? HC[b0 + j] : 0.f;
+          ym[k] = nx ? PM[nb + j] : 0.f;
+          ya[k] = nx ? PA[nb + j] : 0.f;
+          yb[k] = (MODE == M_SOFT && nx) ? PB[nb + j] : 0.f;
+          yc[k] = (MODE == M_SOFT && nx) ? PC[nb + j] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < SC; ++k) {
+          const int j = i - k;
+          if (j < 0) break;
+          const int q = b0 + j;
+          if (MODE == M_LSE) {
+            if (j < K - 1) gl_add(mu, A, xm[k], xa[k], tau2);
+            float m2 = mu, a2 = A;
+            if (j > 0) gl_add(m2, a2, ym[k], ya[k], tau2);
+            HM[q] = m2;
+            HG[q] = a2;
+          } else {
+            if (j < K - 1) gs_add(mu, A, Bc, c, xm[k], xa[k], 0.f, xc[k], tau2);
+            float m2 = mu, a2 = A, b2 = Bc, c2 = c;
+            if (j > 0) gs_add(m2, a2, b2, c2, ym[k], ya[k], yb[k], yc[k], tau2);
+            HM[q] = m2;
+            HG[q] = a2;
+            HC[q] = c2;
+            HB[q] = b2;
+          }
+        }
+      }
+    }
+  };
+
+  const bool do_scan = p.dbg_skip != 1, do_move = p.dbg_skip != 2;
+  if (!scanner && n > 0 && do_move) load(0, 0);
+  __syncthreads();
+  for (long long s = 0; s < n; ++s) {
+    const int b = (int)(s & 1);
+    if (scanner) {
+      if (do_scan) scan(b);
+    } else {
+      if (s >= 1 && do_move) finalize(s - 1, b ^ 1);
+      named_bar(2, NMOV);
+      if (s + 1 < n && do_move) load(s + 1, b ^ 1);
+    }
+    __syncthreads();
+  }
+  if (!scanner && n > 0 && do_move) finalize(n - 1, (int)((n - 1) & 1));
+}
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static int pipe_nb(int K, int words) {
+  long long per_block = (long long)words * (K | 1) * 4;
+  long long nb = (long long)(env_int("STLG_PIPE_BUDGET_KB", 72) * 1024 / per_block);
+  if (nb >= 32) nb = (nb / 32) * 32;
+  if (nb > 128) nb = 128;  // keep >= 4 mover warps
+  int forced = env_int("STLG_PIPE_NB", 0);
+  if (forced > 0) nb = forced;
+  return (int)nb;
+}
+
+// Launch configuration is cached per (kernel, shared-memory size): the
+// attribute / occupancy queries cost microseconds of host time per call.
+struct LaunchCfg {
+  const void* fn;
+  size_t smem;
+  int per_sm, sms;
+};
+static thread_local LaunchCfg g_cfg_cache[64];
+static thread_local int g_cfg_n = 0;
+
+template <typename KernT>
+static cudaError_t launch_persistent(KernT k, FGParams& p, size_t smem, cudaStream_t st) {
+  cudaError_t e;
+  int per_sm = 0, sms = 0;
+  for (int i = 0; i < g_cfg_n; ++i)
+    if (g_cfg_cache[i].fn == (const void*)k && g_cfg_cache[i].smem == smem) {
+      per_sm = g_cfg_cache[i].per_sm;
+      sms = g_cfg_cache[i].sms;
+    }
+  if (per_sm == 0) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, PIPE_THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_cfg_n < 64) g_cfg_cache[g_cfg_n++] = LaunchCfg{(const void*)k, smem, per_sm, sms};
+  }
+  p.dbg_skip = env_int("STLG_PIPE_SKIP", 0);
+  const int J = (p.NB - 1) * p.K;
+  const int tpr = (int)((p.L + J - 1) / J);
+  const long long total = (long long)tpr * p.B;
+  long long grid = (long long)sms * per_sm;
+  if (grid > total) grid = total;
+  k<<<(unsigned)grid, PIPE_THREADS, smem, st>>>(p, tpr, total);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// returns cudaErrorNotSupported when the window is too large for the pipelined layout
+cudaError_t launch_fgt_fwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st) {
+  const int words = (mode == M_SOFT) ? 6 : 3;
+  const int nb = pipe_nb(p.K, words);
+  if (nb < 8) return cudaErrorNotSupported;
+  p.Kp = p.K | 1;
+  p.NB = nb;
+  const size_t smem = (size_t)words * nb * p.Kp * 4;
+#define FWD_PIPE(M)                                                              \
+  switch (ek) {                                                                  \
+    case EK_AFF: return launch_persistent(k_fgt_fwd_pipe<M, EK_AFF>, p, smem, st);   \
+    case EK_NORM: return launch_persistent(k_fgt_fwd_pipe<M, EK_NORM>, p, smem, st); \
+    case EK_SRC: return launch_persistent(k_fgt_fwd_pipe<M, EK_SRC>, p, smem, st);   \
+    case EK_PAIR: return launch_persistent(k_fgt_fwd_pipe<M, EK_PAIR>, p, smem, st); \
+    default: return launch_persistent(k_fgt_fwd_pipe<M, EK_GEN>, p, smem, st);       \
+  }
+  if (mode == M_HARD) FWD_PIPE(M_HARD)
+  if (mode == M_LSE) FWD_PIPE(M_LSE)
+  FWD_PIPE(M_SOFT)
+#undef FWD_PIPE
+}
+
+cudaError_t launch_fgt_bwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st) {
+  if (mode == M_HARD) return cudaErrorNotSupported;
+  const int words = (mode == M_SOFT) ? 12 : 6;
+  const int nb = pipe_nb(p.K, words);
+  if (nb < 8) return cudaErrorNotSupported;
+  p.Kp = p.K | 1;
+  p.NB = nb;
+  const size_t smem = (size_t)words * nb * p.Kp * 4;
+#define BWD_PIPE(M)                                                              \
+  switch (ek) {                                                                  \
+    case EK_AFF: return launch_persistent(k_fgt_bwd_pipe<M, EK_AFF>, p, smem, st);   \
+    case EK_NORM: return launch_persistent(k_fgt_bwd_pipe<M, EK_NORM>, p, smem, st); \
+    case EK_SRC: return launch_persistent(k_fgt_bwd_pipe<M, EK_SRC>, p, smem, st);   \
+    case EK_PAIR: return launch_persistent(k_fgt_bwd_pipe<M, EK_PAIR>, p, smem, st); \
+    default: return launch_persistent(k_fgt_bwd_pipe<M, EK_GEN>, p, smem, st);       \
+  }
+  if (mode == M_LSE) BWD_PIPE(M_LSE)
+  BWD_PIPE(M_SOFT)
+#undef BWD_PIPE
+}
+
+}  // namespace stlg

@@ -164,7 +164,7 @@ STLG_API int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, 
                   const stlg_grad* d_channels, double* d_smooth, void* fwd_ws,
                   size_t fwd_ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, void* stream);
 
-/* Count of device kernel launches issued by this thread since the last reset. */
+/* Count of device kernel launches issued by the library (all threads) since the last reset. */
 STLG_API int64_t stlg_launch_count(int reset);
 
 #ifdef __cplusplus

@@ -1,0 +1,436 @@
+// fg_cav.cuh — timed Eventually / Always (hard and LSE modes) for K = b - a + 1 >= 17:
+// chunk-aligned van Herk / Gil-Werman.
+//
+// Semantics as fg_reg.cuh (masking.py:160-205, tape.py:340-380).  A tile stages
+// N = 16 T samples; thread q owns the chunk [16q, 16q + 16) in registers.  The
+// reduction blocks ARE the chunks, so no block boundary ever falls inside a thread's
+// registers: with K - 1 = 16 d + c (0 <= c < 16), the window starting at i = 16q + k
+// ends in chunk q' = q + d + [k + c >= 16] at offset o = (k + c) mod 16, and
+//     window(i) = suffix_q(k) (+) fold(chunks q+1 .. q'-1) (+) prefix_q'(o).
+// Each thread scans its chunk both ways in registers (prefixes also go to shared
+// memory for the remote reads), publishes its chunk total, and folds the d - 1 / d
+// middle totals once.  A window finish is two monoid combines and one shared
+// load; the result is written into the prefix slot it consumed (each slot is read
+// by exactly one window), then stored coalesced.  Exact monoids (fg_reg.cuh).
+#pragma once
+#include "fg_reg.cuh"
+
+namespace stlg {
+
+// prefix scan of the chunk -> P0 / P1 (own padded slots), total -> TOT; the suffix
+// scan overwrites x in registers.
+template <int RK>
+__device__ __forceinline__ void cav_scans(RSt (&x)[RG_EPT], float tau2, float* P0, float* P1,
+                                          float* T0, float* T1) {
+  const int base = threadIdx.x * (RG_EPT + 1);
+  RSt run = x[0];
+  P0[base] = run.m;
+  if (RK != RK_HARD) P1[base] = run.s;
+#pragma unroll
+  for (int k = 1; k < RG_EPT; ++k) {
+    run = rcomb<RK>(run, x[k], tau2);
+    P0[base + k] = run.m;
+    if (RK != RK_HARD) P1[base + k] = run.s;
+  }
+  T0[threadIdx.x] = run.m;
+  if (RK != RK_HARD) T1[threadIdx.x] = run.s;
+#pragma unroll
+  for (int k = RG_EPT - 2; k >= 0; --k) x[k] = rcomb<RK>(x[k], x[k + 1], tau2);
+}
+
+// middle folds: A0 = chunks q+1 .. q+d-1, A1 = A0 (+) chunk q+d (identity when empty /
+// past the tile; such windows are never finished)
+template <int RK, int NW>
+__device__ __forceinline__ void cav_middle(int d, float tau2, const float* T0, const float* T1, RSt& A0,
+                                           RSt& A1) {
+  const int q = threadIdx.x;
+  RSt a = rident<RK>();
+  const int last = q + d < NW * 32 ? q + d : NW * 32;  // exclusive bound of readable chunks
+  for (int j = q + 1; j < q + d && j < last; ++j) a = rcomb<RK>(a, RSt{T0[j], RK == RK_HARD ? 0.f : T1[j]}, tau2);
+  A0 = a;
+  if (q + d < NW * 32) a = rcomb<RK>(a, RSt{T0[q + d], RK == RK_HARD ? 0.f : T1[q + d]}, tau2);
+  A1 = a;
+}
+
+// window finish for i = 16 q + k in [lo, hi) (FULL: the whole chunk), descending k:
+// fin(k, i, w, slot)
+template <int RK, bool FULL, typename Fin>
+__device__ __forceinline__ void cav_windows(const RSt (&S)[RG_EPT], RSt A0, RSt A1, int d, int c,
+                                            float tau2, int lo, int hi, const float* P0,
+                                            const float* P1, Fin&& fin) {
+  const int q = threadIdx.x;
+  const int i0 = q * RG_EPT;
+  const int sb = (q + d) * (RG_EPT + 1) + c;  // slot of o = k + c in chunk q + d
+#pragma unroll
+  for (int k = RG_EPT - 1; k >= 0; --k) {
+    const int i = i0 + k;
+    if (FULL || (i >= lo && i < hi)) {
+      const bool up = k + c >= RG_EPT;       // the window ends in chunk q + d + 1
+      const int sl = sb + k + (up ? 1 : 0);  // 17 (q + d + up) + (k + c - 16 up)
+      RSt w = rcomb<RK>(S[k], up ? A1 : A0, tau2);
+      const RSt pv{P0[sl], RK == RK_HARD ? 0.f : P1[sl]};
+      w = rcomb<RK>(w, pv, tau2);
+      fin(k, i, w, sl);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward (hard: RK_HARD, LSE: RK_LSE)
+// ---------------------------------------------------------------------------
+template <int RK, int MODE, int EK, int NW>
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS;
+  extern __shared__ float rsm[];
+  __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T];
+  float* P0 = rsm;
+  float* P1 = rsm + C::NP;
+  const int K = p.K;
+  const int d = (K - 1) >> 4, c = (K - 1) & 15;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = N - K + 1;
+  const int t0 = blockIdx.x * J;
+  const int nvalid = L - p.b;
+  const int s0 = t0 + p.a;
+  const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
+  const float czero = p.canon ? 0.f : -0.f;  // x + (-0) == x for every x: canon is one add
+  Ev<MODE, EK> ev(p.child, row, p.mp);
+  const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+  float* outr = p.out + row * L;
+  const int tend = (t0 + J < L ? t0 + J : L) - t0;
+  const int tid = threadIdx.x;
+  if (t0 >= nvalid) {  // every output of the tile overruns
+    for (int i = tid; i < tend; i += T) outr[t0 + i] = __fadd_rn(padv, czero);
+    if (RK == RK_LSE && p.aux != nullptr)
+      for (int i = tid; i < tend; i += T) p.aux[row * L + t0 + i] = 0.f;
+    return;
+  }
+  {
+    float* dst = P0 + tid + (tid >> 4);
+    const int jb = s0 + tid;
+    if (s0 + N <= L) {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<MODE, EK>::Raw r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = ev.load(jb + (h + k) * T);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dst[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<MODE, EK>::Raw r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (jb + (h + k) * T < L) r[k] = ev.load(jb + (h + k) * T);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = jb + (h + k) * T;
+          dst[(h + k) * SS] = j < L ? sg * ev.value(j, r[k]) : 0.f;  // feeds overrun windows only
+        }
+      }
+    }
+  }
+  __syncthreads();
+  RSt x[RG_EPT];
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
+  cav_scans<RK>(x, tau2, P0, P1, T0, T1);  // own slots only: no barrier needed before
+  __syncthreads();
+  RSt A0, A1;
+  cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1);
+  const int i0 = tid * RG_EPT;
+  if (i0 + RG_EPT <= J && t0 + i0 + RG_EPT <= nvalid) {
+    cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, [&](int, int, RSt w, int sl) {
+      const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
+      const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
+      P0[sl] = __fadd_rn(sg * v, czero);
+      if (RK == RK_LSE) P1[sl] = sg * fmaf(l2, itau2, w.m - v);  // residual of v
+    });
+  } else {
+    cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, [&](int, int i, RSt w, int sl) {
+      const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
+      const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
+      const bool live = t0 + i < nvalid;
+      P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
+      if (RK == RK_LSE) P1[sl] = live ? sg * fmaf(l2, itau2, w.m - v) : 0.f;
+    });
+  }
+  __syncthreads();
+  {
+    const float* src = P0 + rpad(tid + K - 1);
+    float* op = outr + t0 + tid;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k)
+      if (tid + k * T < tend) op[k * T] = src[k * SS];
+    if (RK == RK_LSE && p.aux != nullptr) {  // low word of the double-float trace
+      const float* src1 = P1 + rpad(tid + K - 1);
+      float* ap = p.aux + row * L + t0 + tid;
+#pragma unroll
+      for (int k = 0; k < RG_EPT; ++k)
+        if (tid + k * T < tend) ap[k * T] = src1[k * SS];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, LSE (gather form over outputs t; RK_GLSE)
+// ---------------------------------------------------------------------------
+template <int EK, int NW>
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS;
+  extern __shared__ float rsm[];
+  __shared__ float T0[T], T1[T];
+  __shared__ float padsum_sh;
+  float* P0 = rsm;
+  float* P1 = rsm + C::NP;
+  const int K = p.K;
+  const int d = (K - 1) >> 4, c = (K - 1) & 15;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = N - K + 1;  // owned child elements per tile
+  const int j0 = blockIdx.x * J;
+  const int tb = j0 - p.b;  // local index 0 <-> output t = tb
+  const int nvalid = L - p.b;
+  const float tau2 = p.mp.tau2, sg = p.sg;
+  const float* cot = p.cot + row * L;
+  const float* outr = p.out_in + row * L;
+  const float* lor = p.aux_in ? p.aux_in + row * L : nullptr;  // low word of M (double-float)
+  const int tid = threadIdx.x;
+  {
+    float* d0 = P0 + tid + (tid >> 4);
+    float* d1 = P1 + tid + (tid >> 4);
+    const int tt = tb + tid;
+    if (tb >= 0 && tb + N <= nvalid) {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        float gv[8], mv[8], lv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          gv[k] = ld_na(cot + tt + (h + k) * T);
+          mv[k] = ld_na(outr + tt + (h + k) * T);
+          lv[k] = lor ? ld_na(lor + tt + (h + k) * T) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          d0[(h + k) * SS] = -sg * mv[k];
+          d1[(h + k) * SS] = lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        float gv[8], mv[8], lv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int t = tt + (h + k) * T;
+          const bool v = t >= 0 && t < nvalid;
+          gv[k] = v ? ld_na(cot + t) : 0.f;
+          mv[k] = v ? ld_na(outr + t) : 0.f;
+          lv[k] = (v && lor) ? ld_na(lor + t) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int t = tt + (h + k) * T;
+          const bool v = t >= 0 && t < nvalid;
+          d0[(h + k) * SS] = v ? -sg * mv[k] : -FLT_MAX;
+          d1[(h + k) * SS] = lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k];
+        }
+      }
+    }
+  }
+  if (tid < 32) {  // overrun outputs route to c[L-1] ('last' padding)
+    float ps = 0.f;
+    if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + J) {
+      const int t_lo = nvalid > 0 ? nvalid : 0;
+      for (int t = t_lo + tid; t < L; t += 32) ps += cot[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    }
+    if (tid == 0) padsum_sh = ps;
+  }
+  __syncthreads();
+  RSt x[RG_EPT];
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) {
+    const int qq = tid * (RG_EPT + 1) + k;
+    x[k] = RSt{P0[qq], P1[qq]};
+  }
+  cav_scans<RK_GLSE>(x, tau2, P0, P1, T0, T1);
+  __syncthreads();
+  RSt A0, A1;
+  cav_middle<RK_GLSE, NW>(d, tau2, T0, T1, A0, A1);
+  auto fin = [&](int, int, RSt w, int sl) {
+    P0[sl] = w.m;
+    P1[sl] = w.s;
+  };
+  if (tid * RG_EPT + RG_EPT <= J) cav_windows<RK_GLSE, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+  else cav_windows<RK_GLSE, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+  __syncthreads();
+  Ev<M_LSE, EK> ev(p.child, row, p.mp);
+  const int jn = (j0 + J < L ? j0 + J : L) - j0;
+  const float padsum = padsum_sh;
+  const int slb = rpad(tid + K - 1);
+  const int jb = j0 + tid;
+#pragma unroll
+  for (int h = 0; h < RG_EPT; h += 8) {
+    typename Ev<M_LSE, EK>::Raw r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (tid + (h + u) * T < jn) {
+        const int j = jb + (h + u) * T;
+        const int sl = slb + (h + u) * SS;
+        // S == 0 comes with m = -FLT_MAX or u_j + m <= 0: the product is an exact 0
+        float g = P1[sl] * ex2f(tau2 * fmaf(sg, ev.value(j, r[u]), P0[sl]));
+        if (j == L - 1) g += padsum;
+        ev.grad(j, r[u], g);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, hard (RK_HARDI; first-argmax runs as in fg_reg.cuh)
+// ---------------------------------------------------------------------------
+template <int EK, int NW>
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS;
+  extern __shared__ float rsm[];
+  __shared__ float T0[T], T1[T];
+  __shared__ float padsum_sh;
+  float* P0 = rsm;
+  float* P1 = rsm + C::NP;
+  float* G = rsm + 2 * C::NP;
+  const int K = p.K;
+  const int d = (K - 1) >> 4, c = (K - 1) & 15;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int Jo = N - 2 * K + 2;    // owned child elements per tile
+  const int j0 = blockIdx.x * Jo;
+  const int first = j0 - (K - 1);  // local index 0 <-> child element `first`
+  const int nvalid = L - p.b;
+  const int nwin = N - K + 1;      // windows staged per tile
+  const float sg = p.sg;
+  const float* cot = p.cot + row * L;
+  const int tid = threadIdx.x;
+  Ev<M_HARD, EK> ev(p.child, row, p.mp);
+  {
+    float* d0 = P0 + tid + (tid >> 4);
+    float* d1 = P1 + tid + (tid >> 4);
+    const int jb = first + tid;
+    const int tb = jb - p.a;
+    if (first >= 0 && first + N <= L && first - p.a >= 0 && first - p.a + nwin <= nvalid) {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<M_HARD, EK>::Raw r[8];
+        float gv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          r[k] = ev.load(jb + (h + k) * T);
+          gv[k] = (tid + (h + k) * T < nwin) ? ld_na(cot + tb + (h + k) * T) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          d0[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
+          d1[(h + k) * SS] = gv[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<M_HARD, EK>::Raw r[8];
+        float gv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = jb + (h + k) * T, t = tb + (h + k) * T;
+          if (j >= 0 && j < L) r[k] = ev.load(j);
+          gv[k] = (tid + (h + k) * T < nwin && t >= 0 && t < nvalid) ? ld_na(cot + t) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = jb + (h + k) * T;
+          d0[(h + k) * SS] = (j >= 0 && j < L) ? sg * ev.value(j, r[k]) : 0.f;
+          d1[(h + k) * SS] = gv[k];
+        }
+      }
+    }
+  }
+  if (tid < 32) {
+    float ps = 0.f;
+    if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + Jo) {
+      const int t_lo = nvalid > 0 ? nvalid : 0;
+      for (int t = t_lo + tid; t < L; t += 32) ps += cot[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    }
+    if (tid == 0) padsum_sh = ps;
+  }
+  __syncthreads();
+  RSt x[RG_EPT];
+  float g[RG_EPT];
+  {
+    const int q0 = tid * (RG_EPT + 1);
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) {
+      x[k] = RSt{P0[q0 + k], __int_as_float(tid * RG_EPT + k)};
+      g[k] = P1[q0 + k];
+      G[q0 + k] = 0.f;
+    }
+  }
+  cav_scans<RK_HARDI>(x, 0.f, P0, P1, T0, T1);
+  __syncthreads();
+  RSt A0, A1;
+  cav_middle<RK_HARDI, NW>(d, 0.f, T0, T1, A0, A1);
+  {
+    int cur = -1;
+    float acc = 0.f;
+    bool top = true;  // the current run touches the chunk's upper end
+    auto fin = [&](int k, int, RSt w, int) {
+      const int am = __float_as_int(w.s);
+      if (am != cur) {
+        if (cur >= 0) {
+          if (top) atomicAdd(&G[rpad(cur)], acc);
+          else G[rpad(cur)] = acc;
+        }
+        top = cur < 0;
+        cur = am;
+        acc = 0.f;
+      }
+      acc += g[k];
+    };
+    if (tid * RG_EPT + RG_EPT <= nwin) cav_windows<RK_HARDI, true>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
+    else cav_windows<RK_HARDI, false>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
+    if (cur >= 0) atomicAdd(&G[rpad(cur)], acc);
+  }
+  __syncthreads();
+  const int jn = (j0 + Jo < L ? j0 + Jo : L) - j0;
+  const float padsum = padsum_sh;
+  const int gb = rpad(tid + K - 1);
+  const int jb = j0 + tid;
+#pragma unroll
+  for (int h = 0; h < RG_EPT; h += 8) {
+    typename Ev<M_HARD, EK>::Raw r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (tid + (h + u) * T < jn) {
+        const int j = jb + (h + u) * T;
+        float gg = G[gb + (h + u) * SS];
+        if (j == L - 1) gg += padsum;
+        ev.grad(j, r[u], gg);
+      }
+    }
+  }
+}
+
+}  // namespace stlg

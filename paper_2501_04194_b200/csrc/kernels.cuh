@@ -97,4 +97,10 @@ cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs
 // launch accounting (exec.cu)
 void count_launch(int n = 1);
 
+// register-blocked exact timed F / G (hard, LSE): fg_reg.cu
+bool reg_enabled();
+bool reg_applicable(int mode, const FGParams& p, bool bwd);
+cudaError_t launch_reg_fwd(int mode, int ek, FGParams& p, cudaStream_t st);
+cudaError_t launch_reg_bwd(int mode, int ek, FGParams& p, cudaStream_t st);
+
 }  // namespace stlg

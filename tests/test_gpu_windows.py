@@ -1,0 +1,135 @@
+"""Timed F / G window kernels vs the oracle across window widths, lengths and layouts.
+
+The device picks the chunk-aligned kernels for K = b - a + 1 >= 17 and the segmented
+ones for 2 <= K <= 16 (csrc/fg_cav.cuh, csrc/fg_reg.cuh); tiles hold 2048..4096
+samples.  The sweep crosses the K = 16 / 17 switch, chunk multiples (K - 1 = 16 d + c
+with c = 0 and c = 15), tile edges (several tiles per row, partial last tile) and row
+edges (overrun windows, `last` and constant padding).  Hard traces are bit-exact,
+hard gradients exact for the ones cotangent; LSE within 1e-5 relative
+(SURVEY §8(c)).  Tie-heavy integer data exercises the first-argmax rule
+(tape.py:346-348).
+"""
+
+import numpy as np
+import pytest
+
+from devhelp import assert_hard_equal, rel_err, run_device
+
+pytestmark = pytest.mark.gpu
+
+INTERVALS = [(0, 1), (3, 5), (0, 15), (2, 18), (0, 17), (5, 36), (0, 32), (10, 100), (0, 255), (7, 1030)]
+LENGTHS = [50, 1000, 9001]
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_04194_b200 as P
+    P._lib.load()
+    return P
+
+
+def _oracle():
+    import os
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(here, "..", "oracle"))
+    import stl_oracle
+    return stl_oracle
+
+
+def _data(rng, B, L, ties):
+    # stationary AR(1), sd ~ 2: fp32 traces carry |u| eps_32 absolute error and the
+    # LSE weights 2^{tau2 (u - M)} turn it into tau |u| eps_32 relative error, so the
+    # 1e-5 bound is stated for well-scaled signals (|u| of a few units at tau = 10)
+    e = rng.normal(0, 0.3, (B, L))
+    x = np.empty((B, L))
+    x[:, 0] = rng.normal(0, 2, B)
+    for t in range(1, L):
+        x[:, t] = 0.99 * x[:, t - 1] + e[:, t]
+    if ties:
+        x = np.round(x)
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("ab", INTERVALS, ids=[f"a{a}b{b}" for a, b in INTERVALS])
+@pytest.mark.parametrize("L", LENGTHS)
+@pytest.mark.parametrize("op", ["F", "G"])
+def test_hard_windows_vs_oracle(cuda, ab, L, op):
+    P = cuda
+    orc = _oracle()
+    a, b = ab
+    rng = np.random.default_rng(1000 * a + b + L)
+    ties = (a + b + L) % 2 == 0
+    x = _data(rng, 3, L, ties)
+    iv = P.StepInterval(a, b)
+    f = P.Eventually(P.Pred("x", ">", 0.5), iv) if op == "F" else P.Always(P.Pred("x", "<", -0.25), iv)
+    pad = P.PaddingPolicy.last_value() if L % 2 else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(mode=P.Hard(), padding=pad)
+    tr, g, _ = run_device(f, {"x": x}, cfg)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x}, cfg)
+    assert_hard_equal(tr, np.asarray(ref_tr, dtype=np.float32))
+    np.testing.assert_array_equal(g["x"], ref_g["x"])
+    cot = rng.normal(0, 1, tr.shape)
+    _, g2, _ = run_device(f, {"x": x}, cfg, cot=cot)
+    _, ref_g2, _ = orc.trace_and_grad(f, {"x": x}, cfg, cot)
+    assert rel_err(g2["x"], ref_g2["x"]) <= 1e-5
+
+
+@pytest.mark.parametrize("ab", INTERVALS, ids=[f"a{a}b{b}" for a, b in INTERVALS])
+@pytest.mark.parametrize("L", LENGTHS)
+@pytest.mark.parametrize("temp", [1.0, 10.0])
+def test_lse_windows_vs_oracle(cuda, ab, L, temp):
+    P = cuda
+    orc = _oracle()
+    a, b = ab
+    rng = np.random.default_rng(7 + 1000 * a + b + L)
+    x = _data(rng, 3, L, False)
+    iv = P.StepInterval(a, b)
+    f = P.Always(P.Pred("x", ">", 0.1), iv) if (a + L) % 2 else P.Eventually(P.Pred("x", "<", 0.3), iv)
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(temp))
+    cot = rng.normal(0, 1, (3, L))
+    tr, g, _ = run_device(f, {"x": x}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x}, cfg, cot)
+    assert rel_err(tr, ref_tr) <= 1e-5
+    assert rel_err(g["x"], ref_g["x"]) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["hard", "lse"])
+@pytest.mark.parametrize("ab", [(0, 9), (10, 100)])
+@pytest.mark.parametrize("layout", ["pair", "split", "expr"])
+def test_child_layouts(cuda, mode, ab, layout):
+    """Interleaved (x, y) pairs (EK_PAIR), two channels (EK_NORM), fused expression (EK_GEN)."""
+    import torch
+    P = cuda
+    orc = _oracle()
+    rng = np.random.default_rng(hash((mode, ab, layout)) % 2**32)
+    B, L = 2, 7000
+    xy = np.asarray(np.cumsum(rng.normal(0, 0.05, (B, L, 2)), axis=1), dtype=np.float32)
+    iv = P.StepInterval(*ab)
+    cfg = P.SemanticsConfig(mode=P.Hard() if mode == "hard" else P.LogSumExp(5.0))
+    if layout == "expr":
+        f = P.Eventually(P.And(P.Pred("px", ">", -0.25), P.Pred("py", "<", 0.375)), iv)
+    else:
+        f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), iv)
+    arrays = {"px": xy[..., 0].astype(np.float64), "py": xy[..., 1].astype(np.float64)}
+    cot = rng.normal(0, 1, (B, L))
+    dev = torch.device("cuda", 0)
+    if layout == "pair":
+        t = torch.tensor(xy, device=dev).requires_grad_(True)
+        out = P.trace(f, {"px": t[..., 0], "py": t[..., 1]}, cfg)
+        (gt,) = torch.autograd.grad(out, [t], torch.tensor(cot, dtype=torch.float32, device=dev))
+        tr = out.detach().double().cpu().numpy()
+        g = {"px": gt[..., 0].double().cpu().numpy(), "py": gt[..., 1].double().cpu().numpy()}
+    else:
+        tr, g, _ = run_device(f, arrays, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, arrays, cfg, cot)
+    tol = 1e-5
+    if mode == "hard" and layout == "expr":
+        assert_hard_equal(tr, np.asarray(ref_tr, dtype=np.float32))
+    else:  # fp32 sqrt in NormPred / smooth mode
+        assert rel_err(tr, ref_tr) <= tol
+    for k in ("px", "py"):
+        assert rel_err(g[k], ref_g[k]) <= tol

@@ -75,6 +75,81 @@ __device__ __forceinline__ void cav_windows(const RSt (&S)[RG_EPT], RSt A0, RSt 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// LSE frame sums.  When every chunk of a tile spans tau2 (max - min) <= FS_RANGE
+// (log2 units), chunk q works in the frame f_q = its max: terms E = payload *
+// 2^{tau2 (e - f_q)} lie in [2^-120, 1] (normal fp32), so the chunk's prefix /
+// suffix sums are plain adds, the chunk total is the exact-form state (f_q, sum)
+// for the middle fold, and a window is  S alpha + beta + P gamma  in the frame
+// M = max(f_q, m_A, f_q') with per-thread factors for the two remote chunks.
+// Any term lost to underflow is < 2^-126 against a sum >= 2^-120 of the dominant
+// part, so the result equals the exact monoid to fp32 rounding.  A tile with a
+// wider chunk takes the exact path (same kernel, uniform branch).
+// ---------------------------------------------------------------------------
+constexpr float FS_RANGE = 120.f;
+
+struct FsCase {
+  float M, al, be, ga;
+};
+
+// chunk frame (max over live terms; -FLT_MAX if none) and the width flag
+__device__ __forceinline__ bool fs_frame(const RSt (&x)[RG_EPT], bool gl, float tau2, float& f) {
+  float mx = -FLT_MAX, mn = FLT_MAX;
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) {
+    const bool live = !gl || x[k].s != 0.f;
+    mx = live ? fmaxf(mx, x[k].m) : mx;
+    mn = live ? fminf(mn, x[k].m) : mn;
+  }
+  f = mx;
+  return mx > mn && tau2 * (mx - mn) > FS_RANGE;
+}
+
+// E_k -> prefix sums in P0 (own slots), chunk state (f, total) -> T0 / T1;
+// E is overwritten by the suffix sums
+__device__ __forceinline__ void fs_scans(float (&E)[RG_EPT], float f, float* P0, float* T0, float* T1) {
+  const int base = threadIdx.x * (RG_EPT + 1);
+  float run = 0.f;
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) {
+    run += E[k];
+    P0[base + k] = run;
+  }
+  T0[threadIdx.x] = f;
+  T1[threadIdx.x] = run;
+#pragma unroll
+  for (int k = RG_EPT - 2; k >= 0; --k) E[k] += E[k + 1];
+}
+
+__device__ __forceinline__ FsCase fs_case(float f, RSt A, float fp, float tau2) {
+  FsCase r;
+  r.M = fmaxf(fmaxf(f, A.m), fp);
+  r.al = ex2f(tau2 * (f - r.M));
+  r.be = A.s * ex2f(tau2 * (A.m - r.M));
+  r.ga = ex2f(tau2 * (fp - r.M));
+  return r;
+}
+
+// window finish in frame sums: fin(k, i, M, s, slot), descending k
+template <bool FULL, typename Fin>
+__device__ __forceinline__ void fs_windows(const float (&S)[RG_EPT], const FsCase& c0, const FsCase& c1,
+                                           int d, int c, int lo, int hi, const float* P0, Fin&& fin) {
+  const int q = threadIdx.x;
+  const int i0 = q * RG_EPT;
+  const int sb = (q + d) * (RG_EPT + 1) + c;
+#pragma unroll
+  for (int k = RG_EPT - 1; k >= 0; --k) {
+    const int i = i0 + k;
+    if (FULL || (i >= lo && i < hi)) {
+      const bool up = k + c >= RG_EPT;
+      const int sl = sb + k + (up ? 1 : 0);
+      const float s = fmaf(S[k], up ? c1.al : c0.al, fmaf(P0[sl], up ? c1.ga : c0.ga, up ? c1.be : c0.be));
+      fin(k, i, up ? c1.M : c0.M, s, sl);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward (hard: RK_HARD, LSE: RK_LSE)
 // ---------------------------------------------------------------------------
@@ -99,38 +174,33 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   float* outr = p.out + row * L;
+  float* auxr = (RK == RK_LSE && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
   if (t0 >= nvalid) {  // every output of the tile overruns
-    for (int i = tid; i < tend; i += T) outr[t0 + i] = __fadd_rn(padv, czero);
-    if (RK == RK_LSE && p.aux != nullptr)
-      for (int i = tid; i < tend; i += T) p.aux[row * L + t0 + i] = 0.f;
+    for (int i = tid; i < tend; i += T) {
+      outr[t0 + i] = __fadd_rn(padv, czero);
+      if (auxr) auxr[t0 + i] = 0.f;
+    }
     return;
   }
   {
     float* dst = P0 + tid + (tid >> 4);
     const int jb = s0 + tid;
-    if (s0 + N <= L) {
+    const bool interior = s0 + N <= L;
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        typename Ev<MODE, EK>::Raw r[8];
+    for (int h = 0; h < RG_EPT; h += 8) {
+      typename Ev<MODE, EK>::Raw r[8];
+      // past the row end: replicate the last sample (feeds overrun windows only)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) r[k] = ev.load(jb + (h + k) * T);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dst[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
+      for (int k = 0; k < 8; ++k) {
+        const int j = jb + (h + k) * T;
+        r[k] = ev.load(interior ? j : (j < L ? j : L - 1));
       }
-    } else {
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        typename Ev<MODE, EK>::Raw r[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (jb + (h + k) * T < L) r[k] = ev.load(jb + (h + k) * T);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = jb + (h + k) * T;
-          dst[(h + k) * SS] = j < L ? sg * ev.value(j, r[k]) : 0.f;  // feeds overrun windows only
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int j = jb + (h + k) * T;
+        dst[(h + k) * SS] = sg * ev.value(interior ? j : (j < L ? j : L - 1), r[k]);
       }
     }
   }
@@ -138,27 +208,50 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   RSt x[RG_EPT];
 #pragma unroll
   for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
+  const int i0 = tid * RG_EPT;
+  const bool full = i0 + RG_EPT <= J && t0 + i0 + RG_EPT <= nvalid;
+  if constexpr (RK == RK_LSE) {
+    float f;
+    const bool wide = fs_frame(x, false, tau2, f);
+    if (!__syncthreads_or(wide)) {
+      float E[RG_EPT];
+#pragma unroll
+      for (int k = 0; k < RG_EPT; ++k) E[k] = ex2f(tau2 * (x[k].m - f));
+      fs_scans(E, f, P0, T0, T1);
+      __syncthreads();
+      RSt A0, A1;
+      cav_middle<RK_LSE, NW>(d, tau2, T0, T1, A0, A1);
+      const float fp0 = tid + d < T ? T0[tid + d] : -FLT_MAX;
+      const float fp1 = tid + d + 1 < T ? T0[tid + d + 1] : -FLT_MAX;
+      const FsCase c0 = fs_case(f, A0, fp0, tau2), c1 = fs_case(f, A1, fp1, tau2);
+      auto fin = [&](int, int i, float M, float s, int sl) {
+        const float l2 = lg2f(s);
+        const float v = fmaf(l2, itau2, M);
+        const bool live = full || t0 + i < nvalid;
+        P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
+        P1[sl] = live ? sg * fmaf(l2, itau2, M - v) : 0.f;  // residual of v
+      };
+      if (full) fs_windows<true>(E, c0, c1, d, c, 0, J, P0, fin);
+      else fs_windows<false>(E, c0, c1, d, c, 0, J, P0, fin);
+      goto store;
+    }
+  }
   cav_scans<RK>(x, tau2, P0, P1, T0, T1);  // own slots only: no barrier needed before
   __syncthreads();
-  RSt A0, A1;
-  cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1);
-  const int i0 = tid * RG_EPT;
-  if (i0 + RG_EPT <= J && t0 + i0 + RG_EPT <= nvalid) {
-    cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, [&](int, int, RSt w, int sl) {
+  {
+    RSt A0, A1;
+    cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1);
+    auto fin = [&](int, int i, RSt w, int sl) {
       const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
       const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
-      P0[sl] = __fadd_rn(sg * v, czero);
-      if (RK == RK_LSE) P1[sl] = sg * fmaf(l2, itau2, w.m - v);  // residual of v
-    });
-  } else {
-    cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, [&](int, int i, RSt w, int sl) {
-      const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
-      const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
-      const bool live = t0 + i < nvalid;
+      const bool live = full || t0 + i < nvalid;
       P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
-      if (RK == RK_LSE) P1[sl] = live ? sg * fmaf(l2, itau2, w.m - v) : 0.f;
-    });
+      if (RK == RK_LSE) P1[sl] = live ? sg * fmaf(l2, itau2, w.m - v) : 0.f;  // residual of v
+    };
+    if (full) cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+    else cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
   }
+store:
   __syncthreads();
   {
     const float* src = P0 + rpad(tid + K - 1);
@@ -166,9 +259,9 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
-    if (RK == RK_LSE && p.aux != nullptr) {  // low word of the double-float trace
+    if (RK == RK_LSE && auxr != nullptr) {  // low word of the double-float trace
       const float* src1 = P1 + rpad(tid + K - 1);
-      float* ap = p.aux + row * L + t0 + tid;
+      float* ap = auxr + t0 + tid;
 #pragma unroll
       for (int k = 0; k < RG_EPT; ++k)
         if (tid + k * T < tend) ap[k * T] = src1[k * SS];
@@ -201,45 +294,30 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
   const float* outr = p.out_in + row * L;
   const float* lor = p.aux_in ? p.aux_in + row * L : nullptr;  // low word of M (double-float)
   const int tid = threadIdx.x;
+  // phase 1: elements (e_t = -M_t, g_t 2^{-tau2 lo_t}); (-FLT_MAX, 0) outside [0, nvalid)
   {
     float* d0 = P0 + tid + (tid >> 4);
     float* d1 = P1 + tid + (tid >> 4);
     const int tt = tb + tid;
-    if (tb >= 0 && tb + N <= nvalid) {
+    const bool interior = tb >= 0 && tb + N <= nvalid;
+    const int thi = nvalid > 0 ? nvalid - 1 : 0;
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        float gv[8], mv[8], lv[8];
+    for (int h = 0; h < RG_EPT; h += 8) {
+      float gv[8], mv[8], lv[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          gv[k] = ld_na(cot + tt + (h + k) * T);
-          mv[k] = ld_na(outr + tt + (h + k) * T);
-          lv[k] = lor ? ld_na(lor + tt + (h + k) * T) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          d0[(h + k) * SS] = -sg * mv[k];
-          d1[(h + k) * SS] = lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k];
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int t = tt + (h + k) * T;
+        const int tc = interior ? t : (t < 0 ? 0 : (t > thi ? thi : t));  // clamped: no branches
+        gv[k] = ld_na(cot + tc);
+        mv[k] = ld_na(outr + tc);
+        lv[k] = lor ? ld_na(lor + tc) : 0.f;
       }
-    } else {
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        float gv[8], mv[8], lv[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int t = tt + (h + k) * T;
-          const bool v = t >= 0 && t < nvalid;
-          gv[k] = v ? ld_na(cot + t) : 0.f;
-          mv[k] = v ? ld_na(outr + t) : 0.f;
-          lv[k] = (v && lor) ? ld_na(lor + t) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int t = tt + (h + k) * T;
-          const bool v = t >= 0 && t < nvalid;
-          d0[(h + k) * SS] = v ? -sg * mv[k] : -FLT_MAX;
-          d1[(h + k) * SS] = lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k];
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int t = tt + (h + k) * T;
+        const bool v = interior || (t >= 0 && t < nvalid);
+        d0[(h + k) * SS] = v ? -sg * mv[k] : -FLT_MAX;
+        d1[(h + k) * SS] = v ? (lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k]) : 0.f;
       }
     }
   }
@@ -260,17 +338,40 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
     const int qq = tid * (RG_EPT + 1) + k;
     x[k] = RSt{P0[qq], P1[qq]};
   }
-  cav_scans<RK_GLSE>(x, tau2, P0, P1, T0, T1);
+  const bool full = tid * RG_EPT + RG_EPT <= J;
+  float f;
+  const bool wide = fs_frame(x, true, tau2, f);
+  if (!__syncthreads_or(wide)) {
+    float E[RG_EPT];
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) E[k] = x[k].s != 0.f ? x[k].s * ex2f(tau2 * (x[k].m - f)) : 0.f;
+    fs_scans(E, f, P0, T0, T1);
+    __syncthreads();
+    RSt A0, A1;
+    cav_middle<RK_GLSE, NW>(d, tau2, T0, T1, A0, A1);
+    const float fp0 = tid + d < T ? T0[tid + d] : -FLT_MAX;
+    const float fp1 = tid + d + 1 < T ? T0[tid + d + 1] : -FLT_MAX;
+    const FsCase c0 = fs_case(f, A0, fp0, tau2), c1 = fs_case(f, A1, fp1, tau2);
+    auto fin = [&](int, int, float M, float s, int sl) {
+      P0[sl] = M;
+      P1[sl] = s;
+    };
+    if (full) fs_windows<true>(E, c0, c1, d, c, 0, J, P0, fin);
+    else fs_windows<false>(E, c0, c1, d, c, 0, J, P0, fin);
+  } else {
+    cav_scans<RK_GLSE>(x, tau2, P0, P1, T0, T1);
+    __syncthreads();
+    RSt A0, A1;
+    cav_middle<RK_GLSE, NW>(d, tau2, T0, T1, A0, A1);
+    auto fin = [&](int, int, RSt w, int sl) {
+      P0[sl] = w.m;
+      P1[sl] = w.s;
+    };
+    if (full) cav_windows<RK_GLSE, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+    else cav_windows<RK_GLSE, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+  }
   __syncthreads();
-  RSt A0, A1;
-  cav_middle<RK_GLSE, NW>(d, tau2, T0, T1, A0, A1);
-  auto fin = [&](int, int, RSt w, int sl) {
-    P0[sl] = w.m;
-    P1[sl] = w.s;
-  };
-  if (tid * RG_EPT + RG_EPT <= J) cav_windows<RK_GLSE, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
-  else cav_windows<RK_GLSE, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
-  __syncthreads();
+  // phase 3: child element j = j0 + i <- window over t in [j - b, j - a] (local start i)
   Ev<M_LSE, EK> ev(p.child, row, p.mp);
   const int jn = (j0 + J < L ? j0 + J : L) - j0;
   const float padsum = padsum_sh;
@@ -289,12 +390,13 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
         const int sl = slb + (h + u) * SS;
         // S == 0 comes with m = -FLT_MAX or u_j + m <= 0: the product is an exact 0
         float g = P1[sl] * ex2f(tau2 * fmaf(sg, ev.value(j, r[u]), P0[sl]));
-        if (j == L - 1) g += padsum;
+        if (padsum != 0.f && j == L - 1) g += padsum;
         ev.grad(j, r[u], g);
       }
     }
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // backward, hard (RK_HARDI; first-argmax runs as in fg_reg.cuh)

@@ -64,11 +64,14 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        # STLG_LIB: an alternative build of the same ABI (A/B measurements of compile-time
+        # variants); it must exist like the default one — there is no CPU fallback
+        path = os.environ.get("STLG_LIB") or LIB_PATH
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2501_04194_b200.build_lib` "
+                f"{path} is missing: build it with `python -m paper_2501_04194_b200.build_lib` "
                 "(there is no CPU fallback)")
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         lib.stlg_abi_version.restype = c_int
         lib.stlg_last_error.restype = ctypes.c_char_p
         lib.stlg_compile.argtypes = [POINTER(StlgNode), c_int32, c_int32, c_int32, POINTER(StlgCfg),

@@ -39,14 +39,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    """Compile each translation unit in parallel, then link libstlg.so."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = True, out: str | None = None, extra: list | None = None) -> str:
+    """Compile each translation unit in parallel, then link libstlg.so.
+
+    `out` / `extra` build a variant library (e.g. extra=["-DCAV_LB=16"]) for A/B
+    measurements through STLG_LIB; the default build uses neither.
+    """
+    lib_out = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build_obj")
+    objdir = os.path.join(HERE, "build_obj" if out is None else "build_obj_variant")
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)] + list(extra or [])
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
@@ -58,14 +63,14 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

@@ -88,6 +88,9 @@ __device__ __forceinline__ void cav_windows(const RSt (&S)[RG_EPT], RSt A0, RSt 
 // wider chunk takes the exact path (same kernel, uniform branch).
 // ---------------------------------------------------------------------------
 constexpr float FS_RANGE = 120.f;
+#ifndef CAV_LB
+#define CAV_LB 16  // global loads batched per thread in the staging / VJP sweeps
+#endif
 
 struct FsCase {
   float M, al, be, ga;
@@ -189,16 +192,16 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
     const int jb = s0 + tid;
     const bool interior = s0 + N <= L;
 #pragma unroll
-    for (int h = 0; h < RG_EPT; h += 8) {
-      typename Ev<MODE, EK>::Raw r[8];
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      typename Ev<MODE, EK>::Raw r[CAV_LB];
       // past the row end: replicate the last sample (feeds overrun windows only)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < CAV_LB; ++k) {
         const int j = jb + (h + k) * T;
         r[k] = ev.load(interior ? j : (j < L ? j : L - 1));
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < CAV_LB; ++k) {
         const int j = jb + (h + k) * T;
         dst[(h + k) * SS] = sg * ev.value(interior ? j : (j < L ? j : L - 1), r[k]);
       }
@@ -210,10 +213,12 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
   const int i0 = tid * RG_EPT;
   const bool full = i0 + RG_EPT <= J && t0 + i0 + RG_EPT <= nvalid;
+  bool fs_done = false;
   if constexpr (RK == RK_LSE) {
     float f;
     const bool wide = fs_frame(x, false, tau2, f);
     if (!__syncthreads_or(wide)) {
+      fs_done = true;
       float E[RG_EPT];
 #pragma unroll
       for (int k = 0; k < RG_EPT; ++k) E[k] = ex2f(tau2 * (x[k].m - f));
@@ -233,12 +238,11 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
       };
       if (full) fs_windows<true>(E, c0, c1, d, c, 0, J, P0, fin);
       else fs_windows<false>(E, c0, c1, d, c, 0, J, P0, fin);
-      goto store;
     }
   }
-  cav_scans<RK>(x, tau2, P0, P1, T0, T1);  // own slots only: no barrier needed before
-  __syncthreads();
-  {
+  if (!fs_done) {
+    cav_scans<RK>(x, tau2, P0, P1, T0, T1);  // own slots only: no barrier needed before
+    __syncthreads();
     RSt A0, A1;
     cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1);
     auto fin = [&](int, int i, RSt w, int sl) {
@@ -251,7 +255,6 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
     if (full) cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
     else cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
   }
-store:
   __syncthreads();
   {
     const float* src = P0 + rpad(tid + K - 1);
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
   __shared__ float padsum_sh;
   float* P0 = rsm;
   float* P1 = rsm + C::NP;
+  float* P2 = rsm + 2 * C::NP;  // staged low words of M
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
   const int L = (int)p.L;
@@ -290,34 +294,56 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
   const int tb = j0 - p.b;  // local index 0 <-> output t = tb
   const int nvalid = L - p.b;
   const float tau2 = p.mp.tau2, sg = p.sg;
+  const float nsg = -sg, nt2sg = -tau2 * sg;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
   const float* lor = p.aux_in ? p.aux_in + row * L : nullptr;  // low word of M (double-float)
   const int tid = threadIdx.x;
-  // phase 1: elements (e_t = -M_t, g_t 2^{-tau2 lo_t}); (-FLT_MAX, 0) outside [0, nvalid)
+  // phase 1: e_t = -M_t (max space), g_t, lo_t; (-FLT_MAX, 0, 0) outside [0, nvalid)
   {
-    float* d0 = P0 + tid + (tid >> 4);
-    float* d1 = P1 + tid + (tid >> 4);
+    const int so = tid + (tid >> 4);
     const int tt = tb + tid;
-    const bool interior = tb >= 0 && tb + N <= nvalid;
-    const int thi = nvalid > 0 ? nvalid - 1 : 0;
+    if (tb >= 0 && tb + N <= nvalid) {
+      const float* cp = cot + tt;
+      const float* mp = outr + tt;
+      const float* lp = lor ? lor + tt : nullptr;
 #pragma unroll
-    for (int h = 0; h < RG_EPT; h += 8) {
-      float gv[8], mv[8], lv[8];
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        float gv[CAV_LB], mv[CAV_LB], lv[CAV_LB];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = tt + (h + k) * T;
-        const int tc = interior ? t : (t < 0 ? 0 : (t > thi ? thi : t));  // clamped: no branches
-        gv[k] = ld_na(cot + tc);
-        mv[k] = ld_na(outr + tc);
-        lv[k] = lor ? ld_na(lor + tc) : 0.f;
+        for (int k = 0; k < CAV_LB; ++k) {
+          gv[k] = ld_na(cp + (h + k) * T);
+          mv[k] = ld_na(mp + (h + k) * T);
+          lv[k] = lp ? ld_na(lp + (h + k) * T) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          P0[so + (h + k) * SS] = nsg * mv[k];
+          P1[so + (h + k) * SS] = gv[k];
+          P2[so + (h + k) * SS] = lv[k];
+        }
       }
+    } else {
+      const int thi = nvalid > 0 ? nvalid - 1 : 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int t = tt + (h + k) * T;
-        const bool v = interior || (t >= 0 && t < nvalid);
-        d0[(h + k) * SS] = v ? -sg * mv[k] : -FLT_MAX;
-        d1[(h + k) * SS] = v ? (lor ? gv[k] * ex2f(-tau2 * sg * lv[k]) : gv[k]) : 0.f;
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        float gv[CAV_LB], mv[CAV_LB], lv[CAV_LB];
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int t = tt + (h + k) * T;
+          const int tc = t < 0 ? 0 : (t > thi ? thi : t);  // clamped loads: no branches
+          gv[k] = ld_na(cot + tc);
+          mv[k] = ld_na(outr + tc);
+          lv[k] = lor ? ld_na(lor + tc) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int t = tt + (h + k) * T;
+          const bool v = t >= 0 && t < nvalid;
+          P0[so + (h + k) * SS] = v ? nsg * mv[k] : -FLT_MAX;
+          P1[so + (h + k) * SS] = v ? gv[k] : 0.f;
+          P2[so + (h + k) * SS] = v ? lv[k] : 0.f;
+        }
       }
     }
   }
@@ -333,18 +359,22 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
   }
   __syncthreads();
   RSt x[RG_EPT];
+  float lw[RG_EPT];
 #pragma unroll
   for (int k = 0; k < RG_EPT; ++k) {
     const int qq = tid * (RG_EPT + 1) + k;
     x[k] = RSt{P0[qq], P1[qq]};
+    lw[k] = P2[qq];
   }
   const bool full = tid * RG_EPT + RG_EPT <= J;
   float f;
   const bool wide = fs_frame(x, true, tau2, f);
   if (!__syncthreads_or(wide)) {
+    // E = g 2^{tau2 (e - lo - f)} (one ex2; the low word shifts the exponent)
     float E[RG_EPT];
 #pragma unroll
-    for (int k = 0; k < RG_EPT; ++k) E[k] = x[k].s != 0.f ? x[k].s * ex2f(tau2 * (x[k].m - f)) : 0.f;
+    for (int k = 0; k < RG_EPT; ++k)
+      E[k] = x[k].s != 0.f ? x[k].s * ex2f(fmaf(tau2, x[k].m - f, nt2sg * lw[k])) : 0.f;
     fs_scans(E, f, P0, T0, T1);
     __syncthreads();
     RSt A0, A1;
@@ -359,6 +389,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
     if (full) fs_windows<true>(E, c0, c1, d, c, 0, J, P0, fin);
     else fs_windows<false>(E, c0, c1, d, c, 0, J, P0, fin);
   } else {
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) x[k].s = x[k].s != 0.f ? x[k].s * ex2f(nt2sg * lw[k]) : 0.f;
     cav_scans<RK_GLSE>(x, tau2, P0, P1, T0, T1);
     __syncthreads();
     RSt A0, A1;
@@ -377,36 +409,58 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
   const float padsum = padsum_sh;
   const int slb = rpad(tid + K - 1);
   const int jb = j0 + tid;
+  const int jpad = L - 1 - jb;  // (h + u) T == jpad <=> element L - 1
 #pragma unroll
-  for (int h = 0; h < RG_EPT; h += 8) {
-    typename Ev<M_LSE, EK>::Raw r[8];
+  for (int h = 0; h < RG_EPT; h += CAV_LB) {
+    typename Ev<M_LSE, EK>::Raw r[CAV_LB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CAV_LB; ++u)
       if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < CAV_LB; ++u) {
       if (tid + (h + u) * T < jn) {
         const int j = jb + (h + u) * T;
         const int sl = slb + (h + u) * SS;
         // S == 0 comes with m = -FLT_MAX or u_j + m <= 0: the product is an exact 0
         float g = P1[sl] * ex2f(tau2 * fmaf(sg, ev.value(j, r[u]), P0[sl]));
-        if (padsum != 0.f && j == L - 1) g += padsum;
+        g += ((h + u) * T == jpad) ? padsum : 0.f;
         ev.grad(j, r[u], g);
       }
     }
   }
 }
 
+// ---------------------------------------------------------------------------
+// backward, hard (RK_HARDI).  The first argmax a(i) of window i is
+// non-decreasing in i, so the windows routed to one child element form one
+// contiguous run of window starts.  Each thread sums its runs in registers; a
+// segmented warp-shuffle scan (plus one cross-warp step) carries the runs that
+// continue across chunk boundaries, and every run total is written once, by the
+// thread holding its last window, with a plain shared store: deterministic, no
+// atomics.  Then the fused child VJP over the owned elements.
+// ---------------------------------------------------------------------------
+struct RunSeg {
+  int key;    // key of the trailing run
+  float s;    // its (partial) sum
+  int whole;  // the trailing run covers the whole covered range
+};
+__device__ __forceinline__ RunSeg run_comb(RunSeg lo, RunSeg hi) {  // lo: earlier windows
+  return (hi.whole && hi.key == lo.key) ? RunSeg{hi.key, lo.s + hi.s, lo.whole} : hi;
+}
+__device__ __forceinline__ RunSeg run_shfl_up(RunSeg v, int o) {
+  return RunSeg{__shfl_up_sync(0xffffffffu, v.key, o), __shfl_up_sync(0xffffffffu, v.s, o),
+                __shfl_up_sync(0xffffffffu, v.whole, o)};
+}
 
-// ---------------------------------------------------------------------------
-// backward, hard (RK_HARDI; first-argmax runs as in fg_reg.cuh)
-// ---------------------------------------------------------------------------
 template <int EK, int NW>
 __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
+  constexpr int NOKEY = 0x7fffffff;  // windows past the tile: g = 0, key above every element
   extern __shared__ float rsm[];
   __shared__ float T0[T], T1[T];
+  __shared__ RunSeg WR[NW];
+  __shared__ int WK[NW];
   __shared__ float padsum_sh;
   float* P0 = rsm;
   float* P1 = rsm + C::NP;
@@ -423,45 +477,33 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
   const float sg = p.sg;
   const float* cot = p.cot + row * L;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
+  // phase 1: child values u (window start i <-> t = first + i - a), clamped loads
   {
-    float* d0 = P0 + tid + (tid >> 4);
-    float* d1 = P1 + tid + (tid >> 4);
+    const int so = tid + (tid >> 4);
     const int jb = first + tid;
     const int tb = jb - p.a;
-    if (first >= 0 && first + N <= L && first - p.a >= 0 && first - p.a + nwin <= nvalid) {
+    const int thi = nvalid > 0 ? nvalid - 1 : 0;
+    const bool interior = first >= 0 && first + N <= L && first - p.a >= 0 && first - p.a + nwin <= nvalid;
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        typename Ev<M_HARD, EK>::Raw r[8];
-        float gv[8];
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      typename Ev<M_HARD, EK>::Raw r[CAV_LB];
+      float gv[CAV_LB];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          r[k] = ev.load(jb + (h + k) * T);
-          gv[k] = (tid + (h + k) * T < nwin) ? ld_na(cot + tb + (h + k) * T) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          d0[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
-          d1[(h + k) * SS] = gv[k];
-        }
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int j = jb + (h + k) * T, t = tb + (h + k) * T;
+        r[k] = ev.load(interior ? j : (j < 0 ? 0 : (j >= L ? L - 1 : j)));
+        gv[k] = ld_na(cot + (interior ? t : (t < 0 ? 0 : (t > thi ? thi : t))));
       }
-    } else {
 #pragma unroll
-      for (int h = 0; h < RG_EPT; h += 8) {
-        typename Ev<M_HARD, EK>::Raw r[8];
-        float gv[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = jb + (h + k) * T, t = tb + (h + k) * T;
-          if (j >= 0 && j < L) r[k] = ev.load(j);
-          gv[k] = (tid + (h + k) * T < nwin && t >= 0 && t < nvalid) ? ld_na(cot + t) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int j = jb + (h + k) * T;
-          d0[(h + k) * SS] = (j >= 0 && j < L) ? sg * ev.value(j, r[k]) : 0.f;
-          d1[(h + k) * SS] = gv[k];
-        }
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int i = tid + (h + k) * T;
+        const int j = jb + (h + k) * T, t = tb + (h + k) * T;
+        const int jc = interior ? j : (j < 0 ? 0 : (j >= L ? L - 1 : j));
+        const bool wv = i < nwin && (interior || (t >= 0 && t < nvalid));
+        P0[so + (h + k) * SS] = sg * ev.value(jc, r[k]);  // out-of-row samples feed no live window
+        P1[so + (h + k) * SS] = wv ? gv[k] : 0.f;
       }
     }
   }
@@ -491,44 +533,75 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
   __syncthreads();
   RSt A0, A1;
   cav_middle<RK_HARDI, NW>(d, 0.f, T0, T1, A0, A1);
+  int key[RG_EPT];
   {
-    int cur = -1;
+    auto fin = [&](int k, int, RSt w, int) { key[k] = __float_as_int(w.s); };
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) key[k] = NOKEY;
+    if (tid * RG_EPT + RG_EPT <= nwin) cav_windows<RK_HARDI, true>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
+    else cav_windows<RK_HARDI, false>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
+  }
+  // runs of equal keys (ascending window order); interior runs are written directly
+  const int kf = key[0];
+  float sf = 0.f, sl = 0.f;
+  {
+    int cur = kf;
     float acc = 0.f;
-    bool top = true;  // the current run touches the chunk's upper end
-    auto fin = [&](int k, int, RSt w, int) {
-      const int am = __float_as_int(w.s);
-      if (am != cur) {
-        if (cur >= 0) {
-          if (top) atomicAdd(&G[rpad(cur)], acc);
-          else G[rpad(cur)] = acc;
-        }
-        top = cur < 0;
-        cur = am;
+    bool firstrun = true;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) {
+      if (key[k] != cur) {
+        if (firstrun) sf = acc;
+        else if (cur != NOKEY) G[rpad(cur)] = acc;
+        firstrun = false;
+        cur = key[k];
         acc = 0.f;
       }
       acc += g[k];
-    };
-    if (tid * RG_EPT + RG_EPT <= nwin) cav_windows<RK_HARDI, true>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
-    else cav_windows<RK_HARDI, false>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
-    if (cur >= 0) atomicAdd(&G[rpad(cur)], acc);
+    }
+    sl = acc;
+    if (firstrun) sf = acc;
   }
+  const int kl = key[RG_EPT - 1];
+  const bool single = kf == kl;
+  // carries: inclusive segmented scan of the trailing runs over lanes, then warps
+  RunSeg v{kl, sl, single};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const RunSeg y = run_shfl_up(v, o);
+    if (lane >= o) v = run_comb(y, v);
+  }
+  RunSeg ex = run_shfl_up(v, 1);
+  const int kf_next_lane = __shfl_down_sync(0xffffffffu, kf, 1);
+  if (lane == 31) WR[warp] = v;
+  if (lane == 0) WK[warp] = kf;
   __syncthreads();
+  RunSeg wc{NOKEY, 0.f, 0};  // fold of the warps below
+  for (int w = 0; w < warp; ++w) wc = (w == 0) ? WR[0] : run_comb(wc, WR[w]);
+  const RunSeg cin = lane == 0 ? wc : (warp > 0 ? run_comb(wc, ex) : ex);
+  const float carry = (cin.key == kf && kf != NOKEY) ? cin.s : 0.f;
+  const int kn = lane < 31 ? kf_next_lane : (warp + 1 < NW ? WK[warp + 1] : NOKEY - 1);
+  if (!single && kf != NOKEY) G[rpad(kf)] = carry + sf;  // first run ends inside this chunk
+  if (kl != NOKEY && kn != kl) G[rpad(kl)] = single ? carry + sl : sl;  // trailing run ends here
+  __syncthreads();
+  // phase 3: owned local indices [K - 1, K - 1 + Jo)
   const int jn = (j0 + Jo < L ? j0 + Jo : L) - j0;
   const float padsum = padsum_sh;
   const int gb = rpad(tid + K - 1);
   const int jb = j0 + tid;
+  const int jpad = L - 1 - jb;
 #pragma unroll
-  for (int h = 0; h < RG_EPT; h += 8) {
-    typename Ev<M_HARD, EK>::Raw r[8];
+  for (int h = 0; h < RG_EPT; h += CAV_LB) {
+    typename Ev<M_HARD, EK>::Raw r[CAV_LB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < CAV_LB; ++u)
       if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < CAV_LB; ++u) {
       if (tid + (h + u) * T < jn) {
         const int j = jb + (h + u) * T;
         float gg = G[gb + (h + u) * SS];
-        if (j == L - 1) gg += padsum;
+        gg += ((h + u) * T == jpad) ? padsum : 0.f;
         ev.grad(j, r[u], gg);
       }
     }

@@ -20,11 +20,16 @@ p = np.asarray(rng.uniform(-1, 1, (B, 1, 2)) + np.cumsum(0.05 * rng.normal(0, 1,
                dtype=np.float32)
 dev = torch.device("cuda", 0)
 pt = torch.tensor(p, device=dev)
-cfg = P.SemanticsConfig(mode={"lse": P.LogSumExp(10.0), "hard": P.Hard(), "soft": P.SoftMax(10.0)}[mode])
-if mode == "hard":
-    f = P.Eventually(P.Pred("px", ">", 0.5), P.StepInterval(10, 100))
-    names = ["px"]
-    chans = [pt[..., 0]]
+cfg = P.SemanticsConfig(mode={"lse": P.LogSumExp(10.0), "hard": P.Hard(), "hard1d": P.Hard(),
+                               "soft": P.SoftMax(10.0)}[mode])
+if mode == "hard1d":  # C1's formula at full size, contiguous 1-D signal
+    f = P.Always(P.Pred("x", ">", 0.5), P.StepInterval(0, 50))
+    names = ["x"]
+    chans = [pt[..., 0].contiguous()]
+elif mode == "hard":
+    f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
+    names = ["px", "py"]
+    chans = [pt[..., 0], pt[..., 1]]
 else:
     f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
     names = ["px", "py"]
@@ -39,6 +44,7 @@ dp = torch.zeros(B, T, 2, device=dev)
 s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(steps):
     comp.forward(chans, [], out, fws, s)
-    comp.backward(chans, [], out, ones, [dp[..., i] for i in range(len(chans))], None, fws, bws, s)
+    grads = [dp[..., 0].contiguous()] if mode == "hard1d" else [dp[..., i] for i in range(len(chans))]
+    comp.backward(chans, [], out, ones, grads, None, fws, bws, s)
 torch.cuda.synchronize()
 print("ok", float(out[0, 0]), float(dp.abs().sum()))

@@ -10,18 +10,30 @@ B, T = 1024, 10_000
 rng = np.random.default_rng(1)
 p = np.asarray(rng.uniform(-1, 1, (B, 1, 2)) + np.cumsum(0.05 * rng.normal(0, 1, (B, T, 2)), 1), dtype=np.float32)
 dev = torch.device("cuda", 0)
-cfg = P.SemanticsConfig(mode={"lse": P.LogSumExp(10.0), "hard": P.Hard(), "soft": P.SoftMax(10.0)}[mode])
-f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
-comp = compile_formula(f, ["px", "py"], cfg)
+cfg = P.SemanticsConfig(mode={"lse": P.LogSumExp(10.0), "hard": P.Hard(), "hard1d": P.Hard(),
+                               "soft": P.SoftMax(10.0)}[mode])
+if mode == "hard1d":  # C1's formula at full size: Always[0,50](x > 0.5), contiguous 1-D signal
+    f = P.Always(P.Pred("x", ">", 0.5), P.StepInterval(0, 50))
+    comp = compile_formula(f, ["x"], cfg)
+else:
+    f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
+    comp = compile_formula(f, ["px", "py"], cfg)
 sets = [torch.tensor(np.roll(p, 17 * i, 1), device=dev) for i in range(3)]
+if mode == "hard1d":
+    sets = [s_[..., 0].contiguous() for s_ in sets]
 fb, bb = comp.workspace_bytes(B, T)
 fws = torch.empty(fb, dtype=torch.uint8, device=dev); bws = torch.empty(bb, dtype=torch.uint8, device=dev)
 outs = [torch.empty(B, T, device=dev) for _ in range(3)]
 dps = [torch.empty(B, T, 2, device=dev) for _ in range(3)]
 ones = torch.ones(B, T, device=dev)
 def cur(): return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-def fwd(i): comp.forward([sets[i][..., 0], sets[i][..., 1]], [], outs[i], fws, cur())
-def bwd(i): comp.backward([sets[i][..., 0], sets[i][..., 1]], [], outs[i], ones, [dps[i][..., 0], dps[i][..., 1]], None, fws, bws, cur())
+if mode == "hard1d":
+    dps = [torch.empty(B, T, device=dev) for _ in range(3)]
+    def fwd(i): comp.forward([sets[i]], [], outs[i], fws, cur())
+    def bwd(i): comp.backward([sets[i]], [], outs[i], ones, [dps[i]], None, fws, bws, cur())
+else:
+    def fwd(i): comp.forward([sets[i][..., 0], sets[i][..., 1]], [], outs[i], fws, cur())
+    def bwd(i): comp.backward([sets[i][..., 0], sets[i][..., 1]], [], outs[i], ones, [dps[i][..., 0], dps[i][..., 1]], None, fws, bws, cur())
 for i in range(6): fwd(i % 3); bwd(i % 3)
 torch.cuda.synchronize()
 gf, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()

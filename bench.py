@@ -182,6 +182,52 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _hard_c1(P, compile_formula, dev, B, T, args, cur_stream):
+    """C1's formula Always[0,50](x > 0.5) (Hard, last pad) on a contiguous 1-D fp32
+    N(0,1) signal at B x T: fwd + ones-cotangent bwd through CUDA graphs over 3
+    rotating sets (3 x 123 MB > L2).  Algorithmic bytes 16 B / unit."""
+    import torch
+    f = P.Always(P.Pred("x", ">", 0.5), P.StepInterval(0, 50))
+    comp = compile_formula(f, ["x"], P.SemanticsConfig(mode=P.Hard()))
+    g = torch.Generator(device=dev).manual_seed(0)
+    sets = [{"x": torch.randn(B, T, device=dev, generator=g), "out": torch.empty(B, T, device=dev),
+             "dx": torch.empty(B, T, device=dev)} for _ in range(3)]
+    fb, bb = comp.workspace_bytes(B, T)
+    fws = torch.empty(max(fb, 1), dtype=torch.uint8, device=dev)
+    bws = torch.empty(max(bb, 1), dtype=torch.uint8, device=dev)
+    ones = torch.ones(B, T, device=dev)
+    graphs = []
+    for d in sets:
+        comp.forward([d["x"]], [], d["out"], fws, cur_stream())
+        comp.backward([d["x"]], [], d["out"], ones, [d["dx"]], None, fws, bws, cur_stream())
+    torch.cuda.synchronize()
+    for d in sets:
+        gf, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gf):
+            comp.forward([d["x"]], [], d["out"], fws, cur_stream())
+        with torch.cuda.graph(gb):
+            comp.backward([d["x"]], [], d["out"], ones, [d["dx"]], None, fws, bws, cur_stream())
+        graphs.append((gf, gb))
+    for i in range(3):
+        graphs[i % 3][0].replay()
+        graphs[i % 3][1].replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        graphs[i % 3][0].replay()
+        ev[i][1].record(stream)
+        graphs[i % 3][1].replay()
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    bwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    return {"formula": "Always[0,50](x > 0.5), Hard, 1-D N(0,1)", "global_batch": B, "seq_len": T,
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "value": B * T / ((fwd_ms + bwd_ms) / 1e3), "unit": UNIT,
+            "alg_bytes_per_unit": 16}
+
+
 def run_b200(args, rank, world):
     import numpy as np
     import torch
@@ -286,6 +332,9 @@ def run_b200(args, rank, world):
     ms_step = ms / args.steps
     value = B * T * world / (ms_step / 1e3)
 
+    # ---- hard mode at the same scale (C1's formula, SURVEY §8(d) HBM row) ----
+    hard = _hard_c1(P, compile_formula, dev, B, T, args, _cur_stream)
+
     # ---- e2e through the public API: pinned host -> device -> host ----------
     hp = torch.tensor(host).pin_memory()
     h_tr = torch.empty(B, T).pin_memory()
@@ -362,6 +411,8 @@ def run_b200(args, rank, world):
                         "d2h_bytes_per_step": B * T * 4 + B * T * 2 * 4,
                         "ms_per_step": e2e_ms, "path": "paper_2501_04194_b200.trace + autograd"},
                 "gpu_launches": int(launches),
+                "hard_c1": dict(hard, roofline_frac=(16.0 * B * T / ((hard["fwd_ms"] + hard["bwd_ms"]) / 1e3))
+                                / 1e9 / hbm),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if dist:

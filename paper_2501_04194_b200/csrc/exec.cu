@@ -471,13 +471,6 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     e.out_slot = -1;
     plan->entries.push_back(e);
   }
-  if (cfg->masked_fill) {
-    for (auto& e : plan->entries)
-      if (e.kind == E_UNTIL) {
-        delete plan;
-        return fail(STLG_E_UNSUPPORTED, "masked_fill Until is not supported on the device path yet");
-      }
-  }
   mark_first_writers(plan);
   *out_plan = plan;
   return STLG_OK;
@@ -673,6 +666,9 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       p.pad_last = plan->cfg.pad_last;
       p.pad_value = (float)plan->cfg.pad_value;
       p.canon = (!e.untimed && e.b > 0 && (long long)T - e.b > 0) ? 1 : 0;
+      p.fill = plan->cfg.masked_fill;
+      p.sent = (float)plan->cfg.sentinel;
+      if (p.fill) p.canon = 0;  // no _replace_overrun in masked_fill mode (masking.py:261-274)
       p.mp = mode_params(plan->cfg);
       ce = launch_until_fwd(mode, p, st);
     } else {  // E_FG_SMOOTH
@@ -739,6 +735,8 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.untimed = e.untimed;
       p.pad_last = plan->cfg.pad_last;
       p.pad_value = (float)plan->cfg.pad_value;
+      p.fill = plan->cfg.masked_fill;
+      p.sent = (float)plan->cfg.sentinel;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH

@@ -45,6 +45,8 @@ struct UParams {
   int pad_last;
   float pad_value;
   int canon;
+  int fill;    // masked_fill compat: sentinel-filled columns, no overrun rule (masking.py:261-270)
+  float sent;  // SemanticsConfig.sentinel
   ModeP mp;
 };
 

@@ -44,9 +44,12 @@ __device__ __forceinline__ void stage_children(const UParams& p, long long row, 
     if (j < p.L) {
       Ls[i] = expr_eval<MODE>(p.left, row, j, p.mp);
       Rs[i] = expr_eval<MODE>(p.right, row, j, p.mp);
+    } else if (p.pad_last) {  // padded rows (read by masked_fill windows only)
+      Ls[i] = expr_eval<MODE>(p.left, row, p.L - 1, p.mp);
+      Rs[i] = expr_eval<MODE>(p.right, row, p.L - 1, p.mp);
     } else {
-      Ls[i] = 0.f;
-      Rs[i] = 0.f;
+      Ls[i] = p.pad_value;
+      Rs[i] = p.pad_value;
     }
   }
 }
@@ -95,14 +98,50 @@ __device__ __forceinline__ float term_of(float pm, float r, const ModeP& mp, flo
   return pair_red<MODE>(pm, r, -1.f, mp, p1, p2);
 }
 
+// masked_fill (masking.py:261-270): pm_k and the right operand are reductions over
+// FULL columns of `rows` entries, the kept rows plus sentinel fills (+sent for a min,
+// i.e. -sent in max space).  (MX, lse): the kept part's reduction in max space (and
+// its LSE for softmax).  Returns the filled l-space value; lse becomes the filled LSE;
+// `kept` is false when a sentinel wins the hard min (then no gradient flows).
+template <int MODE>
+__device__ __forceinline__ float fill_min(float MX, float& lse, float nu, float sent, bool sent_first,
+                                          float tau2, float itau2, bool& kept) {
+  kept = fill_merge<MODE>(MX, lse, nu, sent, sent_first, tau2, itau2);
+  if (MODE == M_LSE) lse = MX;
+  return -MX;
+}
+// (max-space value, LSE) of a PmState
+template <int MODE>
+__device__ __forceinline__ void pm_mx(const PmState<MODE>& pm, float itau2, float& MX, float& lse) {
+  if (MODE == M_HARD) {
+    MX = pm.m;
+    lse = pm.m;
+  } else if (MODE == M_LSE) {
+    MX = fmaf(lg2f(pm.s), itau2, pm.m);
+    lse = MX;
+  } else {
+    MX = pm.m + pm.q / pm.s;
+    lse = fmaf(lg2f(pm.s), itau2, pm.m);
+  }
+}
+// d(filled min)/d(element) for an element x (l space) of that column
+template <int MODE>
+__device__ __forceinline__ float fill_weight(float x, float vfill, float lse, float tau, float tau2, bool kept) {
+  if (MODE == M_HARD) return kept ? 1.f : 0.f;
+  const float w = ex2f(tau2 * (-x - lse));
+  if (MODE == M_LSE) return w;
+  return w * fmaf(tau, vfill - x, 1.f);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__ UParams p) {
   extern __shared__ __align__(16) float sm[];
   const long long row = blockIdx.y, L = p.L;
   const long long t0 = (long long)blockIdx.x * U_THREADS;
-  const long long nvalid = p.untimed ? L : L - p.b;
+  const long long nvalid = (p.untimed || p.fill) ? L : L - p.b;
   const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
-  const int nst = (int)((t0 + span <= L) ? span : (L - t0));
+  const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
+  const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
   float* Ls = sm;
   float* Rs = sm + nst;
   if (t0 < nvalid) stage_children<MODE>(p, row, t0, nst, Ls, Rs);
@@ -127,7 +166,18 @@ __global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__
       int e = i0 + p.a + k;
       if (k > 0) pm.push(Ls[e], e, tau2);
       float w1, w2;
-      float term = term_of<MODE>(pm.value(itau2), Rs[e], p.mp, w1, w2);
+      float pmv, rv = Rs[e];
+      if (p.fill) {
+        float MX, lse;
+        bool kept;
+        pm_mx<MODE>(pm, itau2, MX, lse);
+        pmv = fill_min<MODE>(MX, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kept);
+        float lr = -rv;
+        rv = fill_min<MODE>(-rv, lr, (float)(rows - 1), p.sent, t + p.a + k > 0, tau2, itau2, kept);
+      } else {
+        pmv = pm.value(itau2);
+      }
+      float term = term_of<MODE>(pmv, rv, p.mp, w1, w2);
       if (MODE == M_HARD) {
         if (k == 0 || term > M) M = term;  // first k wins ties
       } else if (MODE == M_LSE) {
@@ -150,6 +200,10 @@ __global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__
     if (MODE == M_HARD) v = M;
     else if (MODE == M_LSE) v = fmaf(lg2f(S), itau2, M);
     else v = M + Q / S;
+    if (p.fill && p.untimed && t > 0) {  // slices past the end: -sentinel terms (masking.py:271-273)
+      float lse = (MODE == M_SOFT) ? fmaf(lg2f(S), itau2, M) : v;
+      fill_merge<MODE>(v, lse, (float)t, p.sent, false, tau2, itau2);
+    }
   }
   if (p.canon) v = __fadd_rn(v, 0.f);
   p.out[row * L + t] = v;
@@ -173,14 +227,23 @@ struct Systolic {
     float got = __shfl_sync(0xffffffffu, val, src);
     long long j = base + k + ((lane - k) & 31);
     if (j != cur) {
-      if (cur >= 0 && cur < L && acc != 0.f) atomicAdd(dst + cur, acc);
+      put(dst, L);
       cur = j;
       acc = 0.f;
     }
     acc += got;
   }
+  // padded positions (masked_fill windows past the end) feed element L - 1 under
+  // 'last' padding (pad_last is set by the caller) and nothing under a constant pad
+  int pad_last = 0;
+  __device__ __forceinline__ void put(float* dst, long long L) {
+    if (cur >= 0 && acc != 0.f) {
+      if (cur < L) atomicAdd(dst + cur, acc);
+      else if (pad_last) atomicAdd(dst + L - 1, acc);
+    }
+  }
   __device__ __forceinline__ void flush(float* dst, long long L) {
-    if (cur >= 0 && cur < L && acc != 0.f) atomicAdd(dst + cur, acc);
+    put(dst, L);
     reset();
   }
 };
@@ -203,9 +266,10 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
   extern __shared__ __align__(16) float sm[];
   const long long row = blockIdx.y, L = p.L;
   const long long t0 = (long long)blockIdx.x * U_THREADS;
-  const long long nvalid = p.untimed ? L : L - p.b;
+  const long long nvalid = (p.untimed || p.fill) ? L : L - p.b;
   const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
-  const int nst = (int)((t0 + span <= L) ? span : (L - t0));
+  const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
+  const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
   const int Kmax = p.untimed ? (int)(L - t0) : p.K;
   const int nck = (Kmax + U_CB - 1) / U_CB;
   float* Ls = sm;
@@ -247,20 +311,33 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
     pm.init(Ls[tid], tid);
     for (int i = 1; i <= p.a; ++i) pm.push(Ls[tid + i], tid + i, tau2);
     float best = 0.f;
-    int bsrc = 0;  // tile-local index; bit 30 set: right child
+    int bsrc = 0;  // tile-local index; bit 30 set: right child; -1: a sentinel won
     for (int k = 0; k < K; ++k) {
       int e = tid + p.a + k;
       if (k > 0) pm.push(Ls[e], e, tau2);
       float pmv = -pm.m, r = Rs[e];
+      bool kl = true, kr = true;
+      if (p.fill) {
+        float lse = pm.m;
+        pmv = fill_min<M_HARD>(pm.m, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kl);
+        float lr = -r;
+        r = fill_min<M_HARD>(-r, lr, (float)(rows - 1), p.sent, t + p.a + k > 0, tau2, itau2, kr);
+      }
       bool use_l = pmv <= r;
       float term = use_l ? pmv : r;
       if (k == 0 || term > best) {
         best = term;
-        bsrc = use_l ? pm.i : (e | (1 << 30));
+        bsrc = use_l ? (kl ? pm.i : -1) : (kr ? (e | (1 << 30)) : -1);
       }
     }
-    if (bsrc & (1 << 30)) atomicAdd(gr + t0 + (bsrc & ~(1 << 30)), g);
-    else atomicAdd(gl + t0 + bsrc, g);
+    if (p.fill && p.untimed && t > 0 && best < -p.sent) bsrc = -1;  // -sentinel terms win
+    if (bsrc < 0) return;
+    long long j = t0 + (bsrc & ~(1 << 30));
+    if (j >= L) {  // padded row: 'last' padding reads element L - 1
+      if (!p.pad_last) return;
+      j = L - 1;
+    }
+    atomicAdd(((bsrc & (1 << 30)) ? gr : gl) + j, g);
     return;
   }
 
@@ -282,7 +359,16 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
       }
       if (MODE == M_SOFT) {
         float w1, w2;
-        float term = term_of<MODE>(pm.value(itau2), Rs[e], p.mp, w1, w2);
+        float pmv = pm.value(itau2), rv = Rs[e];
+        if (p.fill) {
+          float MX, lse;
+          bool kept;
+          pm_mx<MODE>(pm, itau2, MX, lse);
+          pmv = fill_min<MODE>(MX, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kept);
+          float lr = -rv;
+          rv = fill_min<MODE>(-rv, lr, (float)(rows - 1), p.sent, t + p.a + k > 0, tau2, itau2, kept);
+        }
+        float term = term_of<MODE>(pmv, rv, p.mp, w1, w2);
         if (k == 0) {
           M = term;
           S = 1.f;
@@ -291,12 +377,14 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
         }
       }
     }
+    if (MODE == M_SOFT && p.fill && p.untimed && t > 0 && K > 0) lse_merge(M, S, -p.sent, (float)t, tau2);
     Lout = (MODE == M_SOFT) ? fmaf(lg2f(S), itau2, M) : out_t;
   }
   // ---- pass 2: backwards over checkpoint blocks -------------------------------
   Systolic accL, accR;
   accL.reset();
   accR.reset();
+  accL.pad_last = accR.pad_last = p.pad_last;
   const long long base = t0 + p.a;  // lane i, step k -> element base + k + i (within the warp's t0)
   const int lane = tid & 31;
   const long long wbase = t0 + (tid & ~31) + p.a;
@@ -321,8 +409,16 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
         int e = tid + p.a + k;
         if (k > k_lo) st.push(Ls[e], e, tau2);
         float* bb = BUF + (size_t)(k - k_lo) * 2 * U_THREADS;
-        bb[tid] = st.value(itau2);                                          // pm_k
-        bb[U_THREADS + tid] = (MODE == M_SOFT) ? fmaf(lg2f(st.s), itau2, st.m) : 0.f;  // L_pm (x space)
+        if (p.fill) {  // the filled column's min and LSE
+          float MX, lse;
+          bool kept;
+          pm_mx<MODE>(st, itau2, MX, lse);
+          bb[tid] = fill_min<MODE>(MX, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kept);
+          bb[U_THREADS + tid] = lse;
+        } else {
+          bb[tid] = st.value(itau2);                                          // pm_k
+          bb[U_THREADS + tid] = (MODE == M_SOFT) ? fmaf(lg2f(st.s), itau2, st.m) : 0.f;  // L_pm (x space)
+        }
       }
     }
     for (int k = k_hi - 1; k >= k_lo; --k) {
@@ -332,12 +428,20 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
         float* bb = BUF + (size_t)(k - k_lo) * 2 * U_THREADS;
         float pmk = bb[tid];
         float r = Rs[e];
+        float dr = 1.f;  // d(filled right operand) / d r
+        if (p.fill) {
+          float lr = -r;
+          bool kept;
+          const float rf = fill_min<MODE>(-r, lr, (float)(rows - 1), p.sent, t + p.a + k > 0, tau2, itau2, kept);
+          dr = fill_weight<MODE>(r, rf, lr, tau, tau2, kept);
+          r = rf;
+        }
         float w1, w2;
         float term = term_of<MODE>(pmk, r, p.mp, w1, w2);
         if (MODE == M_LSE) {
           // dr: g exp(tau (term - out)) * w2 ; dpm: g exp(tau (term - out)) * w1
           float wk = ex2f(tau2 * (term - out_t));
-          vr = g * wk * w2;
+          vr = g * wk * w2 * dr;
           float c_pm = g * wk * w1;  // = g exp(tau (2 term - out - pm))
           // SA_k = c_pm_k / g-scale + exp(-tau (pm_k - pm_{k+1})) SA_{k+1}   (ref pm_k)
           SA = have ? fmaf(SA, ex2f(-tau2 * (pmk - prev_ref)), c_pm) : c_pm;
@@ -349,7 +453,7 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
           if (k == 0) pm0 = pmk;
         } else {
           float Wk = ex2f(tau2 * (term - Lout)) * fmaf(tau, term - out_t, 1.f);
-          vr = g * Wk * w2;
+          vr = g * Wk * w2 * dr;
           float c_pm = g * Wk * w1;
           float Lpm = bb[U_THREADS + tid];
           // dl_j = exp(tau (-l_j - Lpm_k0)) [ (1 + tau (pm_k0 - l_j)) SA + tau SB ]
@@ -566,12 +670,12 @@ static const size_t kUSmemMax = 220 * 1024;
 
 static size_t fwd_smem(const UParams& p) {
   long long span = p.untimed ? p.L : (long long)U_THREADS + p.b;
-  if (span > p.L) span = p.L;
+  if (span > p.L && !p.fill) span = p.L;
   return (size_t)2 * span * 4;
 }
 static size_t bwd_smem(const UParams& p) {
   long long span = p.untimed ? p.L : (long long)U_THREADS + p.b;
-  if (span > p.L) span = p.L;
+  if (span > p.L && !p.fill) span = p.L;
   long long kmax = p.untimed ? p.L : p.K;
   long long nck = (kmax + U_CB - 1) / U_CB;
   return (size_t)2 * span * 4 + (size_t)nck * 3 * U_THREADS * 4 + (size_t)U_CB * 2 * U_THREADS * 4;
@@ -579,7 +683,7 @@ static size_t bwd_smem(const UParams& p) {
 
 template <int MODE>
 static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
-  if (p.untimed && MODE == M_HARD) {
+  if (p.untimed && MODE == M_HARD && !p.fill) {
     k_until_unt_hard_fwd<MODE><<<(unsigned)p.B, UH_T, 0, st>>>(p);
     count_launch();
     return cudaGetLastError();
@@ -596,7 +700,7 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
 
 template <int MODE>
 static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
-  if (p.untimed && MODE == M_HARD) {
+  if (p.untimed && MODE == M_HARD && !p.fill) {
     k_until_unt_hard_bwd<MODE><<<(unsigned)p.B, UH_T, 0, st>>>(p);
     count_launch();
     return cudaGetLastError();

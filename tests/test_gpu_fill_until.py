@@ -1,0 +1,66 @@
+"""masked_fill (compat mode) Until on the device vs the oracle (SURVEY §8(a) a8 + a9).
+
+In masked_fill mode the reference builds every pm_k and right operand as a reduction
+over a FULL sentinel-filled column (`_fill_reduce_columns`, masking.py:195-202, 261-270),
+the untimed outer max sees -sentinel for the slices past the end (masking.py:271-273)
+and there is no overrun replacement.  A small sentinel makes the filled entries
+numerically active in the smooth modes (the reference's documented hazard,
+core.py:260-265), so the sweep checks the sentinel algebra, not just its underflow.
+"""
+
+import numpy as np
+import pytest
+
+from devhelp import assert_hard_equal, rel_err, run_device
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_04194_b200 as P
+    P._lib.load()
+    return P
+
+
+def _oracle():
+    import os
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(here, "..", "oracle"))
+    import stl_oracle
+    return stl_oracle
+
+
+@pytest.mark.parametrize("mode", ["hard", "lse", "soft"])
+@pytest.mark.parametrize("iv", [None, (0, 3), (2, 9)], ids=["untimed", "a0b3", "a2b9"])
+@pytest.mark.parametrize("pad", ["last", "const"])
+@pytest.mark.parametrize("sent", [1e5, 4.0])
+@pytest.mark.parametrize("L", [30, 150])
+def test_masked_fill_until_vs_oracle(cuda, mode, iv, pad, sent, L):
+    P = cuda
+    orc = _oracle()
+    rng = np.random.default_rng(hash((mode, iv, pad, sent, L)) % 2**32)
+    x = np.asarray(rng.normal(0, 1.5, (2, L)), dtype=np.float32).astype(np.float64)
+    y = np.asarray(rng.normal(0.2, 1.5, (2, L)), dtype=np.float32).astype(np.float64)
+    if mode == "hard":  # ties for the first-index rules
+        x, y = np.round(x), np.round(y)
+    m = {"hard": P.Hard(), "lse": P.LogSumExp(2.0), "soft": P.SoftMax(2.0)}[mode]
+    padding = P.PaddingPolicy.last_value() if pad == "last" else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(mode=m, padding=padding, masked_fill=True, sentinel=sent)
+    interval = None if iv is None else P.StepInterval(*iv)
+    f = P.Until(P.Pred("x", ">", 0.25), P.Pred("y", "<", 0.5), interval)
+    cot = rng.normal(0, 1, (2, L))
+    tr, g, _ = run_device(f, {"x": x, "y": y}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x, "y": y}, cfg, cot)
+    if mode == "hard":
+        assert_hard_equal(tr, np.asarray(ref_tr, dtype=np.float32))
+        tol = 1e-5
+    else:
+        tol = 1e-5
+        assert rel_err(tr, ref_tr) <= tol
+    for k in ("x", "y"):
+        assert rel_err(g[k], ref_g[k]) <= tol, k

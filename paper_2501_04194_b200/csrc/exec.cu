@@ -274,6 +274,7 @@ struct Bufs {
   int* bflags;    // the same, backward (scratch)
   float* gslots;  // n_slots * B * T (backward)
   float* scratch; // 3 * B * T (backward)
+  float* uslab;   // Until backward checkpoint slab (persistent kernel)
   long long BT;
   float* slot(int s) const { return slots + (long long)s * BT; }
   float* gslot(int s) const { return gslots + (long long)s * BT; }
@@ -489,6 +490,18 @@ int stlg_plan_info(const stlg_plan* plan, int32_t* n_temporal, int32_t* n_slots,
   return STLG_OK;
 }
 
+// per-thread checkpoint slab of the persistent Until backward (largest Until entry)
+static size_t until_slab_bytes(const stlg_plan* plan, long long T) {
+  size_t m = 0;
+  for (const Entry& e : plan->entries)
+    if (e.kind == E_UNTIL) {
+      size_t s = until_bwd_scratch_bytes(plan->cfg.mode, e.untimed, plan->cfg.masked_fill, T,
+                                         e.untimed ? 0 : e.b, e.untimed ? (int)T : e.b - e.a + 1);
+      if (s > m) m = s;
+    }
+  return align256(m);
+}
+
 int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fwd_bytes,
                          size_t* bwd_bytes) {
   if (!plan) return fail(STLG_E_INVALID, "null plan");
@@ -500,7 +513,7 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
                  align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * (size_t)T) +
-                 flags_bytes(B, T) + 1024;
+                 flags_bytes(B, T) + until_slab_bytes(plan, T) + 1024;
   return STLG_OK;
 }
 
@@ -520,6 +533,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.flags = (int*)(base + sb + ab + tables_bytes(plan, T));
   bf.gslots = nullptr;
   bf.scratch = nullptr;
+  bf.uslab = nullptr;
   if (bwd_ws) {
     if (bwd_bytes < need_b) return fail(STLG_E_INVALID, "backward workspace too small");
     uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
@@ -527,6 +541,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
     bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
     bf.bflags = (int*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT) +
                        align256(sizeof(double) * (size_t)T) + 256);
+    bf.uslab = (float*)(((uintptr_t)bf.bflags + flags_bytes(B, T) + 255) & ~(uintptr_t)255);
   }
   return STLG_OK;
 }
@@ -737,6 +752,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.pad_value = (float)plan->cfg.pad_value;
       p.fill = plan->cfg.masked_fill;
       p.sent = (float)plan->cfg.sentinel;
+      p.scratch = bf.uslab;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH

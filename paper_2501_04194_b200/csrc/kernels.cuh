@@ -47,6 +47,7 @@ struct UParams {
   int canon;
   int fill;    // masked_fill compat: sentinel-filled columns, no overrun rule (masking.py:261-270)
   float sent;  // SemanticsConfig.sentinel
+  float* scratch;  // backward: per-thread checkpoint slab of the persistent kernel (or null)
   ModeP mp;
 };
 
@@ -80,6 +81,7 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st);
+size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K);
 cudaError_t launch_until_fwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_until_bwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st);

@@ -30,7 +30,9 @@
 namespace stlg {
 
 constexpr int U_THREADS = 128;
-constexpr int U_CB = 64;  // checkpoint interval of the backward's reverse pass
+constexpr int U_CB_S = 16;  // checkpoint interval, shared-memory variant (short timed windows)
+constexpr int U_CB_G = 32;  // checkpoint interval, global-slab variant (untimed / long windows)
+constexpr int U_PERSIST_PER_SM = 6;  // resident CTAs per SM of the persistent backward
 
 // ---------------------------------------------------------------------------
 // shared staging of the two child traces
@@ -56,14 +58,45 @@ __device__ __forceinline__ void stage_children(const UParams& p, long long row, 
 
 __device__ __forceinline__ float hard_min_first(float x, float y) { return (x <= y) ? x : y; }
 
+// 2^x as a double for x in fp32 range: the fraction through ex2 (fp32, ~2^-22
+// relative), the integer part as exponent bits; 0 below 2^-1022
+__device__ __forceinline__ double ex2d(float x) {
+  if (!(x > -1022.f)) return 0.0;
+  const float n = floorf(fminf(x, 1023.f));
+  const double scale = __longlong_as_double((long long)((int)n + 1023) << 52);
+  return (double)ex2f(x - n) * scale;
+}
+
 // ---------------------------------------------------------------------------
 // per-output forward (all modes, timed; untimed LSE / softmax)
 // ---------------------------------------------------------------------------
 // State of the running pm over x = -l ("max space"):
 //   hard: value;  lse: (m, s);  soft: (m, s, q)
+// fp64 running sums: the LSE / softmax states of Until accumulate up to T terms
+// (untimed), and fp32 additions of terms far below the running sum round
+// systematically (error ~ T eps); each term's own ex2 error stays independent.
+__device__ __forceinline__ void lse_add_d(float& m, double& s, float u, float tau2) {
+  const float d = u - m;
+  const double e = ex2f(-tau2 * fabsf(d));
+  const bool up = d > 0.f;
+  s = up ? fma(s, e, 1.0) : s + e;
+  m = up ? u : m;
+}
+__device__ __forceinline__ void soft_add_d(float& m, double& s, double& q, float u, float tau2) {
+  const float d = u - m;
+  const double e = ex2f(-tau2 * fabsf(d));
+  const bool up = d > 0.f;
+  const double s_up = fma(s, e, 1.0), q_up = e * fma(-(double)d, s, q);
+  const double s_dn = s + e, q_dn = fma((double)d, e, q);
+  s = up ? s_up : s_dn;
+  q = up ? q_up : q_dn;
+  m = up ? u : m;
+}
+
 template <int MODE>
 struct PmState {
-  float m, s, q;
+  float m;
+  double s, q;
   int i;  // hard: index (tile-local) of the first arg-min
   __device__ __forceinline__ void init(float l, int idx) {
     m = -l;
@@ -79,16 +112,16 @@ struct PmState {
         i = idx;
       }
     } else if (MODE == M_LSE) {
-      lse_add(m, s, x, tau2);
+      lse_add_d(m, s, x, tau2);
     } else {
-      soft_add(m, s, q, x, tau2);
+      soft_add_d(m, s, q, x, tau2);
     }
   }
   // pm value (l space)
   __device__ __forceinline__ float value(float itau2) const {
     if (MODE == M_HARD) return -m;
-    if (MODE == M_LSE) return -fmaf(lg2f(s), itau2, m);
-    return -(m + q / s);
+    if (MODE == M_LSE) return -fmaf(lg2f((float)s), itau2, m);
+    return -(m + (float)(q / s));
   }
 };
 
@@ -117,11 +150,11 @@ __device__ __forceinline__ void pm_mx(const PmState<MODE>& pm, float itau2, floa
     MX = pm.m;
     lse = pm.m;
   } else if (MODE == M_LSE) {
-    MX = fmaf(lg2f(pm.s), itau2, pm.m);
+    MX = fmaf(lg2f((float)pm.s), itau2, pm.m);
     lse = MX;
   } else {
-    MX = pm.m + pm.q / pm.s;
-    lse = fmaf(lg2f(pm.s), itau2, pm.m);
+    MX = pm.m + (float)(pm.q / pm.s);
+    lse = fmaf(lg2f((float)pm.s), itau2, pm.m);
   }
 }
 // d(filled min)/d(element) for an element x (l space) of that column
@@ -133,19 +166,36 @@ __device__ __forceinline__ float fill_weight(float x, float vfill, float lse, fl
   return w * fmaf(tau, vfill - x, 1.f);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__ UParams p) {
-  extern __shared__ __align__(16) float sm[];
-  const long long row = blockIdx.y, L = p.L;
-  const long long t0 = (long long)blockIdx.x * U_THREADS;
+// Child value access for one tile of U_THREADS outputs starting at t0: staged in
+// shared memory (tile-local index e, span covers every window of the tile), or
+// read directly through the fused expression (untimed / long windows: any T).
+// Rows past the signal end hold the pad value (masked_fill windows read them).
+template <int MODE, bool STAGED>
+struct USrc {
+  const float* Ls;
+  const float* Rs;
+  const UParams* p;
+  long long row, t0;
+  __device__ __forceinline__ float val(const DExpr& ex, long long j) const {
+    if (j < p->L) return expr_eval<MODE>(ex, row, j, p->mp);
+    return p->pad_last ? expr_eval<MODE>(ex, row, p->L - 1, p->mp) : p->pad_value;
+  }
+  __device__ __forceinline__ float l(int e) const { return STAGED ? Ls[e] : val(p->left, t0 + e); }
+  __device__ __forceinline__ float r(int e) const { return STAGED ? Rs[e] : val(p->right, t0 + e); }
+};
+
+template <int MODE, bool STAGED>
+__device__ __forceinline__ void until_fwd_tile(const UParams& p, long long row, long long t0, float* sm) {
+  const long long L = p.L;
   const long long nvalid = (p.untimed || p.fill) ? L : L - p.b;
   const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
   const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
   const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
-  float* Ls = sm;
-  float* Rs = sm + nst;
-  if (t0 < nvalid) stage_children<MODE>(p, row, t0, nst, Ls, Rs);
-  __syncthreads();
+  USrc<MODE, STAGED> src{sm, sm + nst, &p, row, t0};
+  if (STAGED) {
+    if (t0 < nvalid) stage_children<MODE>(p, row, t0, nst, sm, sm + nst);
+    __syncthreads();
+  }
   const long long t = t0 + threadIdx.x;
   if (t >= L) return;
   float v;
@@ -158,15 +208,16 @@ __global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__
     const int K = p.untimed ? (int)(L - t) : p.K;
     const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2;
     PmState<MODE> pm;
-    pm.init(Ls[i0], i0);
-    for (int i = 1; i <= p.a; ++i) pm.push(Ls[i0 + i], i0 + i, tau2);
+    pm.init(src.l(i0), i0);
+    for (int i = 1; i <= p.a; ++i) pm.push(src.l(i0 + i), i0 + i, tau2);
     // outer max over k, in max space of the terms
-    float M = 0.f, S = 0.f, Q = 0.f;
+    float M = 0.f;
+    double S = 0.0, Q = 0.0;
     for (int k = 0; k < K; ++k) {
       int e = i0 + p.a + k;
-      if (k > 0) pm.push(Ls[e], e, tau2);
+      if (k > 0) pm.push(src.l(e), e, tau2);
       float w1, w2;
-      float pmv, rv = Rs[e];
+      float pmv, rv = src.r(e);
       if (p.fill) {
         float MX, lse;
         bool kept;
@@ -183,30 +234,41 @@ __global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__
       } else if (MODE == M_LSE) {
         if (k == 0) {
           M = term;
-          S = 1.f;
+          S = 1.0;
         } else {
-          lse_add(M, S, term, tau2);
+          lse_add_d(M, S, term, tau2);
         }
       } else {
         if (k == 0) {
           M = term;
-          S = 1.f;
-          Q = 0.f;
+          S = 1.0;
+          Q = 0.0;
         } else {
-          soft_add(M, S, Q, term, tau2);
+          soft_add_d(M, S, Q, term, tau2);
         }
       }
     }
     if (MODE == M_HARD) v = M;
-    else if (MODE == M_LSE) v = fmaf(lg2f(S), itau2, M);
-    else v = M + Q / S;
+    else if (MODE == M_LSE) v = fmaf(lg2f((float)S), itau2, M);
+    else v = M + (float)(Q / S);
     if (p.fill && p.untimed && t > 0) {  // slices past the end: -sentinel terms (masking.py:271-273)
-      float lse = (MODE == M_SOFT) ? fmaf(lg2f(S), itau2, M) : v;
+      float lse = (MODE == M_SOFT) ? fmaf(lg2f((float)S), itau2, M) : v;
       fill_merge<MODE>(v, lse, (float)t, p.sent, false, tau2, itau2);
     }
   }
   if (p.canon) v = __fadd_rn(v, 0.f);
   p.out[row * L + t] = v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(U_THREADS) k_until_fwd(const __grid_constant__ UParams p) {
+  extern __shared__ __align__(16) float sm[];
+  until_fwd_tile<MODE, true>(p, blockIdx.y, (long long)blockIdx.x * U_THREADS, sm);
+}
+// direct reads: any T (untimed windows longer than shared memory)
+template <int MODE>
+__global__ void __launch_bounds__(U_THREADS) k_until_fwd_g(const __grid_constant__ UParams p) {
+  until_fwd_tile<MODE, false>(p, blockIdx.y, (long long)blockIdx.x * U_THREADS, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -261,21 +323,30 @@ struct Systolic {
 //   SA_k      = sum_{k' >= k} exp(tau (2 term_k' - out - pm_k))   (suffix, stable)
 // Softmax: out = softmax_k(term_k) (weights W_k (1 + tau (term_k - out))),
 //   term_k = 2-element softmin(pm_k, r), pm_k = softmin(l[t..t+a+k]).
-template <int MODE>
-__global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__ UParams p) {
-  extern __shared__ __align__(16) float sm[];
-  const long long row = blockIdx.y, L = p.L;
-  const long long t0 = (long long)blockIdx.x * U_THREADS;
+// Checkpoints CK[nck][3] and the block buffer BUF[CB][2] of every thread: in shared
+// memory (stride U_THREADS, slot tid) or in a global slab owned by a persistent
+// grid (stride = resident threads, slot = global thread index).
+struct UScr {
+  float* ck;
+  float* buf;
+  long long stride;  // checkpoints
+  long long slot;
+  int bstride;       // block buffer (shared memory in both variants)
+  int bslot;
+  __device__ __forceinline__ float& CK(int i, int c) const { return ck[((long long)i * 3 + c) * stride + slot]; }
+  __device__ __forceinline__ float& BUF(int i, int c) const { return buf[(i * 2 + c) * bstride + bslot]; }
+};
+
+template <int MODE, bool STAGED, int CB>
+__device__ __forceinline__ void until_bwd_tile(const UParams& p, long long row, long long t0, float* sm,
+                                               const UScr& scr) {
+  const long long L = p.L;
   const long long nvalid = (p.untimed || p.fill) ? L : L - p.b;
   const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
   const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
   const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
   const int Kmax = p.untimed ? (int)(L - t0) : p.K;
-  const int nck = (Kmax + U_CB - 1) / U_CB;
-  float* Ls = sm;
-  float* Rs = sm + nst;
-  float* CK = Rs + nst;                         // checkpoints [nck][3][U_THREADS]
-  float* BUF = CK + (size_t)nck * 3 * U_THREADS;  // block buffer [U_CB][2][U_THREADS]
+  USrc<MODE, STAGED> src{sm, sm + nst, &p, row, t0};
   const int tid = threadIdx.x;
   const long long t = t0 + tid;
   const bool active = t < nvalid;
@@ -294,8 +365,11 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
     }
   }
   if (t0 >= nvalid) return;  // whole tile overruns (uniform)
-  stage_children<MODE>(p, row, t0, nst, Ls, Rs);
-  __syncthreads();
+  if (STAGED) {
+    stage_children<MODE>(p, row, t0, nst, sm, sm + nst);
+    __syncthreads();
+  }
+  (void)Kmax;
   const float tau = p.mp.tau, tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2;
   const int K = active ? (p.untimed ? (int)(L - t) : p.K) : 0;
   const float g = active ? cot[t] : 0.f;
@@ -308,14 +382,14 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
   if (MODE == M_HARD) {
     if (!active || g == 0.f) return;
     PmState<M_HARD> pm;
-    pm.init(Ls[tid], tid);
-    for (int i = 1; i <= p.a; ++i) pm.push(Ls[tid + i], tid + i, tau2);
+    pm.init(src.l(tid), tid);
+    for (int i = 1; i <= p.a; ++i) pm.push(src.l(tid + i), tid + i, tau2);
     float best = 0.f;
     int bsrc = 0;  // tile-local index; bit 30 set: right child; -1: a sentinel won
     for (int k = 0; k < K; ++k) {
       int e = tid + p.a + k;
-      if (k > 0) pm.push(Ls[e], e, tau2);
-      float pmv = -pm.m, r = Rs[e];
+      if (k > 0) pm.push(src.l(e), e, tau2);
+      float pmv = -pm.m, r = src.r(e);
       bool kl = true, kr = true;
       if (p.fill) {
         float lse = pm.m;
@@ -343,23 +417,23 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
 
   // ---- pass 1: forward over k, checkpoints of the pm state; outer LSE ------------
   PmState<MODE> pm;
-  pm.init(Ls[tid], tid);
-  for (int i = 1; i <= p.a; ++i) pm.push(Ls[tid + i], tid + i, tau2);
+  pm.init(src.l(tid), tid);
+  for (int i = 1; i <= p.a; ++i) pm.push(src.l(tid + i), tid + i, tau2);
   float Lout = 0.f;  // LSE over the terms (softmax needs it; LSE: equals out)
   {
-    float M = 0.f, S = 0.f;
+    float M = 0.f;
+    double S = 0.0;
     for (int k = 0; k < K; ++k) {
       int e = tid + p.a + k;
-      if (k > 0) pm.push(Ls[e], e, tau2);
-      if (k % U_CB == 0) {
-        float* c = CK + (size_t)(k / U_CB) * 3 * U_THREADS;
-        c[tid] = pm.m;
-        c[U_THREADS + tid] = pm.s;
-        c[2 * U_THREADS + tid] = pm.q;
+      if (k > 0) pm.push(src.l(e), e, tau2);
+      if (k % CB == 0) {
+        scr.CK(k / CB, 0) = pm.m;
+        scr.CK(k / CB, 1) = (float)pm.s;
+        scr.CK(k / CB, 2) = (float)pm.q;
       }
       if (MODE == M_SOFT) {
         float w1, w2;
-        float pmv = pm.value(itau2), rv = Rs[e];
+        float pmv = pm.value(itau2), rv = src.r(e);
         if (p.fill) {
           float MX, lse;
           bool kept;
@@ -371,14 +445,18 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
         float term = term_of<MODE>(pmv, rv, p.mp, w1, w2);
         if (k == 0) {
           M = term;
-          S = 1.f;
+          S = 1.0;
         } else {
-          lse_add(M, S, term, tau2);
+          lse_add_d(M, S, term, tau2);
         }
       }
     }
-    if (MODE == M_SOFT && p.fill && p.untimed && t > 0 && K > 0) lse_merge(M, S, -p.sent, (float)t, tau2);
-    Lout = (MODE == M_SOFT) ? fmaf(lg2f(S), itau2, M) : out_t;
+    if (MODE == M_SOFT && p.fill && p.untimed && t > 0 && K > 0) {
+      float Sf = (float)S;
+      lse_merge(M, Sf, -p.sent, (float)t, tau2);
+      S = Sf;
+    }
+    Lout = (MODE == M_SOFT) ? fmaf(lg2f((float)S), itau2, M) : out_t;
   }
   // ---- pass 2: backwards over checkpoint blocks -------------------------------
   Systolic accL, accR;
@@ -388,36 +466,39 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
   const long long base = t0 + p.a;  // lane i, step k -> element base + k + i (within the warp's t0)
   const int lane = tid & 31;
   const long long wbase = t0 + (tid & ~31) + p.a;
-  // suffix accumulators
-  float SA = 0.f, SB = 0.f;   // LSE: SA (ref pm_k); soft: SA = sum A, SB = sum A (pm' - pm_k)
-  float prev_ref = 0.f;       // reference of the accumulators (pm_{k+1} for LSE, L_pm_{k+1} for soft)
-  float prev_pm = 0.f;
+  // suffix accumulators over k, fp64 in a fixed reference frame R: each term gets
+  // its own 2^x (no chained per-step rescaling, whose ex2 errors would compound
+  // over long windows); R is re-based only when a term would exceed 2^500.
+  //   LSE:  A = sum_{k'>=k} c_k' 2^{tau2 (pm_k' - R)}          (R <= pm_k', l space)
+  //         dl_e = A 2^{tau2 (R - l_e)}
+  //   soft: A = sum c_k' 2^{tau2 (R - Lpm_k')},  Bc = sum c_k' 2^{..} (pm_k' - C)
+  //         dl_e = 2^{tau2 (-l_e - R)} [(1 + tau (pm_k - l_e)) A + tau (Bc - (pm_k - C) A)]
+  double A = 0.0, Bc = 0.0;
+  float R = 0.f, Cc = 0.f;
   bool have = false;
-  float pm0 = 0.f, Lpm0 = 0.f;
-  for (int cb = (Kw + U_CB - 1) / U_CB - 1; cb >= 0; --cb) {
-    const int k_lo = cb * U_CB;
-    const int k_hi = min(k_lo + U_CB, Kw);
+  float pm0 = 0.f;
+  for (int cb = (Kw + CB - 1) / CB - 1; cb >= 0; --cb) {
+    const int k_lo = cb * CB;
+    const int k_hi = min(k_lo + CB, Kw);
     // recompute the block forward from its checkpoint into BUF
     if (k_lo < K) {
-      float* c = CK + (size_t)cb * 3 * U_THREADS;
       PmState<MODE> st;
-      st.m = c[tid];
-      st.s = c[U_THREADS + tid];
-      st.q = c[2 * U_THREADS + tid];
+      st.m = scr.CK(cb, 0);
+      st.s = scr.CK(cb, 1);
+      st.q = scr.CK(cb, 2);
       st.i = 0;
       for (int k = k_lo; k < min(k_hi, K); ++k) {
         int e = tid + p.a + k;
-        if (k > k_lo) st.push(Ls[e], e, tau2);
-        float* bb = BUF + (size_t)(k - k_lo) * 2 * U_THREADS;
+        if (k > k_lo) st.push(src.l(e), e, tau2);
         if (p.fill) {  // the filled column's min and LSE
           float MX, lse;
           bool kept;
           pm_mx<MODE>(st, itau2, MX, lse);
-          bb[tid] = fill_min<MODE>(MX, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kept);
-          bb[U_THREADS + tid] = lse;
+          scr.BUF(k - k_lo, 0) = fill_min<MODE>(MX, lse, (float)(rows - (p.a + k + 1)), p.sent, t > 0, tau2, itau2, kept);
+          scr.BUF(k - k_lo, 1) = lse;
         } else {
-          bb[tid] = st.value(itau2);                                          // pm_k
-          bb[U_THREADS + tid] = (MODE == M_SOFT) ? fmaf(lg2f(st.s), itau2, st.m) : 0.f;  // L_pm (x space)
+          scr.BUF(k - k_lo, 0) = st.value(itau2);                                          // pm_k
+          scr.BUF(k - k_lo, 1) = (MODE == M_SOFT) ? fmaf(lg2f((float)st.s), itau2, st.m) : 0.f;  // L_pm (x space)
         }
       }
     }
@@ -425,9 +506,8 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
       float vr = 0.f, vl = 0.f;
       if (k < K) {
         int e = tid + p.a + k;
-        float* bb = BUF + (size_t)(k - k_lo) * 2 * U_THREADS;
-        float pmk = bb[tid];
-        float r = Rs[e];
+        float pmk = scr.BUF(k - k_lo, 0);
+        float r = src.r(e);
         float dr = 1.f;  // d(filled right operand) / d r
         if (p.fill) {
           float lr = -r;
@@ -442,42 +522,43 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
           // dr: g exp(tau (term - out)) * w2 ; dpm: g exp(tau (term - out)) * w1
           float wk = ex2f(tau2 * (term - out_t));
           vr = g * wk * w2 * dr;
-          float c_pm = g * wk * w1;  // = g exp(tau (2 term - out - pm))
-          // SA_k = c_pm_k / g-scale + exp(-tau (pm_k - pm_{k+1})) SA_{k+1}   (ref pm_k)
-          SA = have ? fmaf(SA, ex2f(-tau2 * (pmk - prev_ref)), c_pm) : c_pm;
-          prev_ref = pmk;
-          have = true;
+          const float c_pm = g * wk * w1;  // = g exp(tau (2 term - out - pm))
+          if (!have) {
+            R = pmk;
+            have = true;
+          } else if (tau2 * (pmk - R) > 500.f) {
+            A *= ex2d(tau2 * (R - pmk));
+            R = pmk;
+          }
+          A += (double)c_pm * ex2d(tau2 * (pmk - R));
           // element e = t + a + k receives dpm via exp(tau (pm_k - l_e)) (k >= 1;
           // k == 0 elements are the a-prefix, handled after the loop)
-          if (k > 0) vl = SA * ex2f(tau2 * (pmk - Ls[e]));
+          if (k > 0) vl = (float)(A * ex2d(tau2 * (R - src.l(e))));
           if (k == 0) pm0 = pmk;
         } else {
           float Wk = ex2f(tau2 * (term - Lout)) * fmaf(tau, term - out_t, 1.f);
           vr = g * Wk * w2 * dr;
-          float c_pm = g * Wk * w1;
-          float Lpm = bb[U_THREADS + tid];
-          // dl_j = exp(tau (-l_j - Lpm_k0)) [ (1 + tau (pm_k0 - l_j)) SA + tau SB ]
-          //   SA = sum_{k'>=k0} c_pm_k' exp(-tau (Lpm_k' - Lpm_k0)),
-          //   SB = sum_{k'>=k0} c_pm_k' exp(...) (pm_k' - pm_k0)
-          if (have) {
-            float f = ex2f(-tau2 * (prev_ref - Lpm));
-            SB = f * fmaf(prev_pm - pmk, SA, SB);
-            SA = fmaf(SA, f, c_pm);
-          } else {
-            SA = c_pm;
-            SB = 0.f;
+          const float c_pm = g * Wk * w1;
+          const float Lpm = scr.BUF(k - k_lo, 1);
+          if (!have) {
+            R = Lpm;
+            Cc = pmk;
+            have = true;
+          } else if (tau2 * (R - Lpm) > 500.f) {
+            const double f = ex2d(tau2 * (Lpm - R));
+            A *= f;
+            Bc *= f;
+            R = Lpm;
           }
-          prev_ref = Lpm;
-          prev_pm = pmk;
-          have = true;
+          const double w = (double)c_pm * ex2d(tau2 * (R - Lpm));
+          A += w;
+          Bc += w * (double)(pmk - Cc);
           if (k > 0) {
-            float l = Ls[e];
-            vl = ex2f(tau2 * (-l - Lpm)) * fmaf(1.f + tau * (pmk - l), SA, tau * SB);
+            const float l = src.l(e);
+            const double sb = Bc - (double)(pmk - Cc) * A;
+            vl = (float)(ex2d(tau2 * (-l - R)) * ((1.0 + (double)tau * (pmk - l)) * A + (double)tau * sb));
           }
-          if (k == 0) {
-            pm0 = pmk;
-            Lpm0 = Lpm;
-          }
+          if (k == 0) pm0 = pmk;
         }
       }
       accR.step(vr, wbase, k, gr, L);
@@ -490,15 +571,50 @@ __global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__
   for (int i = 0; i <= p.a; ++i) {
     float vl = 0.f;
     if (K > 0) {
-      float l = Ls[tid + i];
-      if (MODE == M_LSE) vl = SA * ex2f(tau2 * (pm0 - l));
-      else vl = ex2f(tau2 * (-l - Lpm0)) * fmaf(1.f + tau * (pm0 - l), SA, tau * SB);
+      float l = src.l(tid + i);
+      if (MODE == M_LSE) {
+        vl = (float)(A * ex2d(tau2 * (R - l)));
+      } else {
+        const double sb = Bc - (double)(pm0 - Cc) * A;
+        vl = (float)(ex2d(tau2 * (-l - R)) * ((1.0 + (double)tau * (pm0 - l)) * A + (double)tau * sb));
+      }
     }
     accL.step(vl, wbase - p.a, i, gl, L);
   }
   accL.flush(gl, L);
   (void)lane;
   (void)base;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(U_THREADS) k_until_bwd(const __grid_constant__ UParams p) {
+  extern __shared__ __align__(16) float sm[];
+  const long long L = p.L;
+  const long long t0 = (long long)blockIdx.x * U_THREADS;
+  const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
+  const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
+  const int Kmax = p.untimed ? (int)(L - t0) : p.K;
+  const int nck = (Kmax + U_CB_S - 1) / U_CB_S;
+  float* ck = sm + 2 * nst;
+  UScr scr{ck, ck + (size_t)nck * 3 * U_THREADS, U_THREADS, threadIdx.x, U_THREADS, (int)threadIdx.x};
+  until_bwd_tile<MODE, true, U_CB_S>(p, blockIdx.y, t0, sm, scr);
+}
+
+// persistent grid, direct child reads, per-thread checkpoints in the global slab
+// `p.scratch` (U_CB_G-step blocks): any T, occupancy independent of the window
+template <int MODE>
+__global__ void __launch_bounds__(U_THREADS) k_until_bwd_g(const __grid_constant__ UParams p, int ntx,
+                                                            long long ntiles) {
+  extern __shared__ __align__(16) float sm[];  // block buffer [U_CB_G][2][U_THREADS]
+  const long long stride = (long long)gridDim.x * U_THREADS;
+  UScr scr{p.scratch, sm, stride, (long long)blockIdx.x * U_THREADS + threadIdx.x, U_THREADS,
+           (int)threadIdx.x};
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row = tile / ntx;
+    const long long t0 = (tile - row * ntx) * U_THREADS;
+    until_bwd_tile<MODE, false, U_CB_G>(p, row, t0, nullptr, scr);
+    __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -673,12 +789,41 @@ static size_t fwd_smem(const UParams& p) {
   if (span > p.L && !p.fill) span = p.L;
   return (size_t)2 * span * 4;
 }
+// shared-memory backward: staging + checkpoints every U_CB_S steps + block buffer
 static size_t bwd_smem(const UParams& p) {
   long long span = p.untimed ? p.L : (long long)U_THREADS + p.b;
   if (span > p.L && !p.fill) span = p.L;
   long long kmax = p.untimed ? p.L : p.K;
-  long long nck = (kmax + U_CB - 1) / U_CB;
-  return (size_t)2 * span * 4 + (size_t)nck * 3 * U_THREADS * 4 + (size_t)U_CB * 2 * U_THREADS * 4;
+  long long nck = (kmax + U_CB_S - 1) / U_CB_S;
+  return (size_t)2 * span * 4 + (size_t)nck * 3 * U_THREADS * 4 + (size_t)U_CB_S * 2 * U_THREADS * 4;
+}
+// the shared variant keeps >= 3 CTAs per SM; beyond that, the persistent global-slab one
+static bool bwd_uses_smem(const UParams& p) { return !p.untimed && bwd_smem(p) <= 72 * 1024; }
+
+static int until_sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K) {
+  UParams p;
+  memset(&p, 0, sizeof(p));
+  p.L = L;
+  p.b = b;
+  p.K = K;
+  p.untimed = untimed;
+  p.fill = fill;
+  if (mode == M_HARD) return 0;  // one source per output: no checkpoints
+  if (bwd_uses_smem(p)) return 0;
+  const long long stride = (long long)until_sm_count() * U_PERSIST_PER_SM * U_THREADS;
+  const long long nck = (untimed ? L : K) / U_CB_G + 1;
+  return (size_t)(nck * 3) * stride * 4;
 }
 
 template <int MODE>
@@ -688,12 +833,15 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
     count_launch();
     return cudaGetLastError();
   }
-  size_t smem = fwd_smem(p);
-  if (smem > kUSmemMax) return cudaErrorNotSupported;
-  cudaError_t e = set_smem_u(k_until_fwd<MODE>, smem);
-  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((p.L + U_THREADS - 1) / U_THREADS), (unsigned)p.B);
-  k_until_fwd<MODE><<<grid, U_THREADS, smem, st>>>(p);
+  size_t smem = fwd_smem(p);
+  if (smem <= 64 * 1024) {
+    cudaError_t e = set_smem_u(k_until_fwd<MODE>, smem);
+    if (e != cudaSuccess) return e;
+    k_until_fwd<MODE><<<grid, U_THREADS, smem, st>>>(p);
+  } else {  // long untimed windows: direct reads
+    k_until_fwd_g<MODE><<<grid, U_THREADS, 0, st>>>(p);
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -705,14 +853,33 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
     count_launch();
     return cudaGetLastError();
   }
-  size_t smem = bwd_smem(p);
-  if (smem > kUSmemMax) return cudaErrorNotSupported;
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.gl, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.gr, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
-  if ((e = set_smem_u(k_until_bwd<MODE>, smem)) != cudaSuccess) return e;
-  dim3 grid((unsigned)((p.L + U_THREADS - 1) / U_THREADS), (unsigned)p.B);
-  k_until_bwd<MODE><<<grid, U_THREADS, smem, st>>>(p);
+  const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
+  if (bwd_uses_smem(p) || MODE == M_HARD) {
+    size_t smem = (MODE == M_HARD) ? fwd_smem(p) : bwd_smem(p);
+    if (smem <= kUSmemMax) {
+      if ((e = set_smem_u(k_until_bwd<MODE>, smem)) != cudaSuccess) return e;
+      dim3 grid((unsigned)ntx, (unsigned)p.B);
+      k_until_bwd<MODE><<<grid, U_THREADS, smem, st>>>(p);
+    } else if (MODE == M_HARD) {
+      // hard (masked_fill, long untimed): one source per output, no checkpoints
+      const long long ntiles = (long long)ntx * p.B;
+      long long grid = (long long)until_sm_count() * 8;
+      if (grid > ntiles) grid = ntiles;
+      k_until_bwd_g<MODE><<<(unsigned)grid, U_THREADS, 0, st>>>(p, ntx, ntiles);
+    } else {
+      return cudaErrorNotSupported;
+    }
+  } else {
+    if (p.scratch == nullptr) return cudaErrorNotSupported;
+    const long long ntiles = (long long)ntx * p.B;
+    long long grid = (long long)until_sm_count() * U_PERSIST_PER_SM;
+    if (grid > ntiles) grid = ntiles;
+    const size_t bsm = (size_t)U_CB_G * 2 * U_THREADS * 4;
+    k_until_bwd_g<MODE><<<(unsigned)grid, U_THREADS, bsm, st>>>(p, ntx, ntiles);
+  }
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // child VJPs from the accumulated cotangents (left first: first-writer order)

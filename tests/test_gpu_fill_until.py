@@ -64,3 +64,22 @@ def test_masked_fill_until_vs_oracle(cuda, mode, iv, pad, sent, L):
         assert rel_err(tr, ref_tr) <= tol
     for k in ("x", "y"):
         assert rel_err(g[k], ref_g[k]) <= tol, k
+
+
+def test_untimed_lse_until_long_signal(cuda):
+    """Untimed LSE Until at T=6000: the backward's checkpoints live in the persistent
+    kernel's global slab (the shared-memory design stopped near T=5000)."""
+    P = cuda
+    orc = _oracle()
+    T = 6000
+    rng = np.random.default_rng(6000)
+    x = np.asarray(rng.normal(0, 1, (1, T)), dtype=np.float32).astype(np.float64)
+    y = np.asarray(rng.normal(0, 1, (1, T)), dtype=np.float32).astype(np.float64)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0))
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(10.0))
+    cot = rng.normal(0, 1, (1, T))
+    tr, g, _ = run_device(f, {"x": x, "y": y}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x, "y": y}, cfg, cot)
+    assert rel_err(tr, ref_tr) <= 1e-5
+    for k in ("x", "y"):
+        assert rel_err(g[k], ref_g[k]) <= 1e-5, k

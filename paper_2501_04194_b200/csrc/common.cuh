@@ -424,7 +424,11 @@ __device__ __forceinline__ bool exact_owns(const int* tile_slow, int fast_J, int
 // specialisations with the row's pointers hoisted into registers; EK_GEN
 // interprets any fused expression.  Element indices are row-relative ints.
 // ---------------------------------------------------------------------------
-enum ExprKind { EK_GEN = 0, EK_AFF = 1, EK_NORM = 2, EK_SRC = 3, EK_PAIR = 4 };
+// EK_AFF: affine leaf, any element stride; EK_AFF1 / EK_NORM / EK_SRC: unit element
+// stride of the source(s) and gradient destination(s) (contiguous [B, T] planes:
+// addresses are row base + j, so every strided sweep uses immediate offsets);
+// EK_PAIR: interleaved (x, y) pair.  expr_kind() checks the strides.
+enum ExprKind { EK_GEN = 0, EK_AFF = 1, EK_NORM = 2, EK_SRC = 3, EK_PAIR = 4, EK_AFF1 = 5 };
 
 __device__ __forceinline__ float sqrt_fast(float x) {
   float y;
@@ -478,6 +482,12 @@ struct LeafRegs {
       }
     }
   }
+  __device__ __forceinline__ static void put1(float* p, int j, float g, int st) {
+    if (p) {
+      if (st) p[j] = g;
+      else p[j] += g;
+    }
+  }
   __device__ __forceinline__ static void put(float* p, int es, int j, float g, int st) {
     if (p) {
       float* q = p + (long long)j * es;
@@ -502,14 +512,25 @@ struct Ev<MODE, EK_AFF> : LeafRegs {
 };
 
 template <int MODE>
+struct Ev<MODE, EK_AFF1> : LeafRegs {
+  struct Raw {
+    float x;
+  };
+  __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
+  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
+  __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
+  __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * (s_out * s_in), st1); }
+};
+
+template <int MODE>
 struct Ev<MODE, EK_SRC> : LeafRegs {
   struct Raw {
     float x;
   };
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
-  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + (long long)j * es1)}; }
+  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * r.x; }
-  __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * s_out, st1); }
+  __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * s_out, st1); }
 };
 
 template <int MODE>
@@ -521,9 +542,7 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {
     pair = (p2 == p1 + 1) && es1 == 2 && es2 == 2 && ((reinterpret_cast<uintptr_t>(p1) & 7) == 0);
   }
-  __device__ __forceinline__ Raw load(int j) const {
-    return Raw{ld_na(p1 + (long long)j * es1), ld_na(p2 + (long long)j * es2)};
-  }
+  __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j), ld_na(p2 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const {
     float dx = r.x - cx, dy = r.y - cy;
     return s_out * __fadd_rn(s_in * sqrt_fast(fmaf(dx, dx, dy * dy)), c);
@@ -532,8 +551,8 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
     float dx = r.x - cx, dy = r.y - cy;
     float d2 = fmaf(dx, dx, dy * dy);
     float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
-    put(g1, ges1, j, dx * sc, st1);
-    put(g2, ges2, j, dy * sc, st2);
+    put1(g1, j, dx * sc, st1);
+    put1(g2, j, dy * sc, st2);
   }
 };
 
@@ -587,15 +606,18 @@ struct Ev<MODE, EK_GEN> {
 __host__ __device__ inline int expr_kind(const DExpr& e) {
   if (e.n_step != 1) return EK_GEN;
   int k = e.leaf[0].kind;
-  if (k == LEAF_AFFINE) return EK_AFF;
+  // unit element stride of source i and of its gradient destination (if any)
+  auto unit = [&](int i) { return e.src[i].es == 1 && (e.dst[i].p == nullptr || e.dst[i].es == 1); };
+  if (k == LEAF_AFFINE) return unit(e.leaf[0].src) ? EK_AFF1 : EK_AFF;
   if (k == LEAF_NORM) {
     const DSrc& a = e.src[e.leaf[0].src];
     const DSrc& b = e.src[e.leaf[0].src2];
     bool pair = b.p == a.p + 1 && a.es == 2 && b.es == 2 && a.rs == b.rs && (a.rs % 2 == 0) &&
                 ((reinterpret_cast<uintptr_t>(a.p) & 7) == 0);
-    return pair ? EK_PAIR : EK_NORM;
+    if (pair) return EK_PAIR;
+    return (unit(e.leaf[0].src) && unit(e.leaf[0].src2)) ? EK_NORM : EK_GEN;
   }
-  if (k == LEAF_SRC) return EK_SRC;
+  if (k == LEAF_SRC) return unit(e.leaf[0].src) ? EK_SRC : EK_GEN;
   return EK_GEN;
 }
 

@@ -747,7 +747,7 @@ static bool use_direct(int K, int mode) {
 }
 
 #define DISPATCH_EK(EKV, ...)          \
-  if ((EKV) == EK_AFF) {               \
+  if ((EKV) == EK_AFF || (EKV) == EK_AFF1) { \
     constexpr int EK = EK_AFF;         \
     __VA_ARGS__;                       \
   } else if ((EKV) == EK_NORM) {       \

@@ -365,6 +365,7 @@ cudaError_t launch_lse_fast_fwd(int ek, FGParams& p, int* slow, cudaStream_t st)
   const int J = FF_N - p.K + 1;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
   switch (ek) {
+    case EK_AFF1:
     case EK_AFF: k_lse_fast_fwd<EK_AFF><<<grid, FF_T, 0, st>>>(p, slow); break;
     case EK_NORM: k_lse_fast_fwd<EK_NORM><<<grid, FF_T, 0, st>>>(p, slow); break;
     case EK_SRC: k_lse_fast_fwd<EK_SRC><<<grid, FF_T, 0, st>>>(p, slow); break;
@@ -379,6 +380,7 @@ cudaError_t launch_lse_fast_bwd(int ek, FGParams& p, int* slow, cudaStream_t st)
   const int J = FF_N - p.K + 1;
   dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
   switch (ek) {
+    case EK_AFF1:
     case EK_AFF: k_lse_fast_bwd<EK_AFF><<<grid, FF_T, 0, st>>>(p, slow); break;
     case EK_NORM: k_lse_fast_bwd<EK_NORM><<<grid, FF_T, 0, st>>>(p, slow); break;
     case EK_SRC: k_lse_fast_bwd<EK_SRC><<<grid, FF_T, 0, st>>>(p, slow); break;

@@ -714,7 +714,7 @@ cudaError_t launch_fgt_fwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st) 
   const size_t smem = (size_t)words * nb * p.Kp * 4;
 #define FWD_PIPE(M)                                                              \
   switch (ek) {                                                                  \
-    case EK_AFF: return launch_persistent(k_fgt_fwd_pipe<M, EK_AFF>, p, smem, st);   \
+    case EK_AFF1: case EK_AFF: return launch_persistent(k_fgt_fwd_pipe<M, EK_AFF>, p, smem, st);   \
     case EK_NORM: return launch_persistent(k_fgt_fwd_pipe<M, EK_NORM>, p, smem, st); \
     case EK_SRC: return launch_persistent(k_fgt_fwd_pipe<M, EK_SRC>, p, smem, st);   \
     case EK_PAIR: return launch_persistent(k_fgt_fwd_pipe<M, EK_PAIR>, p, smem, st); \
@@ -736,7 +736,7 @@ cudaError_t launch_fgt_bwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st) 
   const size_t smem = (size_t)words * nb * p.Kp * 4;
 #define BWD_PIPE(M)                                                              \
   switch (ek) {                                                                  \
-    case EK_AFF: return launch_persistent(k_fgt_bwd_pipe<M, EK_AFF>, p, smem, st);   \
+    case EK_AFF1: case EK_AFF: return launch_persistent(k_fgt_bwd_pipe<M, EK_AFF>, p, smem, st);   \
     case EK_NORM: return launch_persistent(k_fgt_bwd_pipe<M, EK_NORM>, p, smem, st); \
     case EK_SRC: return launch_persistent(k_fgt_bwd_pipe<M, EK_SRC>, p, smem, st);   \
     case EK_PAIR: return launch_persistent(k_fgt_bwd_pipe<M, EK_PAIR>, p, smem, st); \

@@ -624,7 +624,10 @@ inline cudaError_t reg_launch(KernT k, dim3 grid, int threads, size_t smem, cons
   }
 
 #define REG_DISPATCH_EK(EKV, ...)      \
-  if ((EKV) == EK_AFF) {               \
+  if ((EKV) == EK_AFF1) {              \
+    constexpr int EK = EK_AFF1;        \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_AFF) {        \
     constexpr int EK = EK_AFF;         \
     __VA_ARGS__;                       \
   } else if ((EKV) == EK_NORM) {       \

@@ -153,64 +153,23 @@ __device__ __forceinline__ void fs_windows(const float (&S)[RG_EPT], const FsCas
   }
 }
 
-// ---------------------------------------------------------------------------
-// forward (hard: RK_HARD, LSE: RK_LSE)
-// ---------------------------------------------------------------------------
-template <int RK, int MODE, int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __grid_constant__ FGParams p) {
+// Forward after staging: x = the tile's chunk values (max space).  Scans, middle
+// folds, window finish into the consumed prefix slots, coalesced stores.
+template <int RK, int NW>
+__device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, int t0, int J, float padv,
+                                             RSt (&x)[RG_EPT], float* P0, float* P1, float* T0, float* T1) {
   using C = RC<NW>;
-  constexpr int T = C::T, N = C::N, SS = C::SS;
-  extern __shared__ float rsm[];
-  __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T];
-  float* P0 = rsm;
-  float* P1 = rsm + C::NP;
+  constexpr int T = C::T, SS = C::SS;
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
   const int L = (int)p.L;
-  const long long row = blockIdx.y;
-  const int J = N - K + 1;
-  const int t0 = blockIdx.x * J;
   const int nvalid = L - p.b;
-  const int s0 = t0 + p.a;
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
-  const float czero = p.canon ? 0.f : -0.f;  // x + (-0) == x for every x: canon is one add
-  Ev<MODE, EK> ev(p.child, row, p.mp);
-  const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+  const float czero = p.canon ? 0.f : -0.f;
   float* outr = p.out + row * L;
   float* auxr = (RK == RK_LSE && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
-  if (t0 >= nvalid) {  // every output of the tile overruns
-    for (int i = tid; i < tend; i += T) {
-      outr[t0 + i] = __fadd_rn(padv, czero);
-      if (auxr) auxr[t0 + i] = 0.f;
-    }
-    return;
-  }
-  {
-    float* dst = P0 + tid + (tid >> 4);
-    const int jb = s0 + tid;
-    const bool interior = s0 + N <= L;
-#pragma unroll
-    for (int h = 0; h < RG_EPT; h += CAV_LB) {
-      typename Ev<MODE, EK>::Raw r[CAV_LB];
-      // past the row end: replicate the last sample (feeds overrun windows only)
-#pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int j = jb + (h + k) * T;
-        r[k] = ev.load(interior ? j : (j < L ? j : L - 1));
-      }
-#pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int j = jb + (h + k) * T;
-        dst[(h + k) * SS] = sg * ev.value(interior ? j : (j < L ? j : L - 1), r[k]);
-      }
-    }
-  }
-  __syncthreads();
-  RSt x[RG_EPT];
-#pragma unroll
-  for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
   const int i0 = tid * RG_EPT;
   const bool full = i0 + RG_EPT <= J && t0 + i0 + RG_EPT <= nvalid;
   bool fs_done = false;
@@ -270,6 +229,67 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
         if (tid + k * T < tend) ap[k * T] = src1[k * SS];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// forward (hard: RK_HARD, LSE: RK_LSE)
+// ---------------------------------------------------------------------------
+template <int RK, int MODE, int EK, int NW>
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS;
+  extern __shared__ float rsm[];
+  __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T];
+  float* P0 = rsm;
+  float* P1 = rsm + C::NP;
+  const int K = p.K;
+  const int d = (K - 1) >> 4, c = (K - 1) & 15;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = N - K + 1;
+  const int t0 = blockIdx.x * J;
+  const int nvalid = L - p.b;
+  const int s0 = t0 + p.a;
+  const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
+  const float czero = p.canon ? 0.f : -0.f;  // x + (-0) == x for every x: canon is one add
+  Ev<MODE, EK> ev(p.child, row, p.mp);
+  const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
+  float* outr = p.out + row * L;
+  float* auxr = (RK == RK_LSE && p.aux != nullptr) ? p.aux + row * L : nullptr;
+  const int tend = (t0 + J < L ? t0 + J : L) - t0;
+  const int tid = threadIdx.x;
+  if (t0 >= nvalid) {  // every output of the tile overruns
+    for (int i = tid; i < tend; i += T) {
+      outr[t0 + i] = __fadd_rn(padv, czero);
+      if (auxr) auxr[t0 + i] = 0.f;
+    }
+    return;
+  }
+  {
+    float* dst = P0 + tid + (tid >> 4);
+    const int jb = s0 + tid;
+    const bool interior = s0 + N <= L;
+#pragma unroll
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      typename Ev<MODE, EK>::Raw r[CAV_LB];
+      // past the row end: replicate the last sample (feeds overrun windows only)
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int j = jb + (h + k) * T;
+        r[k] = ev.load(interior ? j : (j < L ? j : L - 1));
+      }
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int j = jb + (h + k) * T;
+        dst[(h + k) * SS] = sg * ev.value(interior ? j : (j < L ? j : L - 1), r[k]);
+      }
+    }
+  }
+  __syncthreads();
+  RSt x[RG_EPT];
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
+  cav_fwd_core<RK, NW>(p, row, t0, J, padv, x, P0, P1, T0, T1);
 }
 
 // ---------------------------------------------------------------------------

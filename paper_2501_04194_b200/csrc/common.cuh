@@ -411,12 +411,6 @@ __device__ __forceinline__ bool fill_merge(float& M, float& lse, float nu, float
   return true;
 }
 
-// With a fast-path tiling active, the exact (guarded) kernels write only the
-// elements of tiles the fast kernel left to them.
-__device__ __forceinline__ bool exact_owns(const int* tile_slow, int fast_J, int fast_tpr,
-                                           long long row, int idx) {
-  return tile_slow == nullptr || tile_slow[row * fast_tpr + idx / fast_J] != 0;
-}
 
 // ---------------------------------------------------------------------------
 // evaluators.  The single-leaf kinds (the common case: a Pred / NormPred / a

@@ -270,8 +270,6 @@ struct Bufs {
   float* slots;   // n_slots * B * T
   float* aux;     // n_aux * B * T
   float* tables;  // n_tables * T (log2 smooth weights)
-  int* flags;     // device flags (fast-path fallback), forward
-  int* bflags;    // the same, backward (scratch)
   float* gslots;  // n_slots * B * T (backward)
   float* scratch; // 3 * B * T (backward)
   float* uslab;   // Until backward checkpoint slab (persistent kernel)
@@ -286,10 +284,6 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 void fwd_layout(const stlg_plan* p, long long BT, size_t* slots_b, size_t* aux_b) {
   *slots_b = align256(sizeof(float) * (size_t)p->n_slots * BT);
   *aux_b = align256(sizeof(float) * (size_t)p->n_aux * BT);
-}
-// fast-path flags: one "any slow" int + one int per (row, fast tile) (tiles >= 3000 samples)
-size_t flags_bytes(long long B, long long T) {
-  return align256(sizeof(int) * (size_t)(1 + B * (T / 3000 + 2)));
 }
 size_t tables_bytes(const stlg_plan* p, long long T) {
   return align256(sizeof(float) * (size_t)p->n_tables * (size_t)T);
@@ -509,11 +503,11 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   long long BT = (long long)B * T;
   size_t sb, ab;
   fwd_layout(plan, BT, &sb, &ab);
-  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + flags_bytes(B, T) + 256;
+  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + 256;
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
                  align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * (size_t)T) +
-                 flags_bytes(B, T) + until_slab_bytes(plan, T) + 1024;
+                 until_slab_bytes(plan, T) + 1024;
   return STLG_OK;
 }
 
@@ -530,7 +524,6 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.slots = (float*)base;
   bf.aux = (float*)(base + sb);
   bf.tables = (float*)(base + sb + ab);
-  bf.flags = (int*)(base + sb + ab + tables_bytes(plan, T));
   bf.gslots = nullptr;
   bf.scratch = nullptr;
   bf.uslab = nullptr;
@@ -539,9 +532,8 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
     uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
     bf.gslots = (float*)bb;
     bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
-    bf.bflags = (int*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT) +
-                       align256(sizeof(double) * (size_t)T) + 256);
-    bf.uslab = (float*)(((uintptr_t)bf.bflags + flags_bytes(B, T) + 255) & ~(uintptr_t)255);
+    bf.uslab = (float*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT) +
+                        align256(sizeof(double) * (size_t)T) + 256);
   }
   return STLG_OK;
 }
@@ -662,7 +654,6 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       if ((rc = resolve(plan, e.e1, channels, nullptr, bf, T, false, p.child))) return rc;
       p.out = out;
       p.aux = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
-      p.flag = bf.flags;
       if (e.kind == E_POINTWISE) ce = launch_pointwise_fwd(mode, p, st);
       else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_fwd(mode, p, st);
       else ce = launch_fg_untimed_fwd(mode, p, st);
@@ -729,7 +720,6 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.aux_in = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
       p.cot = g;
       p.gbuf = bf.scratch;
-      p.flag = bf.bflags;
       if (e.kind == E_POINTWISE) ce = launch_pointwise_vjp(mode, p, g, st);
       else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_bwd(mode, p, st);
       else ce = launch_fg_untimed_bwd(mode, p, st);

@@ -115,7 +115,6 @@ constexpr int FG_THREADS = 256;
 
 template <int MODE, int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ FGParams p) {
-  if (p.guard != nullptr && *p.guard == 0) return;  // fast path covered every tile
   extern __shared__ __align__(16) float sm[];
   __shared__ float padv_sh;
   const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
@@ -241,7 +240,6 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_fwd(const __grid_constant__ 
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   for (int i = threadIdx.x; i < tend; i += FG_THREADS) {
     int t = t0 + i;
-    if (!exact_owns(p.tile_slow, p.fast_J, p.fast_tpr, row, t)) continue;
     int q = i + div_k(i, K, invK) * dK;
     float v;
     if (t < nvalid) {
@@ -280,7 +278,6 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 template <int MODE, int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant__ FGParams p) {
-  if (p.guard != nullptr && *p.guard == 0) return;  // fast path covered every tile
   extern __shared__ __align__(16) float sm[];
   __shared__ float red_sh[32];
   const int NB = p.NB, K = p.K, Kp = p.Kp, dK = Kp - K;
@@ -416,7 +413,6 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant
       int i = i0 + u * FG_THREADS;
       if (i >= jn) continue;
       int j = j0 + i;
-      if (!exact_owns(p.tile_slow, p.fast_J, p.fast_tpr, row, j)) continue;
       int q = i + div_k(i, K, invK) * dK;
       float A = HG[q];
       float g = 0.f;
@@ -677,26 +673,6 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
 // ===========================================================================
 static int odd_stride(int K) { return K | 1; }
 
-// STLG_FAST=0 disables the exp-factorised LSE kernels (A/B measurements).  The
-// forward one is opt-in (STLG_FAST_FWD=1): on B200 the pipelined exact forward is
-// faster (profiles/r1_c2_ncu_summary.md); the backward fast kernel is the default.
-static bool fast_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STLG_FAST");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-static bool fast_fwd_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STLG_FAST_FWD");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1 && fast_enabled();
-}
-
 // STLG_PIPE=0 selects the non-pipelined timed kernels (A/B measurements)
 bool pipe_enabled() {
   static int v = -1;
@@ -784,15 +760,6 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
   }
   const int ek = expr_kind(p.child);
   cudaError_t e;
-  if (mode == M_LSE && p.flag != nullptr && fast_lse_applicable(p) && fast_fwd_enabled()) {
-    if ((e = cudaMemsetAsync(p.flag, 0, sizeof(int), st)) != cudaSuccess) return e;
-    p.tile_slow = p.flag + 1;
-    p.fast_J = fast_lse_tile(p.K);
-    p.fast_tpr = (int)((p.L + p.fast_J - 1) / p.fast_J);
-    if ((e = launch_lse_fast_fwd(ek, p, p.flag, st)) != cudaSuccess) return e;
-    p.guard = p.flag;  // the exact kernel below runs only if some tile was out of range,
-                       // and then writes only those tiles (tile_slow)
-  }
   if (pipe_enabled()) {
     e = launch_fgt_fwd_pipe(mode, ek, p, st);
     if (e != cudaErrorNotSupported) return e;
@@ -844,14 +811,6 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
   }
   p.Kp = odd_stride(p.K);
   const int ek = expr_kind(p.child);
-  if (mode == M_LSE && p.flag != nullptr && fast_lse_applicable(p) && fast_enabled()) {
-    if ((e = cudaMemsetAsync(p.flag, 0, sizeof(int), st)) != cudaSuccess) return e;
-    p.tile_slow = p.flag + 1;
-    p.fast_J = fast_lse_tile(p.K);
-    p.fast_tpr = (int)((p.L + p.fast_J - 1) / p.fast_J);
-    if ((e = launch_lse_fast_bwd(ek, p, p.flag, st)) != cudaSuccess) return e;
-    p.guard = p.flag;
-  }
   if (mode == M_HARD) {
     // U, PV, PI over NB+1 blocks + GT over NB blocks + J accumulators
     int nb = pick_nb(p.K, 5);

@@ -37,7 +37,6 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 template <int MODE, int EK>
 __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_fwd_pipe(const __grid_constant__ FGParams p,
                                                                int tiles_per_row, long long total) {
-  if (p.guard != nullptr && *p.guard == 0) return;  // fast path covered every tile
   extern __shared__ __align__(16) float sm[];
   __shared__ float padv_sh[2];
   __shared__ float rng_sh[2][2][8];  // per buffer: {max, min} of the tile's samples, per mover warp
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_fwd_pipe(const __grid_c
     float* auxr = (MODE == M_SOFT) ? p.aux + row * L : nullptr;
     int i = mid;
     if (MODE != M_SOFT && dK == 0 && !p.fill && t0 + tend <= nvalid &&
-        p.tile_slow == nullptr) {  // interior outputs
+        true) {  // interior outputs
       const int canon = p.canon;
       for (; i + 3 * NMOV < tend; i += 4 * NMOV) {
         float v[4];
@@ -152,7 +151,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_fwd_pipe(const __grid_c
     }
     for (; i < tend; i += NMOV) {
       const int t = t0 + i;
-      if (!exact_owns(p.tile_slow, p.fast_J, p.fast_tpr, row, t)) continue;
       const int q = dK ? i + div_k(i, K, invK) : i;
       float v;
       if (t < nvalid) {
@@ -327,7 +325,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_fwd_pipe(const __grid_c
 template <int MODE, int EK>
 __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_bwd_pipe(const __grid_constant__ FGParams p,
                                                                int tiles_per_row, long long total) {
-  if (p.guard != nullptr && *p.guard == 0) return;  // fast path covered every tile
   extern __shared__ __align__(16) float sm[];
   __shared__ float padsum_sh[2];
   __shared__ float rng_sh[2][2][8];  // per buffer: {max, min} of M_t over live outputs, per mover warp
@@ -433,7 +430,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_bwd_pipe(const __grid_c
     Ev<MODE, EK> ev(p.child, row, p.mp);
     const int jn = (j0 + J < L ? j0 + J : L) - j0;
     int i0 = mid;
-    if (MODE == M_LSE && dK == 0 && j0 + jn < L && p.tile_slow == nullptr) {  // interior
+    if (MODE == M_LSE && dK == 0 && j0 + jn < L ) {  // interior
       for (; i0 + 7 * NMOV < jn; i0 += 8 * NMOV) {
         typename Ev<MODE, EK>::Raw r[8];
 #pragma unroll
@@ -460,7 +457,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 3) k_fgt_bwd_pipe(const __grid_c
         int i = i0 + u * NMOV;
         if (i >= jn) continue;
         int j = j0 + i;
-        if (!exact_owns(p.tile_slow, p.fast_J, p.fast_tpr, row, j)) continue;
         int q = dK ? i + div_k(i, K, invK) : i;
         float A = HG[q];
         float g = 0.f;

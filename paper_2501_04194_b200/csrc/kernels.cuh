@@ -24,10 +24,6 @@ struct FGParams {
   int fill;       // masked_fill compat: reduce sentinel-filled full columns (masking.py:195-202)
   float sent;     // SemanticsConfig.sentinel
   int dbg_skip;   // measurement knob (STLG_PIPE_SKIP): 1 skip scans, 2 skip loads/stores
-  const int* guard;  // exact kernels: run only if *guard != 0 (a fast-path tile needed them)
-  int* flag;         // fast-path kernels: set to 1 when a tile falls outside the fast range
-  int* tile_slow;    // per (row, fast tile): 1 if that tile was left to the exact kernel
-  int fast_J, fast_tpr;  // fast-path tiling (elements per tile, tiles per row)
   ModeP mp;
 };
 
@@ -90,10 +86,6 @@ cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st);
 cudaError_t launch_fgt_fwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st);
 cudaError_t launch_fgt_bwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st);
 bool pipe_enabled();
-bool fast_lse_applicable(const FGParams& p);
-cudaError_t launch_lse_fast_fwd(int ek, FGParams& p, int* slow, cudaStream_t st);
-cudaError_t launch_lse_fast_bwd(int ek, FGParams& p, int* slow, cudaStream_t st);
-int fast_lse_tile(int K);  // elements (outputs / owned children) per fast-path tile
 
 cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs, long long es,
                                 float v, cudaStream_t st);

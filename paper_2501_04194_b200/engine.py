@@ -150,38 +150,62 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+# rows per library call: the kernels index rows on grid.y (stlg_forward rejects
+# B > 65535); larger batches run as row chunks (rows are independent).
+MAX_ROWS_PER_CALL = 65535
+
+
+def _row_chunks(B):
+    return [(r, min(r + MAX_ROWS_PER_CALL, B)) for r in range(0, B, MAX_ROWS_PER_CALL)]
+
+
 class _TraceFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, comp, params, abc, *chans):
         B, T = chans[0].shape
         dev = chans[0].device
         out = torch.empty((B, T), dtype=torch.float32, device=dev)
-        fb, bb = comp.workspace_bytes(B, T)
-        fws = torch.empty(fb, dtype=torch.uint8, device=dev)
-        comp.forward(chans, params, out, fws, _stream())
+        fws_list = []
+        bb_list = []
+        for r0, r1 in _row_chunks(B):
+            fb, bb = comp.workspace_bytes(r1 - r0, T)
+            fws = torch.empty(fb, dtype=torch.uint8, device=dev)
+            comp.forward([c[r0:r1] for c in chans], params, out[r0:r1], fws, _stream())
+            fws_list.append(fws)
+            bb_list.append(bb)
         ctx.comp = comp
         ctx.params = params
-        ctx.bwd_bytes = bb
-        ctx.save_for_backward(out, fws, *chans)
+        ctx.bwd_bytes = bb_list
+        ctx.save_for_backward(out, *fws_list, *chans)
+        ctx.n_chunks = len(fws_list)
         return out
 
     @staticmethod
     def backward(ctx, g):
-        out, fws, *chans = ctx.saved_tensors
+        saved = ctx.saved_tensors
+        out = saved[0]
+        fws_list = saved[1:1 + ctx.n_chunks]
+        chans = saved[1 + ctx.n_chunks:]
         comp = ctx.comp
         B, T = out.shape
         dev = out.device
         g = g.to(torch.float32).contiguous()
         dch = [torch.empty((B, T), dtype=torch.float32, device=dev)
                if ctx.needs_input_grad[3 + i] else None for i in range(len(chans))]
-        d_smooth = None
-        if comp.n_smooth:
-            d_smooth = torch.zeros(3 * comp.n_smooth, dtype=torch.float64, device=dev)
-        bws = torch.empty(ctx.bwd_bytes, dtype=torch.uint8, device=dev)
-        comp.backward(chans, ctx.params, out, g, dch, d_smooth, fws, bws, _stream())
+        d_total = None
+        for (r0, r1), fws, bb in zip(_row_chunks(B), fws_list, ctx.bwd_bytes):
+            d_smooth = None
+            if comp.n_smooth:
+                d_smooth = torch.zeros(3 * comp.n_smooth, dtype=torch.float64, device=dev)
+            bws = torch.empty(bb, dtype=torch.uint8, device=dev)
+            comp.backward([c[r0:r1] for c in chans], ctx.params, out[r0:r1], g[r0:r1],
+                          [d[r0:r1] if d is not None else None for d in dch], d_smooth, fws, bws,
+                          _stream())
+            if d_smooth is not None:
+                d_total = d_smooth if d_total is None else d_total + d_smooth
         dabc = None
-        if ctx.needs_input_grad[2] and d_smooth is not None:
-            dabc = d_smooth.view(-1, 3).sum(0)
+        if ctx.needs_input_grad[2] and d_total is not None:
+            dabc = d_total.view(-1, 3).sum(0)
         return (None, None, dabc, *dch)
 
 

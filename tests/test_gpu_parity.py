@@ -242,3 +242,24 @@ def test_c4_full_size(cuda):
                                                        smooth_binding=(si.a, si.b, si.c))
     _, _, d4 = run(slice(0, 4))
     assert rel_err(d4, np.array(ref_abc)) <= SMOOTH_TOL
+
+
+def test_batch_beyond_one_launch_grid(cuda):
+    """B > 65535 rows (the kernels' grid.y limit): the API splits the batch into row
+    chunks; every row must equal the same row computed in a small batch."""
+    import torch
+    import paper_2501_04194_b200 as P
+    B, T = 65535 + 7, 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(B, T, device="cuda", generator=g)
+    f = P.Eventually(P.Pred("x", ">", 0.5), P.StepInterval(2, 9))
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(3.0))
+    xt = x.clone().requires_grad_(True)
+    out = P.trace(f, {"x": xt}, cfg)
+    (gx,) = torch.autograd.grad(out, [xt], torch.ones_like(out))
+    rows = [0, 65534, 65535, B - 1]
+    xs = x[rows].clone().requires_grad_(True)
+    out_s = P.trace(f, {"x": xs}, cfg)
+    (gs,) = torch.autograd.grad(out_s, [xs], torch.ones_like(out_s))
+    assert torch.equal(out[rows], out_s)
+    assert torch.equal(gx[rows], gs)

@@ -21,19 +21,22 @@ namespace stlg {
 // scan overwrites x in registers.
 template <int RK>
 __device__ __forceinline__ void cav_scans(RSt (&x)[RG_EPT], float tau2, float* P0, float* P1,
-                                          float* T0, float* T1) {
+                                          float* T0, float* T1, float* P2 = nullptr, float* T2 = nullptr) {
   const int base = threadIdx.x * (RG_EPT + 1);
   RSt run = x[0];
   P0[base] = run.m;
   if (RK != RK_HARD) P1[base] = run.s;
+  if (rk3<RK>()) P2[base] = run.q;
 #pragma unroll
   for (int k = 1; k < RG_EPT; ++k) {
     run = rcomb<RK>(run, x[k], tau2);
     P0[base + k] = run.m;
     if (RK != RK_HARD) P1[base + k] = run.s;
+    if (rk3<RK>()) P2[base + k] = run.q;
   }
   T0[threadIdx.x] = run.m;
   if (RK != RK_HARD) T1[threadIdx.x] = run.s;
+  if (rk3<RK>()) T2[threadIdx.x] = run.q;
 #pragma unroll
   for (int k = RG_EPT - 2; k >= 0; --k) x[k] = rcomb<RK>(x[k], x[k + 1], tau2);
 }
@@ -42,13 +45,15 @@ __device__ __forceinline__ void cav_scans(RSt (&x)[RG_EPT], float tau2, float* P
 // past the tile; such windows are never finished)
 template <int RK, int NW>
 __device__ __forceinline__ void cav_middle(int d, float tau2, const float* T0, const float* T1, RSt& A0,
-                                           RSt& A1) {
+                                           RSt& A1, const float* T2 = nullptr) {
   const int q = threadIdx.x;
   RSt a = rident<RK>();
   const int last = q + d < NW * 32 ? q + d : NW * 32;  // exclusive bound of readable chunks
-  for (int j = q + 1; j < q + d && j < last; ++j) a = rcomb<RK>(a, RSt{T0[j], RK == RK_HARD ? 0.f : T1[j]}, tau2);
+  for (int j = q + 1; j < q + d && j < last; ++j)
+    a = rcomb<RK>(a, RSt{T0[j], RK == RK_HARD ? 0.f : T1[j], rk3<RK>() ? T2[j] : 0.f}, tau2);
   A0 = a;
-  if (q + d < NW * 32) a = rcomb<RK>(a, RSt{T0[q + d], RK == RK_HARD ? 0.f : T1[q + d]}, tau2);
+  if (q + d < NW * 32)
+    a = rcomb<RK>(a, RSt{T0[q + d], RK == RK_HARD ? 0.f : T1[q + d], rk3<RK>() ? T2[q + d] : 0.f}, tau2);
   A1 = a;
 }
 
@@ -57,7 +62,7 @@ __device__ __forceinline__ void cav_middle(int d, float tau2, const float* T0, c
 template <int RK, bool FULL, typename Fin>
 __device__ __forceinline__ void cav_windows(const RSt (&S)[RG_EPT], RSt A0, RSt A1, int d, int c,
                                             float tau2, int lo, int hi, const float* P0,
-                                            const float* P1, Fin&& fin) {
+                                            const float* P1, Fin&& fin, const float* P2 = nullptr) {
   const int q = threadIdx.x;
   const int i0 = q * RG_EPT;
   const int sb = (q + d) * (RG_EPT + 1) + c;  // slot of o = k + c in chunk q + d
@@ -68,7 +73,7 @@ __device__ __forceinline__ void cav_windows(const RSt (&S)[RG_EPT], RSt A0, RSt 
       const bool up = k + c >= RG_EPT;       // the window ends in chunk q + d + 1
       const int sl = sb + k + (up ? 1 : 0);  // 17 (q + d + up) + (k + c - 16 up)
       RSt w = rcomb<RK>(S[k], up ? A1 : A0, tau2);
-      const RSt pv{P0[sl], RK == RK_HARD ? 0.f : P1[sl]};
+      const RSt pv{P0[sl], RK == RK_HARD ? 0.f : P1[sl], rk3<RK>() ? P2[sl] : 0.f};
       w = rcomb<RK>(w, pv, tau2);
       fin(k, i, w, sl);
     }
@@ -157,7 +162,8 @@ __device__ __forceinline__ void fs_windows(const float (&S)[RG_EPT], const FsCas
 // folds, window finish into the consumed prefix slots, coalesced stores.
 template <int RK, int NW>
 __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, int t0, int J, float padv,
-                                             RSt (&x)[RG_EPT], float* P0, float* P1, float* T0, float* T1) {
+                                             RSt (&x)[RG_EPT], float* P0, float* P1, float* T0, float* T1,
+                                             float* P2 = nullptr, float* T2 = nullptr) {
   using C = RC<NW>;
   constexpr int T = C::T, SS = C::SS;
   const int K = p.K;
@@ -167,7 +173,7 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   const float czero = p.canon ? 0.f : -0.f;
   float* outr = p.out + row * L;
-  float* auxr = (RK == RK_LSE && p.aux != nullptr) ? p.aux + row * L : nullptr;
+  float* auxr = ((RK == RK_LSE || RK == RK_SOFT) && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
   const int i0 = tid * RG_EPT;
@@ -200,19 +206,25 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
     }
   }
   if (!fs_done) {
-    cav_scans<RK>(x, tau2, P0, P1, T0, T1);  // own slots only: no barrier needed before
+    cav_scans<RK>(x, tau2, P0, P1, T0, T1, P2, T2);  // own slots only: no barrier needed before
     __syncthreads();
     RSt A0, A1;
-    cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1);
+    cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1, T2);
     auto fin = [&](int, int i, RSt w, int sl) {
       const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
-      const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
       const bool live = full || t0 + i < nvalid;
-      P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
-      if (RK == RK_LSE) P1[sl] = live ? sg * fmaf(l2, itau2, w.m - v) : 0.f;  // residual of v
+      if (RK == RK_SOFT) {  // value m + q / s; aux: the window LSE (max space) for the backward
+        const float v = w.m + w.q / w.s;
+        P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
+        P1[sl] = live ? fmaf(l2, itau2, w.m) : 0.f;
+      } else {
+        const float v = (RK == RK_HARD) ? w.m : fmaf(l2, itau2, w.m);
+        P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
+        if (RK == RK_LSE) P1[sl] = live ? sg * fmaf(l2, itau2, w.m - v) : 0.f;  // residual of v
+      }
     };
-    if (full) cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
-    else cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin);
+    if (full) cav_windows<RK, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin, P2);
+    else cav_windows<RK, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin, P2);
   }
   __syncthreads();
   {
@@ -221,7 +233,7 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
-    if (RK == RK_LSE && auxr != nullptr) {  // low word of the double-float trace
+    if (auxr != nullptr) {  // LSE: low word of the double-float trace; softmax: window LSE
       const float* src1 = P1 + rpad(tid + K - 1);
       float* ap = auxr + t0 + tid;
 #pragma unroll
@@ -239,9 +251,10 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
-  __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T];
+  __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T], T2[rk3<RK>() ? T : 1];
   float* P0 = rsm;
   float* P1 = rsm + C::NP;
+  float* P2 = rsm + 2 * C::NP;  // softmax only
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
   const int L = (int)p.L;
@@ -255,7 +268,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   float* outr = p.out + row * L;
-  float* auxr = (RK == RK_LSE && p.aux != nullptr) ? p.aux + row * L : nullptr;
+  float* auxr = ((RK == RK_LSE || RK == RK_SOFT) && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
   if (t0 >= nvalid) {  // every output of the tile overruns
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   RSt x[RG_EPT];
 #pragma unroll
   for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
-  cav_fwd_core<RK, NW>(p, row, t0, J, padv, x, P0, P1, T0, T1);
+  cav_fwd_core<RK, NW>(p, row, t0, J, padv, x, P0, P1, T0, T1, P2, T2);
 }
 
 // ---------------------------------------------------------------------------
@@ -443,6 +456,125 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
         const int sl = slb + (h + u) * SS;
         // S == 0 comes with m = -FLT_MAX or u_j + m <= 0: the product is an exact 0
         float g = P1[sl] * ex2f(tau2 * fmaf(sg, ev.value(j, r[u]), P0[sl]));
+        g += ((h + u) * T == jpad) ? padsum : 0.f;
+        ev.grad(j, r[u], g);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, softmax (gather form over outputs t; RK_GSOFT).  The reference VJP of
+// the softmax-weighted window (tape.py:360-380) gives child j
+//   sum_t g_t 2^{tau2 (u_j - L_t)} (1 + tau (u_j - M_t))
+//     = 2^{tau2 (u_j + m)} [A + tau ((u_j - c) A - Bc)],
+//   A = sum g_t 2^{-tau2 L_t - m},  Bc = sum g_t (M_t - c) 2^{-tau2 L_t - m}
+// with L_t the forward's window LSE (aux), M_t the trace (max space) and c a
+// per-tile centre (keeps the final difference small).
+// ---------------------------------------------------------------------------
+template <int EK, int NW>
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_soft(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS;
+  extern __shared__ float rsm[];
+  __shared__ float T0[T], T1[T], T2[T];
+  __shared__ float padsum_sh;
+  float* P0 = rsm;
+  float* P1 = rsm + C::NP;
+  float* P2 = rsm + 2 * C::NP;
+  const int K = p.K;
+  const int d = (K - 1) >> 4, c = (K - 1) & 15;
+  const int L = (int)p.L;
+  const long long row = blockIdx.y;
+  const int J = N - K + 1;  // owned child elements per tile
+  const int j0 = blockIdx.x * J;
+  const int tb = j0 - p.b;  // local index 0 <-> output t = tb
+  const int nvalid = L - p.b;
+  const float tau = p.mp.tau, tau2 = p.mp.tau2, sg = p.sg;
+  const float* cot = p.cot + row * L;
+  const float* outr = p.out_in + row * L;
+  const float* lser = p.aux_in + row * L;
+  const int tid = threadIdx.x;
+  const int thi = nvalid > 0 ? nvalid - 1 : 0;
+  const float cc = nvalid > 0 ? sg * outr[tb < 0 ? 0 : (tb > thi ? thi : tb)] : 0.f;  // centre
+  {
+    const int so = tid + (tid >> 4);
+    const int tt = tb + tid;
+    const bool interior = tb >= 0 && tb + N <= nvalid;
+#pragma unroll
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      float gv[CAV_LB], mv[CAV_LB], lv[CAV_LB];
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int t = tt + (h + k) * T;
+        const int tc = interior ? t : (t < 0 ? 0 : (t > thi ? thi : t));
+        gv[k] = ld_na(cot + tc);
+        mv[k] = ld_na(outr + tc);
+        lv[k] = ld_na(lser + tc);
+      }
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int t = tt + (h + k) * T;
+        const bool v = interior || (t >= 0 && t < nvalid);
+        P0[so + (h + k) * SS] = v ? -lv[k] : -FLT_MAX;
+        P1[so + (h + k) * SS] = v ? gv[k] : 0.f;
+        P2[so + (h + k) * SS] = v ? gv[k] * (sg * mv[k] - cc) : 0.f;
+      }
+    }
+  }
+  if (tid < 32) {  // overrun outputs route to c[L-1] ('last' padding)
+    float ps = 0.f;
+    if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + J) {
+      const int t_lo = nvalid > 0 ? nvalid : 0;
+      for (int t = t_lo + tid; t < L; t += 32) ps += cot[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    }
+    if (tid == 0) padsum_sh = ps;
+  }
+  __syncthreads();
+  RSt x[RG_EPT];
+#pragma unroll
+  for (int k = 0; k < RG_EPT; ++k) {
+    const int qq = tid * (RG_EPT + 1) + k;
+    x[k] = RSt{P0[qq], P1[qq], P2[qq]};
+  }
+  const bool full = tid * RG_EPT + RG_EPT <= J;
+  cav_scans<RK_GSOFT>(x, tau2, P0, P1, T0, T1, P2, T2);
+  __syncthreads();
+  {
+    RSt A0, A1;
+    cav_middle<RK_GSOFT, NW>(d, tau2, T0, T1, A0, A1, T2);
+    auto fin = [&](int, int, RSt w, int sl) {
+      P0[sl] = w.m;
+      P1[sl] = w.s;
+      P2[sl] = w.q;
+    };
+    if (full) cav_windows<RK_GSOFT, true>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin, P2);
+    else cav_windows<RK_GSOFT, false>(x, A0, A1, d, c, tau2, 0, J, P0, P1, fin, P2);
+  }
+  __syncthreads();
+  Ev<M_SOFT, EK> ev(p.child, row, p.mp);
+  const int jn = (j0 + J < L ? j0 + J : L) - j0;
+  const float padsum = padsum_sh;
+  const int slb = rpad(tid + K - 1);
+  const int jb = j0 + tid;
+  const int jpad = L - 1 - jb;
+#pragma unroll
+  for (int h = 0; h < RG_EPT; h += CAV_LB) {
+    typename Ev<M_SOFT, EK>::Raw r[CAV_LB];
+#pragma unroll
+    for (int u = 0; u < CAV_LB; ++u)
+      if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
+#pragma unroll
+    for (int u = 0; u < CAV_LB; ++u) {
+      if (tid + (h + u) * T < jn) {
+        const int j = jb + (h + u) * T;
+        const int sl = slb + (h + u) * SS;
+        const float uj = sg * ev.value(j, r[u]);
+        const float A = P1[sl];
+        // A == 0 comes with m = -FLT_MAX (nothing live) or u_j + m <= 0: exact 0
+        float g = ex2f(tau2 * (uj + P0[sl])) * fmaf(tau, fmaf(uj - cc, A, -P2[sl]), A);
         g += ((h + u) * T == jpad) ? padsum : 0.f;
         ev.grad(j, r[u], g);
       }

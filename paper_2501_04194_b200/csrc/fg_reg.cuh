@@ -33,7 +33,7 @@
 
 namespace stlg {
 
-enum { RK_HARD = 0, RK_HARDI = 1, RK_LSE = 2, RK_GLSE = 3 };
+enum { RK_HARD = 0, RK_HARDI = 1, RK_LSE = 2, RK_GLSE = 3, RK_SOFT = 4, RK_GSOFT = 5 };
 constexpr int RG_EPT = 16;  // samples per thread
 
 template <int NW>
@@ -48,8 +48,13 @@ struct RC {
 __device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
 
 struct RSt {
-  float m, s;
+  float m, s, q;  // q: softmax payload (RK_SOFT / RK_GSOFT), otherwise unused
 };
+// monoid kinds with a third state word
+template <int RK>
+constexpr bool rk3() {
+  return RK == RK_SOFT || RK == RK_GSOFT;
+}
 struct RSeg {
   float m, s;
   int r;  // a block boundary lies inside the covered range
@@ -57,20 +62,29 @@ struct RSeg {
 
 template <int RK>
 __device__ __forceinline__ RSt rident() {
-  if (RK == RK_HARD) return {-INFINITY, 0.f};
-  if (RK == RK_HARDI) return {-INFINITY, __int_as_float(-1)};
-  return {-FLT_MAX, 0.f};
+  if (RK == RK_HARD) return {-INFINITY, 0.f, 0.f};
+  if (RK == RK_HARDI) return {-INFINITY, __int_as_float(-1), 0.f};
+  return {-FLT_MAX, 0.f, 0.f};
 }
 
 // e covers earlier positions than l
 template <int RK>
 __device__ __forceinline__ RSt rcomb(RSt e, RSt l, float tau2) {
-  if (RK == RK_HARD) return {fmaxf(e.m, l.m), 0.f};
+  if (RK == RK_HARD) return {fmaxf(e.m, l.m), 0.f, 0.f};
   if (RK == RK_HARDI) return (l.m > e.m || __float_as_int(e.s) < 0) ? l : e;
   const float d = l.m - e.m;
   const float x = ex2f(-tau2 * fabsf(d));
   const bool up = d > 0.f;
-  return {up ? l.m : e.m, up ? fmaf(e.s, x, l.s) : fmaf(l.s, x, e.s)};
+  if (RK == RK_SOFT) {  // (m, s, q): s = sum 2^{tau2 (u - m)}, q = sum (u - m) 2^{tau2 (u - m)}
+    const float s_up = fmaf(e.s, x, l.s), q_up = fmaf(x, fmaf(-d, e.s, e.q), l.q);
+    const float s_dn = fmaf(l.s, x, e.s), q_dn = fmaf(x, fmaf(d, l.s, l.q), e.q);
+    return {up ? l.m : e.m, up ? s_up : s_dn, up ? q_up : q_dn};
+  }
+  if (RK == RK_GSOFT) {  // (m, a, b): two payloads under one max shift
+    return {up ? l.m : e.m, up ? fmaf(e.s, x, l.s) : fmaf(l.s, x, e.s),
+            up ? fmaf(e.q, x, l.q) : fmaf(l.q, x, e.q)};
+  }
+  return {up ? l.m : e.m, up ? fmaf(e.s, x, l.s) : fmaf(l.s, x, e.s), 0.f};
 }
 
 template <int RK>

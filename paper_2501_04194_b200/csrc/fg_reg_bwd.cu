@@ -19,6 +19,10 @@ static cudaError_t bwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
     } else {
       REG_DISPATCH_EK(ek, e = reg_launch(k_reg_bwd_hard<EK, NW>, grid, C::T, smem, p, st))
     }
+  } else if (mode == M_SOFT) {  // K >= 17 (reg_applicable)
+    const int J = C::N - p.K + 1;
+    dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
+    REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_soft<EK, NW>, grid, C::T, (size_t)3 * C::NP * 4, p, st))
   } else {
     const int J = C::N - p.K + 1;
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);

@@ -16,7 +16,7 @@ bool reg_enabled() {
 }
 
 bool reg_applicable(int mode, const FGParams& p, bool bwd) {
-  if (mode != M_HARD && mode != M_LSE) return false;
+  if (mode != M_HARD && mode != M_LSE && !(mode == M_SOFT && p.K >= 17)) return false;
   if (p.padmode || p.fill || p.K < 2 || p.L >= (1LL << 30) || p.B > 65535) return false;
   return reg_pick_nw(p.L, p.K, bwd && mode == M_HARD) > 0;
 }
@@ -35,6 +35,9 @@ static cudaError_t fwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
     } else {
       REG_DISPATCH_EK(ek, e = reg_launch(k_reg_fwd<RK_HARD, M_HARD, EK, NW>, grid, C::T, smem, p, st))
     }
+  } else if (mode == M_SOFT) {  // K >= 17 (reg_applicable)
+    const size_t smem = (size_t)3 * C::NP * 4;
+    REG_DISPATCH_EK(ek, e = reg_launch(k_cav_fwd<RK_SOFT, M_SOFT, EK, NW>, grid, C::T, smem, p, st))
   } else {
     const size_t smem = (size_t)2 * C::NP * 4;
     if (cav) {

@@ -476,6 +476,15 @@ struct LeafRegs {
       }
     }
   }
+  // store-mode at compile time (every gradient destination of the leaf is a first writer)
+  template <bool ST>
+  __device__ __forceinline__ static void put1t(float* p, int j, float g) {
+    if (p) {
+      if (ST) p[j] = g;
+      else p[j] += g;
+    }
+  }
+  __device__ __forceinline__ bool all_store() const { return (g1 == nullptr || st1) && (g2 == nullptr || st2); }
   __device__ __forceinline__ static void put1(float* p, int j, float g, int st) {
     if (p) {
       if (st) p[j] = g;
@@ -503,6 +512,8 @@ struct Ev<MODE, EK_AFF> : LeafRegs {
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + (long long)j * es1)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * (s_out * s_in), st1); }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw r, float g) const { grad(j, r, g); }
 };
 
 template <int MODE>
@@ -514,6 +525,8 @@ struct Ev<MODE, EK_AFF1> : LeafRegs {
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * (s_out * s_in), st1); }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw, float g) const { put1t<ST>(g1, j, g * (s_out * s_in)); }
 };
 
 template <int MODE>
@@ -525,6 +538,8 @@ struct Ev<MODE, EK_SRC> : LeafRegs {
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * r.x; }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * s_out, st1); }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw, float g) const { put1t<ST>(g1, j, g * s_out); }
 };
 
 template <int MODE>
@@ -547,6 +562,14 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
     float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
     put1(g1, j, dx * sc, st1);
     put1(g2, j, dy * sc, st2);
+  }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw r, float g) const {
+    float dx = r.x - cx, dy = r.y - cy;
+    float d2 = fmaf(dx, dx, dy * dy);
+    float sc = d2 > 0.f ? g * (s_out * s_in) * rsqrt_fast(d2) : 0.f;
+    put1t<ST>(g1, j, dx * sc);
+    put1t<ST>(g2, j, dy * sc);
   }
 };
 
@@ -582,6 +605,8 @@ struct Ev<MODE, EK_PAIR> : LeafRegs {
       put(g2, ges2, j, dy * sc, st2);
     }
   }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw r, float g) const { grad(j, r, g); }
 };
 
 template <int MODE>
@@ -594,6 +619,9 @@ struct Ev<MODE, EK_GEN> {
   __device__ __forceinline__ Raw load(int) const { return Raw{}; }
   __device__ __forceinline__ float value(int j, Raw) const { return expr_eval<MODE>(*e, row, j, mp); }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { expr_vjp<MODE>(*e, row, j, g, mp); }
+  template <bool ST>
+  __device__ __forceinline__ void grad_t(int j, Raw r, float g) const { grad(j, r, g); }
+  __device__ __forceinline__ bool all_store() const { return false; }
 };
 
 // host-side choice of the evaluator for an expression

@@ -13,6 +13,8 @@
 // load; the result is written into the prefix slot it consumed (each slot is read
 // by exactly one window), then stored coalesced.  Exact monoids (fg_reg.cuh).
 #pragma once
+#include <type_traits>
+
 #include "fg_reg.cuh"
 
 namespace stlg {
@@ -29,7 +31,7 @@ __device__ __forceinline__ void cav_scans(RSt (&x)[RG_EPT], float tau2, float* P
   if (rk3<RK>()) P2[base] = run.q;
 #pragma unroll
   for (int k = 1; k < RG_EPT; ++k) {
-    run = rcomb<RK>(run, x[k], tau2);
+    run = rcomb_s<RK>(run, x[k], tau2);
     P0[base + k] = run.m;
     if (RK != RK_HARD) P1[base + k] = run.s;
     if (rk3<RK>()) P2[base + k] = run.q;
@@ -38,7 +40,7 @@ __device__ __forceinline__ void cav_scans(RSt (&x)[RG_EPT], float tau2, float* P
   if (RK != RK_HARD) T1[threadIdx.x] = run.s;
   if (rk3<RK>()) T2[threadIdx.x] = run.q;
 #pragma unroll
-  for (int k = RG_EPT - 2; k >= 0; --k) x[k] = rcomb<RK>(x[k], x[k + 1], tau2);
+  for (int k = RG_EPT - 2; k >= 0; --k) x[k] = rcomb_s<RK>(x[k], x[k + 1], tau2);
 }
 
 // middle folds: A0 = chunks q+1 .. q+d-1, A1 = A0 (+) chunk q+d (identity when empty /
@@ -631,35 +633,50 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
-  // phase 1: child values u (window start i <-> t = first + i - a), clamped loads
+  // phase 1: child values u (window start i <-> t = first + i - a)
   {
     const int so = tid + (tid >> 4);
     const int jb = first + tid;
     const int tb = jb - p.a;
-    const int thi = nvalid > 0 ? nvalid - 1 : 0;
-    const bool interior = first >= 0 && first + N <= L && first - p.a >= 0 && first - p.a + nwin <= nvalid;
+    if (first >= 0 && first + N <= L && first - p.a >= 0 && first - p.a + nwin <= nvalid) {
 #pragma unroll
-    for (int h = 0; h < RG_EPT; h += CAV_LB) {
-      typename Ev<M_HARD, EK>::Raw r[CAV_LB];
-      float gv[CAV_LB];
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        typename Ev<M_HARD, EK>::Raw r[CAV_LB];
+        float gv[CAV_LB];
 #pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int j = jb + (h + k) * T, t = tb + (h + k) * T;
-        r[k] = ev.load(interior ? j : (j < 0 ? 0 : (j >= L ? L - 1 : j)));
-        gv[k] = ld_na(cot + (interior ? t : (t < 0 ? 0 : (t > thi ? thi : t))));
+        for (int k = 0; k < CAV_LB; ++k) {
+          r[k] = ev.load(jb + (h + k) * T);
+          gv[k] = ld_na(cot + tb + (h + k) * T);  // i >= nwin: masked below
+        }
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          P0[so + (h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
+          P1[so + (h + k) * SS] = (tid + (h + k) * T < nwin) ? gv[k] : 0.f;
+        }
       }
+    } else {  // clamped loads: samples outside the row feed no live window
+      const int thi = nvalid > 0 ? nvalid - 1 : 0;
 #pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int i = tid + (h + k) * T;
-        const int j = jb + (h + k) * T, t = tb + (h + k) * T;
-        const int jc = interior ? j : (j < 0 ? 0 : (j >= L ? L - 1 : j));
-        const bool wv = i < nwin && (interior || (t >= 0 && t < nvalid));
-        P0[so + (h + k) * SS] = sg * ev.value(jc, r[k]);  // out-of-row samples feed no live window
-        P1[so + (h + k) * SS] = wv ? gv[k] : 0.f;
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        typename Ev<M_HARD, EK>::Raw r[CAV_LB];
+        float gv[CAV_LB];
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int j = jb + (h + k) * T, t = tb + (h + k) * T;
+          r[k] = ev.load(j < 0 ? 0 : (j >= L ? L - 1 : j));
+          gv[k] = ld_na(cot + (t < 0 ? 0 : (t > thi ? thi : t)));
+        }
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int j = jb + (h + k) * T, t = tb + (h + k) * T;
+          const bool wv = tid + (h + k) * T < nwin && t >= 0 && t < nvalid;
+          P0[so + (h + k) * SS] = sg * ev.value(j < 0 ? 0 : (j >= L ? L - 1 : j), r[k]);
+          P1[so + (h + k) * SS] = wv ? gv[k] : 0.f;
+        }
       }
     }
   }
-  if (tid < 32) {
+  if (tid < 32) {  // overrun outputs route to c[L-1] ('last' padding)
     float ps = 0.f;
     if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + Jo) {
       const int t_lo = nvalid > 0 ? nvalid : 0;
@@ -670,15 +687,17 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
     if (tid == 0) padsum_sh = ps;
   }
   __syncthreads();
+  const float padsum = padsum_sh;
+  const int kpad = (padsum != 0.f) ? L - 1 - first : -1;  // local index receiving the pad sum
   RSt x[RG_EPT];
   float g[RG_EPT];
   {
     const int q0 = tid * (RG_EPT + 1);
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) {
-      x[k] = RSt{P0[q0 + k], __int_as_float(tid * RG_EPT + k)};
+      x[k] = RSt{P0[q0 + k], __int_as_float(tid * RG_EPT + k), 0.f};
       g[k] = P1[q0 + k];
-      G[q0 + k] = 0.f;
+      G[q0 + k] = (tid * RG_EPT + k == kpad) ? padsum : 0.f;
     }
   }
   cav_scans<RK_HARDI>(x, 0.f, P0, P1, T0, T1);
@@ -693,27 +712,25 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
     if (tid * RG_EPT + RG_EPT <= nwin) cav_windows<RK_HARDI, true>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
     else cav_windows<RK_HARDI, false>(x, A0, A1, d, c, 0.f, 0, nwin, P0, P1, fin);
   }
-  // runs of equal keys (ascending window order); interior runs are written directly
+  // runs of equal keys (ascending window order), branch-free: an interior run is
+  // stored where it ends; the first / last runs go through the carry scan
   const int kf = key[0];
-  float sf = 0.f, sl = 0.f;
+  float sf = 0.f, acc = 0.f;
   {
     int cur = kf;
-    float acc = 0.f;
     bool firstrun = true;
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) {
-      if (key[k] != cur) {
-        if (firstrun) sf = acc;
-        else if (cur != NOKEY) G[rpad(cur)] = acc;
-        firstrun = false;
-        cur = key[k];
-        acc = 0.f;
-      }
-      acc += g[k];
+      const bool chg = key[k] != cur;
+      if (chg && !firstrun && cur != NOKEY) G[rpad(cur)] = acc + (cur == kpad ? padsum : 0.f);
+      sf = (chg && firstrun) ? acc : sf;
+      firstrun = firstrun && !chg;
+      acc = chg ? g[k] : acc + g[k];
+      cur = key[k];
     }
-    sl = acc;
     if (firstrun) sf = acc;
   }
+  const float sl = acc;
   const int kl = key[RG_EPT - 1];
   const bool single = kf == kl;
   // carries: inclusive segmented scan of the trailing runs over lanes, then warps
@@ -729,35 +746,34 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const 
   if (lane == 0) WK[warp] = kf;
   __syncthreads();
   RunSeg wc{NOKEY, 0.f, 0};  // fold of the warps below
-  for (int w = 0; w < warp; ++w) wc = (w == 0) ? WR[0] : run_comb(wc, WR[w]);
+#pragma unroll
+  for (int w = 0; w < NW - 1; ++w)
+    if (w < warp) wc = (w == 0) ? WR[0] : run_comb(wc, WR[w]);
   const RunSeg cin = lane == 0 ? wc : (warp > 0 ? run_comb(wc, ex) : ex);
   const float carry = (cin.key == kf && kf != NOKEY) ? cin.s : 0.f;
   const int kn = lane < 31 ? kf_next_lane : (warp + 1 < NW ? WK[warp + 1] : NOKEY - 1);
-  if (!single && kf != NOKEY) G[rpad(kf)] = carry + sf;  // first run ends inside this chunk
-  if (kl != NOKEY && kn != kl) G[rpad(kl)] = single ? carry + sl : sl;  // trailing run ends here
+  if (!single && kf != NOKEY) G[rpad(kf)] = carry + sf + (kf == kpad ? padsum : 0.f);
+  if (kl != NOKEY && kn != kl) G[rpad(kl)] = (single ? carry + sl : sl) + (kl == kpad ? padsum : 0.f);
   __syncthreads();
-  // phase 3: owned local indices [K - 1, K - 1 + Jo)
+  // phase 3: owned local indices [K - 1, K - 1 + Jo): fused child VJP
   const int jn = (j0 + Jo < L ? j0 + Jo : L) - j0;
-  const float padsum = padsum_sh;
   const int gb = rpad(tid + K - 1);
   const int jb = j0 + tid;
-  const int jpad = L - 1 - jb;
+  auto vjp = [&](auto store) {
+    constexpr bool ST = decltype(store)::value;
 #pragma unroll
-  for (int h = 0; h < RG_EPT; h += CAV_LB) {
-    typename Ev<M_HARD, EK>::Raw r[CAV_LB];
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      typename Ev<M_HARD, EK>::Raw r[CAV_LB];
 #pragma unroll
-    for (int u = 0; u < CAV_LB; ++u)
-      if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
+      for (int u = 0; u < CAV_LB; ++u)
+        if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
 #pragma unroll
-    for (int u = 0; u < CAV_LB; ++u) {
-      if (tid + (h + u) * T < jn) {
-        const int j = jb + (h + u) * T;
-        float gg = G[gb + (h + u) * SS];
-        gg += ((h + u) * T == jpad) ? padsum : 0.f;
-        ev.grad(j, r[u], gg);
-      }
+      for (int u = 0; u < CAV_LB; ++u)
+        if (tid + (h + u) * T < jn) ev.template grad_t<ST>(jb + (h + u) * T, r[u], G[gb + (h + u) * SS]);
     }
-  }
+  };
+  if (ev.all_store()) vjp(std::true_type{});
+  else vjp(std::false_type{});
 }
 
 }  // namespace stlg

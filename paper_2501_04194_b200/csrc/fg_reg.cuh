@@ -87,6 +87,14 @@ __device__ __forceinline__ RSt rcomb(RSt e, RSt l, float tau2) {
   return {up ? l.m : e.m, up ? fmaf(e.s, x, l.s) : fmaf(l.s, x, e.s), 0.f};
 }
 
+// scan-internal combine: both operands are real states (no identity), so the
+// first-argmax kind skips the identity test
+template <int RK>
+__device__ __forceinline__ RSt rcomb_s(RSt e, RSt l, float tau2) {
+  if (RK == RK_HARDI) return (l.m > e.m) ? l : e;
+  return rcomb<RK>(e, l, tau2);
+}
+
 template <int RK>
 __device__ __forceinline__ RSeg rshfl_up(RSeg v, int o) {
   RSeg r;

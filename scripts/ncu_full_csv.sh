@@ -7,5 +7,6 @@ ncu --set full --import-source on --clock-control none -k regex:$kre -s $skip -c
 rc=$?
 ncu -i gpurun_out/$name.ncu-rep --page raw --csv > gpurun_out/$name.csv 2>/dev/null
 ncu -i gpurun_out/$name.ncu-rep --page source --csv --print-source sass > gpurun_out/${name}_sass.csv 2>/dev/null
+ncu -i gpurun_out/$name.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${name}_src.csv 2>/dev/null
 [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/$name.ncu-rep
 echo "$name rc=$rc"

@@ -283,20 +283,29 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   {
     float* dst = P0 + tid + (tid >> 4);
     const int jb = s0 + tid;
-    const bool interior = s0 + N <= L;
+    if (s0 + N <= L) {
 #pragma unroll
-    for (int h = 0; h < RG_EPT; h += CAV_LB) {
-      typename Ev<MODE, EK>::Raw r[CAV_LB];
-      // past the row end: replicate the last sample (feeds overrun windows only)
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        typename Ev<MODE, EK>::Raw r[CAV_LB];
 #pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int j = jb + (h + k) * T;
-        r[k] = ev.load(interior ? j : (j < L ? j : L - 1));
+        for (int k = 0; k < CAV_LB; ++k) r[k] = ev.load(jb + (h + k) * T);
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) dst[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
       }
+    } else {  // past the row end: replicate the last sample (feeds overrun windows only)
 #pragma unroll
-      for (int k = 0; k < CAV_LB; ++k) {
-        const int j = jb + (h + k) * T;
-        dst[(h + k) * SS] = sg * ev.value(interior ? j : (j < L ? j : L - 1), r[k]);
+      for (int h = 0; h < RG_EPT; h += CAV_LB) {
+        typename Ev<MODE, EK>::Raw r[CAV_LB];
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int j = jb + (h + k) * T;
+          r[k] = ev.load(j < L ? j : L - 1);
+        }
+#pragma unroll
+        for (int k = 0; k < CAV_LB; ++k) {
+          const int j = jb + (h + k) * T;
+          dst[(h + k) * SS] = sg * ev.value(j < L ? j : L - 1, r[k]);
+        }
       }
     }
   }

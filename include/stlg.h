@@ -164,6 +164,20 @@ STLG_API int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, 
                   const stlg_grad* d_channels, double* d_smooth, void* fwd_ws,
                   size_t fwd_ws_bytes, void* bwd_ws, size_t bwd_ws_bytes, void* stream);
 
+/* Batched interval-mining objective (replaces the per-pair
+ * loop of apps.grid_eval over apps.mining_objective, apps.py:272-335).
+ * data: device fp32 [n, length] (row stride `row_stride`, unit element stride);
+ * a, b: device fp64 [npairs] window bounds in (0, 1); sharp: sigmoid sharpness c;
+ * mode: STLG_MODE_* with temperature `temp`.  loss_out (device fp64 [npairs]):
+ *   mean_n relu(-rho0_n) + gamma (a - b),  rho0_n = smooth min of row n under
+ *   w_i = relu(sigmoid(c (i - a L)) - sigmoid(c (i - b L)) - eps);
+ * NaN where no weight is positive (the reference's EmptyWindowError).
+ * dloss_out (device fp64 [2 npairs], optional): d loss / d a, d loss / d b. */
+STLG_API int stlg_mining_grid(const float* data, int64_t n, int64_t length, int64_t row_stride,
+                              const double* a, const double* b, int64_t npairs, double sharp,
+                              double eps, int32_t mode, double temp, double gamma, double* loss_out,
+                              double* dloss_out, void* stream);
+
 /* Count of device kernel launches issued by the library (all threads) since the last reset. */
 STLG_API int64_t stlg_launch_count(int reset);
 

@@ -21,6 +21,8 @@ from .engine import (Compiled, Gradients, always_trace, compile_formula, eventua
 
 __version__ = "0.1.0"
 
+from .mining import AnnealSchedule, MiningConfig, grid_eval_mining, mine_interval, mining_objective
+
 __all__ = [
     "DivergedError", "EmptySignalError", "EmptyWindowError", "Hard", "InvalidIntervalError",
     "LogSumExp", "Mode", "NamedSignals", "NonFiniteSampleError", "PaddingPolicy",
@@ -31,4 +33,5 @@ __all__ = [
     "validate_against", "variables",
     "Compiled", "Gradients", "always_trace", "compile_formula", "eventually_trace", "robustness",
     "robustness_trace", "trace", "until_trace", "value_and_grad",
+    "AnnealSchedule", "MiningConfig", "grid_eval_mining", "mine_interval", "mining_objective",
 ]

@@ -23,7 +23,8 @@ MODE_HARD, MODE_SOFTMAX, MODE_LSE = 0, 1, 2
 OK, E_SHAPE, E_EMPTY_WINDOW, E_UNSUPPORTED, E_CUDA, E_INVALID = range(6)
 
 EXPORTS = ("stlg_abi_version", "stlg_last_error", "stlg_compile", "stlg_free", "stlg_plan_info",
-           "stlg_workspace_bytes", "stlg_forward", "stlg_backward", "stlg_launch_count")
+           "stlg_workspace_bytes", "stlg_forward", "stlg_backward", "stlg_launch_count",
+           "stlg_mining_grid")
 
 
 class StlgNode(ctypes.Structure):
@@ -93,6 +94,10 @@ def load():
         lib.stlg_backward.restype = c_int
         lib.stlg_launch_count.argtypes = [c_int]
         lib.stlg_launch_count.restype = c_int64
+        lib.stlg_mining_grid.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_int64,
+                                         c_double, c_double, c_int32, c_double, c_double, c_void_p,
+                                         c_void_p, c_void_p]
+        lib.stlg_mining_grid.restype = c_int
         got = lib.stlg_abi_version()
         if got != ABI_VERSION:
             raise RuntimeError(f"libstlg ABI {got} != expected {ABI_VERSION}; rebuild the library")

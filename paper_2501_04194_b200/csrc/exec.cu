@@ -396,6 +396,21 @@ int stlg_abi_version(void) { return STLG_ABI_VERSION; }
 
 const char* stlg_last_error(void) { return g_err.c_str(); }
 
+int stlg_mining_grid(const float* data, int64_t n, int64_t length, int64_t row_stride, const double* a,
+                     const double* b, int64_t npairs, double sharp, double eps, int32_t mode, double temp,
+                     double gamma, double* loss_out, double* dloss_out, void* stream) {
+  if (!data || !a || !b || !loss_out) return fail(STLG_E_INVALID, "null argument");
+  if (n <= 0 || length <= 0) return fail(STLG_E_SHAPE, "dataset must be a non-empty (n, length) array");
+  if (npairs < 0) return fail(STLG_E_INVALID, "negative pair count");
+  if (mode != STLG_MODE_HARD && !(temp > 0)) return fail(STLG_E_INVALID, "temperature must be positive");
+  if ((size_t)3 * length * sizeof(float) > 220 * 1024)
+    return fail(STLG_E_UNSUPPORTED, "mining rows longer than 18000 samples");
+  const int m = mode == STLG_MODE_HARD ? M_HARD : (mode == STLG_MODE_LSE ? M_LSE : M_SOFT);
+  cudaError_t ce = launch_mining_grid(m, data, n, (int)length, row_stride, a, b, npairs, sharp, eps,
+                                      (float)temp, gamma, loss_out, dloss_out, (cudaStream_t)stream);
+  return cuda_status(ce, "mining launch");
+}
+
 int64_t stlg_launch_count(int reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }

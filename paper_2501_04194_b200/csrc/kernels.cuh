@@ -78,6 +78,9 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st);
 size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K);
+cudaError_t launch_mining_grid(int mode, const float* x, long long n, int L, long long rs, const double* a,
+                               const double* b, long long npairs, double c, double eps, float tau,
+                               double gamma, double* loss, double* dloss, cudaStream_t st);
 cudaError_t launch_until_fwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_until_bwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st);

@@ -179,3 +179,16 @@ def test_large_elementwise_trees_are_split():
         f = P.And(f, l)
     c = P.compile_formula(P.Eventually(f, P.StepInterval(0, 4)), ["x"], P.SemanticsConfig())
     assert c.n_slots >= 1 and c.root_temporal == 1
+
+
+def test_anneal_schedule_matches_reference_formula():
+    """smoothing.py:146-160: endpoints hit exactly, sigmoid midpoint."""
+    from paper_2501_04194_b200.mining import AnnealSchedule
+    s = AnnealSchedule("sigmoid", 1.0, 30.0, 100)
+    assert abs(s.value(0) - 1.0) < 1e-12 and abs(s.value(100) - 30.0) < 1e-12
+    assert abs(s.value(50) - 15.5) < 1e-12
+    lin = AnnealSchedule("linear", 2.0, 4.0, 10)
+    assert abs(lin.value(5) - 3.0) < 1e-12
+    assert AnnealSchedule("constant", 7.0, 7.0, 1).value(123) == 7.0
+    with pytest.raises(ValueError):
+        AnnealSchedule("cubic", 1.0, 2.0, 3)

@@ -22,6 +22,8 @@ from .engine import (Compiled, Gradients, always_trace, compile_formula, eventua
 __version__ = "0.1.0"
 
 from .mining import AnnealSchedule, MiningConfig, grid_eval_mining, mine_interval, mining_objective
+from .planning import (PlannerConfig, box_formula, plan_trajectory, planning_formula, planning_objective,
+                       rollout_single_integrator)
 
 __all__ = [
     "DivergedError", "EmptySignalError", "EmptyWindowError", "Hard", "InvalidIntervalError",
@@ -34,4 +36,6 @@ __all__ = [
     "Compiled", "Gradients", "always_trace", "compile_formula", "eventually_trace", "robustness",
     "robustness_trace", "trace", "until_trace", "value_and_grad",
     "AnnealSchedule", "MiningConfig", "grid_eval_mining", "mine_interval", "mining_objective",
+    "PlannerConfig", "box_formula", "plan_trajectory", "planning_formula", "planning_objective",
+    "rollout_single_integrator",
 ]

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 LIB = os.path.join(HERE, "libstlg.so")
-SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_reg_bwd.cu", "until.cu", "smooth.cu", "mining.cu"]
+SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_reg_bwd.cu", "fg_unt.cu", "until.cu", "smooth.cu", "mining.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "fg_reg.cuh", "fg_cav.cuh"]
 
 NVCC_FLAGS = [

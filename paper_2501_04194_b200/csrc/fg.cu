@@ -1139,6 +1139,8 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_bwd_hard(const __grid_const
 }
 
 cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st) {
+  cudaError_t err;
+  if (reg_enabled() && launch_unt_fwd(mode, p, st, err)) return err;
   dim3 grid((unsigned)p.B);
   if (mode == M_HARD) k_fg_untimed_fwd<M_HARD><<<grid, UT_T, 0, st>>>(p);
   else if (mode == M_LSE) k_fg_untimed_fwd<M_LSE><<<grid, UT_T, 0, st>>>(p);

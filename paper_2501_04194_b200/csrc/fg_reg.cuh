@@ -33,7 +33,9 @@
 
 namespace stlg {
 
-enum { RK_HARD = 0, RK_HARDI = 1, RK_LSE = 2, RK_GLSE = 3, RK_SOFT = 4, RK_GSOFT = 5 };
+// RK_HARDV: value-only first argmax (ties keep the earlier operand, so -0 / +0 follow
+// the reference where no `+ 0.0` canonicalisation follows, e.g. untimed windows)
+enum { RK_HARD = 0, RK_HARDI = 1, RK_LSE = 2, RK_GLSE = 3, RK_SOFT = 4, RK_GSOFT = 5, RK_HARDV = 6 };
 constexpr int RG_EPT = 16;  // samples per thread
 
 template <int NW>
@@ -62,7 +64,7 @@ struct RSeg {
 
 template <int RK>
 __device__ __forceinline__ RSt rident() {
-  if (RK == RK_HARD) return {-INFINITY, 0.f, 0.f};
+  if (RK == RK_HARD || RK == RK_HARDV) return {-INFINITY, 0.f, 0.f};
   if (RK == RK_HARDI) return {-INFINITY, __int_as_float(-1), 0.f};
   return {-FLT_MAX, 0.f, 0.f};
 }
@@ -71,6 +73,7 @@ __device__ __forceinline__ RSt rident() {
 template <int RK>
 __device__ __forceinline__ RSt rcomb(RSt e, RSt l, float tau2) {
   if (RK == RK_HARD) return {fmaxf(e.m, l.m), 0.f, 0.f};
+  if (RK == RK_HARDV) return (l.m > e.m) ? l : e;
   if (RK == RK_HARDI) return (l.m > e.m || __float_as_int(e.s) < 0) ? l : e;
   const float d = l.m - e.m;
   const float x = ex2f(-tau2 * fabsf(d));

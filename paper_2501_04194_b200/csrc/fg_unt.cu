@@ -1,0 +1,145 @@
+// fg_unt.cu — untimed Eventually / Always forward, hard and LSE (masking.py:217-227,
+// tape.py:475-535: out[t] = R_{j = t .. L-1} s[j], a reverse scan per row, no padding,
+// no `+ 0.0` canonicalisation).
+//
+// One CTA per row walks the row from its end in tiles of 16 T samples: coalesced
+// loads through the typed child evaluator, a transpose through shared memory, each
+// thread scans its 16-sample chunk in registers, a warp-shuffle suffix scan and one
+// cross-warp step give every thread the fold of the samples after its chunk (plus
+// the carry of the tiles already done), and the outputs leave through shared memory
+// with coalesced stores.  Three barriers per 4096 samples; two alternating buffers
+// let the next tile's loads overlap the previous tile's stores.
+#include "fg_reg.cuh"
+
+namespace stlg {
+
+constexpr int UN_NW = 8;
+using UNC = RC<UN_NW>;
+
+template <int RK, int MODE, int EK>
+__global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ FGParams p) {
+  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
+  __shared__ float buf[2][NP];
+  __shared__ RSt WS[UN_NW];
+  const long long row = blockIdx.x;
+  const int L = (int)p.L;
+  const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Ev<MODE, EK> ev(p.child, row, p.mp);
+  float* outr = p.out + row * L;
+  const RSt id = rident<RK>();
+  RSt carry = id;  // fold of every sample after the current tile
+  int b = 0;
+  for (int c0 = ((L - 1) / N) * N; c0 >= 0; c0 -= N, b ^= 1) {
+    float* P = buf[b];
+    const int nt = (L - c0 < N) ? L - c0 : N;  // live samples in this tile
+    {
+      float* dst = P + tid + (tid >> 4);
+      const int jb = c0 + tid;
+      if (nt == N) {
+#pragma unroll
+        for (int h = 0; h < RG_EPT; h += 8) {
+          typename Ev<MODE, EK>::Raw r[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) r[k] = ev.load(jb + (h + k) * T);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dst[(h + k) * SS] = sg * ev.value(jb + (h + k) * T, r[k]);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < RG_EPT; h += 8) {
+          typename Ev<MODE, EK>::Raw r[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = jb + (h + k) * T;
+            r[k] = ev.load(j < L ? j : L - 1);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = jb + (h + k) * T;
+            dst[(h + k) * SS] = sg * ev.value(j < L ? j : L - 1, r[k]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // chunk [16 tid, 16 tid + 16): suffix scan in registers (past the row end: identity)
+    RSt S[RG_EPT];
+    const int q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) S[k] = (i0 + k < nt) ? RSt{P[q0 + k], 1.f, 0.f} : id;
+#pragma unroll
+    for (int k = RG_EPT - 2; k >= 0; --k) S[k] = rcomb_s<RK>(S[k], S[k + 1], tau2);
+    // fold of the later threads of the warp, then of the later warps and tiles
+    RSt v = S[0];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      RSt w{__shfl_down_sync(0xffffffffu, v.m, o), RK == RK_HARDV ? 0.f : __shfl_down_sync(0xffffffffu, v.s, o), 0.f};
+      if (lane + o < 32) v = rcomb<RK>(v, w, tau2);
+    }
+    RSt ex{__shfl_down_sync(0xffffffffu, v.m, 1), RK == RK_HARDV ? 0.f : __shfl_down_sync(0xffffffffu, v.s, 1), 0.f};
+    if (lane == 0) WS[warp] = v;
+    __syncthreads();
+    RSt cw = carry;
+#pragma unroll
+    for (int w = UN_NW - 1; w > 0; --w)
+      if (w > warp) cw = rcomb<RK>(WS[w], cw, tau2);
+    const RSt cin = lane < 31 ? rcomb<RK>(ex, cw, tau2) : cw;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) {
+      const RSt o = rcomb<RK>(S[k], cin, tau2);
+      const float val = (RK == RK_HARDV) ? o.m : fmaf(lg2f(o.s), itau2, o.m);
+      P[q0 + k] = sg * val;  // own slots: read by the coalesced store after the barrier
+    }
+    {
+      RSt tile = WS[UN_NW - 1];
+#pragma unroll
+      for (int w = UN_NW - 2; w >= 0; --w) tile = rcomb<RK>(WS[w], tile, tau2);
+      carry = rcomb<RK>(tile, carry, tau2);
+    }
+    __syncthreads();
+    const float* src = P + tid + (tid >> 4);
+    float* op = outr + c0 + tid;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k)
+      if (tid + k * T < nt) op[k * T] = src[k * SS];
+  }
+}
+
+#define UNT_DISPATCH_EK(EKV, ...)      \
+  if ((EKV) == EK_AFF1) {              \
+    constexpr int EK = EK_AFF1;        \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_AFF) {        \
+    constexpr int EK = EK_AFF;         \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_NORM) {       \
+    constexpr int EK = EK_NORM;        \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_SRC) {        \
+    constexpr int EK = EK_SRC;         \
+    __VA_ARGS__;                       \
+  } else if ((EKV) == EK_PAIR) {       \
+    constexpr int EK = EK_PAIR;        \
+    __VA_ARGS__;                       \
+  } else {                             \
+    constexpr int EK = EK_GEN;         \
+    __VA_ARGS__;                       \
+  }
+
+// register-blocked untimed forward (hard / LSE without masked_fill); false: not handled
+bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
+  if (p.fill || (mode != M_HARD && mode != M_LSE) || p.L >= (1LL << 30)) return false;
+  const int ek = expr_kind(p.child);
+  dim3 grid((unsigned)p.B);
+  if (mode == M_HARD) {
+    UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_HARDV, M_HARD, EK><<<grid, UNC::T, 0, st>>>(p)))
+  } else {
+    UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_LSE, M_LSE, EK><<<grid, UNC::T, 0, st>>>(p)))
+  }
+  count_launch();
+  err = cudaGetLastError();
+  return true;
+}
+
+}  // namespace stlg

@@ -1150,6 +1150,10 @@ cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st) {
 }
 
 cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st) {
+  {
+    cudaError_t err;
+    if (reg_enabled() && launch_unt_bwd(mode, p, st, err)) return err;
+  }
   dim3 grid((unsigned)p.B);
   if (mode == M_HARD) {
     cudaError_t e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st);

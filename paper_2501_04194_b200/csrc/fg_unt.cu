@@ -106,6 +106,100 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
   }
 }
 
+// Untimed LSE backward (gather form, tape.py:475-535): child j receives
+//   2^{tau2 u_j} sum_{t <= j} g_t 2^{-tau2 M_t}
+// — an inclusive prefix scan over the outputs of the (e_t = -M_t, g_t) elements
+// (RK_GLSE), tiles walked from the row start with the carry of the tiles done, then
+// the fused child VJP over the tile.
+template <int EK>
+__global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant__ FGParams p) {
+  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
+  __shared__ float B0[NP], B1[NP];
+  __shared__ RSt WP[UN_NW];
+  const long long row = blockIdx.x;
+  const int L = (int)p.L;
+  const float tau2 = p.mp.tau2, sg = p.sg, nsg = -p.sg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* cot = p.cot + row * L;
+  const float* outr = p.out_in + row * L;
+  Ev<M_LSE, EK> ev(p.child, row, p.mp);
+  const RSt id = rident<RK_GLSE>();
+  RSt carry = id;  // fold of every output before the current tile
+  const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
+  for (int c0 = 0; c0 < L; c0 += N) {
+    const int nt = (L - c0 < N) ? L - c0 : N;
+#pragma unroll
+    for (int h = 0; h < RG_EPT; h += 8) {
+      float gv[8], mv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = c0 + tid + (h + k) * T;
+        const int tc = t < L ? t : L - 1;
+        gv[k] = ld_na(cot + tc);
+        mv[k] = ld_na(outr + tc);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool v = tid + (h + k) * T < nt;
+        B0[so + (h + k) * SS] = v ? nsg * mv[k] : -FLT_MAX;
+        B1[so + (h + k) * SS] = v ? gv[k] : 0.f;
+      }
+    }
+    __syncthreads();
+    RSt Pk[RG_EPT];
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) Pk[k] = (i0 + k < nt) ? RSt{B0[q0 + k], B1[q0 + k], 0.f} : id;
+#pragma unroll
+    for (int k = 1; k < RG_EPT; ++k) Pk[k] = rcomb<RK_GLSE>(Pk[k - 1], Pk[k], tau2);
+    RSt v = Pk[RG_EPT - 1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      RSt w{__shfl_up_sync(0xffffffffu, v.m, o), __shfl_up_sync(0xffffffffu, v.s, o), 0.f};
+      if (lane >= o) v = rcomb<RK_GLSE>(w, v, tau2);
+    }
+    RSt ex{__shfl_up_sync(0xffffffffu, v.m, 1), __shfl_up_sync(0xffffffffu, v.s, 1), 0.f};
+    if (lane == 31) WP[warp] = v;
+    __syncthreads();
+    RSt cw = carry;
+#pragma unroll
+    for (int w = 0; w < UN_NW - 1; ++w)
+      if (w < warp) cw = rcomb<RK_GLSE>(cw, WP[w], tau2);
+    const RSt cin = lane > 0 ? rcomb<RK_GLSE>(cw, ex, tau2) : cw;
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) {
+      const RSt o = rcomb<RK_GLSE>(cin, Pk[k], tau2);
+      B0[q0 + k] = o.m;  // own slots
+      B1[q0 + k] = o.s;
+    }
+    {
+      RSt tile = WP[0];
+#pragma unroll
+      for (int w = 1; w < UN_NW; ++w) tile = rcomb<RK_GLSE>(tile, WP[w], tau2);
+      carry = rcomb<RK_GLSE>(carry, tile, tau2);
+    }
+    __syncthreads();
+    const int jb = c0 + tid;
+#pragma unroll
+    for (int h = 0; h < RG_EPT; h += 8) {
+      typename Ev<M_LSE, EK>::Raw r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (tid + (h + u) * T < nt) r[u] = ev.load(jb + (h + u) * T);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (tid + (h + u) * T < nt) {
+          const int j = jb + (h + u) * T;
+          const int sl = so + (h + u) * SS;
+          // S == 0 comes with m = -FLT_MAX or u_j + m <= 0: the product is an exact 0
+          const float g = B1[sl] * ex2f(tau2 * fmaf(sg, ev.value(j, r[u]), B0[sl]));
+          ev.grad(j, r[u], g);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 #define UNT_DISPATCH_EK(EKV, ...)      \
   if ((EKV) == EK_AFF1) {              \
     constexpr int EK = EK_AFF1;        \
@@ -137,6 +231,16 @@ bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   } else {
     UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_LSE, M_LSE, EK><<<grid, UNC::T, 0, st>>>(p)))
   }
+  count_launch();
+  err = cudaGetLastError();
+  return true;
+}
+
+// register-blocked untimed LSE backward (no masked_fill); false: not handled
+bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
+  if (p.fill || mode != M_LSE || p.L >= (1LL << 30)) return false;
+  const int ek = expr_kind(p.child);
+  UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
   count_launch();
   err = cudaGetLastError();
   return true;

@@ -102,5 +102,6 @@ bool reg_applicable(int mode, const FGParams& p, bool bwd);
 cudaError_t launch_reg_fwd(int mode, int ek, FGParams& p, cudaStream_t st);
 cudaError_t launch_reg_bwd(int mode, int ek, FGParams& p, cudaStream_t st);
 bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err);  // fg_unt.cu
+bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err);
 
 }  // namespace stlg

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
 // backward, LSE (gather form over outputs t; RK_GLSE)
 // ---------------------------------------------------------------------------
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_lse(const _
 // per-tile centre (keeps the final difference small).
 // ---------------------------------------------------------------------------
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_soft(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_soft(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
@@ -616,7 +616,7 @@ __device__ __forceinline__ RunSeg run_shfl_up(RunSeg v, int o) {
 }
 
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   constexpr int NOKEY = 0x7fffffff;  // windows past the tile: g = 0, key above every element

@@ -44,7 +44,8 @@ struct RC {
   static constexpr int N = T * RG_EPT;         // staged samples
   static constexpr int NP = N + N / 16;        // padded words per array
   static constexpr int SS = T + T / 16;        // padded stride of a strided sweep
-  static constexpr int MINB = 1024 / T;        // ~32 resident warps per SM
+  static constexpr int MINB = 1024 / T;        // ~32 resident warps per SM (forward kernels)
+  static constexpr int MINB_B = 65536 / (T * 72);  // backward kernels: ~72 registers (no spills)
 };
 
 __device__ __forceinline__ int rpad(int i) { return i + (i >> 4); }
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_fwd(const __gri
 // backward, LSE (gather form over outputs t; RK_GLSE)
 // ---------------------------------------------------------------------------
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_bwd_lse(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_lse(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_bwd_lse(const _
 // ends can be shared with neighbours (shared-memory atomic).
 // ---------------------------------------------------------------------------
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_bwd_hard(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
@@ -611,7 +612,17 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_bwd_hard(const 
 }
 
 // tile size: NW in [4, 8] warps (N = 512 NW samples) minimising staged samples per row
-inline int reg_pick_nw(long long L, int K, bool hard_bwd) {
+// Forward kernels run fastest at NW = 4 (smaller barrier groups, 8 resident CTAs)
+// even with more staged overlap (C2: 0.041 vs 0.043 ms at NW = 7); backward widths
+// minimise the staged samples per row.
+inline int reg_pick_nw(long long L, int K, bool hard_bwd, bool fwd = false) {
+  static int forced = -1;  // STLG_REG_NW=4..8: fixed tile width (A/B measurements)
+  if (forced < 0) {
+    const char* e = getenv("STLG_REG_NW");
+    forced = (e && e[0] >= '4' && e[0] <= '8') ? e[0] - '0' : 0;
+  }
+  if (forced && 512LL * forced >= 4LL * K) return forced;
+  if (fwd && 2048LL >= 4LL * K) return 4;
   int best = -1;
   long long best_cost = 0;
   for (int nw = 8; nw >= 4; --nw) {

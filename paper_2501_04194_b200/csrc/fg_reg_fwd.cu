@@ -51,7 +51,7 @@ static cudaError_t fwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
 
 cudaError_t launch_reg_fwd(int mode, int ek, FGParams& p, cudaStream_t st) {
   cudaError_t e;
-  REG_DISPATCH_NW(reg_pick_nw(p.L, p.K, false), e = fwd_nw<NW>(mode, ek, p, st))
+  REG_DISPATCH_NW(reg_pick_nw(p.L, p.K, false, mode != M_SOFT), e = fwd_nw<NW>(mode, ek, p, st))
   return e;
 }
 

@@ -774,6 +774,370 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
+// untimed LogSumExp Until in reciprocal form (non-fill)
+// ---------------------------------------------------------------------------
+// With S_k(t) = sum_{j=t..k} e^{-tau l_j} and E_k = e^{-tau r_k}, the reference's
+// incremental pm_k gives e^{-tau pm_k} = S_k, its two-element LSE-min gives
+// e^{tau term_k} = 1 / (S_k + E_k) =: 1 / D_k, and the outer LSE-max is
+//   out[t] = (1/tau) ln A_t,   A_t = sum_{k >= t} 1 / D_k(t)        (same function)
+// with the VJP
+//   d out / d r_k = E_k D_k^-2 / A_t,   d out / d l_j = e_j sum_{k >= j} D_k^-2 / A_t.
+// Still O(T^2) pairs, but one reciprocal per pair instead of the per-pair ex2 / lg2 of
+// the incremental form.  Columns come in chunks of 32 (one warp's share of a
+// 128-column stage): the chunk's fp64 prefix Q_k and B_k = Q_k + E_k are shared by
+// every output t before the chunk, D_k(t) = base_t + B_k with base_t = S over
+// [t, chunk start) (built by additions only: no cancellation), and each thread
+// evaluates its pairs in fp32 under a per-chunk power-of-two frame that puts its
+// largest terms at ~1 (smaller terms may flush: they are below 2^-100 of the sum).
+// A thread's own chunk is done exactly in fp64.  Rows whose values span more than
+// UL_RANGE log2 units (or hold non-finite values) run the per-pair kernels'
+// tile functions inside the same launch.
+constexpr int UL_T = 128;
+constexpr int UL_C = 32;
+constexpr float UL_RANGE = 400.f;
+
+struct UlStage {
+  double ex[UL_T], E[UL_T];  // e^{-tau l}, e^{-tau r} under the tile frame F
+  float bk[UL_T];            // B_k / 2^fmin
+  float rho[UL_T], eta[UL_T];  // E_k / B_k, e_k / B_k (backward)
+  double qtot[4], bmin[4];
+  int fmin[4];
+};
+
+__device__ __forceinline__ int ilogb_d(double x) { return (int)((__double2hiint(x) >> 20) & 0x7ff) - 1023; }
+__device__ __forceinline__ double pow2d(int e) { return __hiloint2double((e + 1023) << 20, 0); }
+__device__ __forceinline__ float pow2f(int e) {
+  if (e < -126) return 0.f;
+  return __int_as_float((min(e, 127) + 127) << 23);
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// tile frame F = max over [t0, L) of -tau2 l and -tau2 r; false: take the per-pair path
+__device__ __forceinline__ bool ul_frame(const UParams& p, long long row, long long t0, float& F, float* red) {
+  const float tau2 = p.mp.tau2;
+  float hi = -INFINITY, lo = INFINITY;
+  bool ok = true;
+  for (long long k = t0 + threadIdx.x; k < p.L; k += UL_T) {
+    const float u = -tau2 * expr_eval<M_LSE>(p.left, row, k, p.mp);
+    const float v = -tau2 * expr_eval<M_LSE>(p.right, row, k, p.mp);
+    ok = ok && isfinite(u) && isfinite(v);
+    hi = fmaxf(hi, fmaxf(u, v));
+    lo = fminf(lo, fminf(u, v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w] = hi;
+    red[4 + w] = lo;
+  }
+  ok = __syncthreads_and(ok);
+  hi = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  lo = fminf(fminf(red[4], red[5]), fminf(red[6], red[7]));
+  F = hi;
+  __syncthreads();
+  return ok && hi - lo <= UL_RANGE;
+}
+
+// one 128-column stage at k0: warp w builds chunk w
+template <bool BWD>
+__device__ __forceinline__ void ul_stage(const UParams& p, long long row, long long k0, float F, UlStage& S) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long k = k0 + tid;
+  const bool valid = k < p.L;
+  const float tau2 = p.mp.tau2;
+  double ex = 0.0, E = 0.0;
+  if (valid) {
+    ex = ex2d(fmaf(-tau2, expr_eval<M_LSE>(p.left, row, k, p.mp), -F));
+    E = ex2d(fmaf(-tau2, expr_eval<M_LSE>(p.right, row, k, p.mp), -F));
+  }
+  double qc = ex;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, qc, o);
+    if (lane >= o) qc += y;
+  }
+  const double B = qc + E;
+  double bm = valid ? B : INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bm = fmin(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+  const int fm = ilogb_d(bm);  // warp-uniform (unused when the whole chunk is past L)
+  S.ex[tid] = ex;
+  S.E[tid] = E;
+  S.bk[tid] = valid ? (float)fmin(B * pow2d(-fm), 3.0e38) : 3.0e38f;
+  if (BWD) {
+    S.rho[tid] = valid ? (float)(E / B) : 0.f;
+    S.eta[tid] = valid ? (float)(ex / B) : 0.f;
+  }
+  if (lane == 31) {
+    S.qtot[w] = qc;
+    S.bmin[w] = bm;
+    S.fmin[w] = fm;
+  }
+}
+
+// sum over the chunk of 1 / D_k(t), D = base + B (fp64 result, tile frame)
+__device__ __forceinline__ double ul_chunk_fwd(const UlStage& S, int c, int n, double base) {
+  const double den = base + S.bmin[c];
+  const int g = -ilogb_d(den);                 // den 2^g in [1, 2): every D 2^g >= 1
+  const float scale = pow2f(S.fmin[c] + g);    // <= 1
+  const float bb = (float)(base * pow2d(g));
+  const float* bk = S.bk + c * UL_C;
+  float s0 = 0.f, s1 = 0.f;
+  if (n == UL_C) {
+#pragma unroll
+    for (int j = 0; j < UL_C; j += 2) {
+      s0 += rcp_approx(fmaf(bk[j], scale, bb));
+      s1 += rcp_approx(fmaf(bk[j + 1], scale, bb));
+    }
+  } else {
+    for (int j = 0; j < n; ++j) s0 += rcp_approx(fmaf(bk[j], scale, bb));
+  }
+  return (double)(s0 + s1) * pow2d(g);
+}
+
+__global__ void __launch_bounds__(UL_T) k_until_unt_lse_fwd(const __grid_constant__ UParams p) {
+  __shared__ UlStage S;
+  __shared__ float red[8];
+  const long long row = blockIdx.y, t0 = (long long)blockIdx.x * UL_T;
+  float F;
+  if (!ul_frame(p, row, t0, F, red)) {
+    until_fwd_tile<M_LSE, false>(p, row, t0, nullptr);
+    return;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long L = p.L, t = t0 + tid;
+  double A = 0.0, base = 0.0;
+  for (long long k0 = t0; k0 < L; k0 += UL_T) {
+    __syncthreads();
+    ul_stage<false>(p, row, k0, F, S);
+    __syncthreads();
+    const bool diag = k0 == t0;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      const long long c0 = k0 + c * UL_C;
+      if (c0 >= L) break;
+      const int n = (int)min((long long)UL_C, L - c0);
+      if (diag && c == w) {  // the thread's own chunk, exactly
+        double s = 0.0;
+        for (int j = lane; j < n; ++j) {
+          s += S.ex[c * UL_C + j];
+          A += 1.0 / (s + S.E[c * UL_C + j]);
+        }
+        base = s;
+      } else if (!diag || c > w) {
+        A += ul_chunk_fwd(S, c, n, base);
+        base += S.qtot[c];
+      }
+    }
+  }
+  if (t < L) p.out[row * L + t] = (float)((log2(A) - (double)F) / (double)p.mp.tau2);
+}
+
+// 32 values per lane -> lane i holds the warp's sum of value i
+template <int S>
+__device__ __forceinline__ void rs_step(float (&v)[UL_C]) {
+  const bool up = threadIdx.x & S;
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const float send = up ? v[j] : v[j + S];
+    const float keep = up ? v[j + S] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, S);
+  }
+}
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[UL_C]) {
+  rs_step<16>(v);
+  rs_step<8>(v);
+  rs_step<4>(v);
+  rs_step<2>(v);
+  rs_step<1>(v);
+}
+
+// descending pass over one off-diagonal chunk: column sums of
+//   P_k = g E_k D_k^-2 / A  (-> d r_k),   Q_k = g e_k R_k / A,  R_k = sum_{k'>=k} D_k'^-2 (-> d l_k)
+// in the thread's frame g (the smallest D of this chunk and the tail at ~1); R
+// carried in fp64 across chunks (Rt64, frame gprev)
+__device__ __forceinline__ void ul_chunk_bwd(const UlStage& S, int c, int n, double base, double A, float gt,
+                                             double& dtail, double& Rt64, int& gprev, float* colP,
+                                             float* colQ) {
+  const int lane = threadIdx.x & 31;
+  const double den = base + S.bmin[c];
+  const double dmin = fmin(den, dtail);
+  const int g = -ilogb_d(dmin);
+  if (Rt64 != 0.0) Rt64 *= pow2d(-2 * (g - gprev));
+  gprev = g;
+  const float scale = pow2f(min(S.fmin[c] + g, 126));
+  const float bb = (float)(base * pow2d(g));
+  const float gl = (gt == 0.f) ? 0.f : (float)((double)gt * (pow2d(g) / A));
+  const float rt = (float)Rt64;
+  const float* bk = S.bk + c * UL_C;
+  const float* rho = S.rho + c * UL_C;
+  const float* eta = S.eta + c * UL_C;
+  float P[UL_C], Q[UL_C];
+  float rr = 0.f;
+#pragma unroll
+  for (int j = UL_C - 1; j >= 0; --j) {
+    if (j < n) {
+      const float t1 = fminf(bk[j] * scale, 0x1p120f);  // B_k in the frame
+      const float q = rcp_approx(t1 + bb);              // 1 / D_k
+      const float gq = gl * q;
+      P[j] = gq * (rho[j] * t1 * q);
+      rr = fmaf(q, q, rr);
+      Q[j] = gl * (eta[j] * t1) * (rt + rr);
+    } else {
+      P[j] = 0.f;
+      Q[j] = 0.f;
+    }
+  }
+  Rt64 += (double)rr;
+  dtail = dmin;
+  warp_reduce_scatter(P);
+  warp_reduce_scatter(Q);
+  atomicAdd(colP + c * UL_C + lane, P[0]);
+  atomicAdd(colQ + c * UL_C + lane, Q[0]);
+}
+
+// persistent grid; tiles that fail the range check run the per-pair backward with
+// its checkpoints in the global slab (same layout as k_until_bwd_g)
+__global__ void __launch_bounds__(UL_T) k_until_unt_lse_bwd(const __grid_constant__ UParams p, int ntx,
+                                                             long long ntiles) {
+  extern __shared__ __align__(16) float dsm[];  // block buffer [U_CB_G][2][UL_T], then CQ[nch]
+  __shared__ UlStage S;
+  __shared__ float colP[UL_T], colQ[UL_T];
+  __shared__ float red[8];
+  const long long stride = (long long)gridDim.x * U_THREADS;
+  UScr scr{p.scratch, dsm, stride, (long long)blockIdx.x * U_THREADS + threadIdx.x, U_THREADS,
+           (int)threadIdx.x};
+  double* CQ = (double*)(dsm + U_CB_G * 2 * U_THREADS);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long L = p.L;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row = tile / ntx;
+    const long long t0 = (tile - row * ntx) * UL_T;
+    const long long t = t0 + tid;
+    const float gt = t < L ? p.cot[row * L + t] : 0.f;
+    if (!__syncthreads_or(gt != 0.f)) continue;
+    float F;
+    if (!ul_frame(p, row, t0, F, red)) {
+      until_bwd_tile<M_LSE, false, U_CB_G>(p, row, t0, nullptr, scr);
+      __syncthreads();
+      continue;
+    }
+    // ---- pass 1 (ascending): A_t, the thread's own-chunk sum, base after the first stage,
+    //      and the running chunk totals CQ (chunks of later stages)
+    double A = 0.0, base = 0.0, sown = 0.0, head = 0.0, X = 0.0;
+    int ci = 0;
+    for (long long k0 = t0; k0 < L; k0 += UL_T, ci += 4) {
+      __syncthreads();
+      ul_stage<false>(p, row, k0, F, S);
+      __syncthreads();
+      const bool diag = k0 == t0;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        const long long c0 = k0 + c * UL_C;
+        if (c0 >= L) break;
+        const int n = (int)min((long long)UL_C, L - c0);
+        if (tid == 0) {
+          CQ[ci + c] = X;
+          if (!diag) X += S.qtot[c];
+        }
+        if (diag && c == w) {
+          double s = 0.0;
+          for (int j = lane; j < n; ++j) {
+            s += S.ex[c * UL_C + j];
+            A += 1.0 / (s + S.E[c * UL_C + j]);
+          }
+          sown = s;
+          base = s;
+        } else if (!diag || c > w) {
+          A += ul_chunk_fwd(S, c, n, base);
+          base += S.qtot[c];
+        }
+      }
+      if (diag) head = base;
+    }
+    // ---- pass 2 (descending)
+    double dtail = INFINITY, Rt64 = 0.0;
+    int gprev = 0;
+    const int nstage = (int)((L - t0 + UL_T - 1) / UL_T);
+    float* gl_row = p.gl + row * L;
+    float* gr_row = p.gr + row * L;
+    for (int s = nstage - 1; s >= 0; --s) {
+      const long long k0 = t0 + (long long)s * UL_T;
+      __syncthreads();
+      ul_stage<true>(p, row, k0, F, S);
+      colP[tid] = 0.f;
+      colQ[tid] = 0.f;
+      __syncthreads();
+      const bool diag = s == 0;
+#pragma unroll 1
+      for (int c = 3; c >= 0; --c) {
+        const long long c0 = k0 + c * UL_C;
+        if (c0 >= L) continue;
+        if (diag && c < w) break;
+        const int n = (int)min((long long)UL_C, L - c0);
+        if (diag && c == w) {  // own chunk: exact fp64, tail R in the tile frame
+          double Rt = Rt64 * pow2d(2 * gprev);
+          const double cA = (gt == 0.f) ? 0.0 : (double)gt / A;
+          for (int k = n - 1; k >= 0; --k) {
+            float pv = 0.f, qv = 0.f;
+            if (k >= lane && cA != 0.0) {
+              double sk = 0.0;
+              for (int j = lane; j <= k; ++j) sk += S.ex[c * UL_C + j];
+              const double D = sk + S.E[c * UL_C + k];
+              const double w2 = 1.0 / (D * D);
+              Rt += w2;
+              pv = (float)(cA * S.E[c * UL_C + k] * w2);
+              qv = (float)(cA * S.ex[c * UL_C + k] * Rt);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              pv += __shfl_xor_sync(0xffffffffu, pv, o);
+              qv += __shfl_xor_sync(0xffffffffu, qv, o);
+            }
+            if (lane == 0) {  // other warps add this chunk's off-diagonal sums concurrently
+              atomicAdd(colP + c * UL_C + k, pv);
+              atomicAdd(colQ + c * UL_C + k, qv);
+            }
+          }
+          continue;
+        }
+        double bc;
+        if (diag) {
+          bc = sown;
+          for (int cc = w + 1; cc < c; ++cc) bc += S.qtot[cc];
+        } else {
+          bc = head + CQ[4 * s + c];
+        }
+        ul_chunk_bwd(S, c, n, bc, A, gt, dtail, Rt64, gprev, colP, colQ);
+      }
+      __syncthreads();
+      const long long k = k0 + tid;
+      if (k < L) {
+        if (colP[tid] != 0.f) atomicAdd(gr_row + k, colP[tid]);
+        if (colQ[tid] != 0.f) atomicAdd(gl_row + k, colQ[tid]);
+      }
+    }
+  }
+}
+
+static bool ul_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("STLG_UL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 template <typename KernT>
@@ -834,6 +1198,11 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((p.L + U_THREADS - 1) / U_THREADS), (unsigned)p.B);
+  if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled()) {
+    k_until_unt_lse_fwd<<<grid, UL_T, 0, st>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
   size_t smem = fwd_smem(p);
   if (smem <= 64 * 1024) {
     cudaError_t e = set_smem_u(k_until_fwd<MODE>, smem);
@@ -857,7 +1226,14 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if ((e = cudaMemsetAsync(p.gl, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.gr, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
-  if (bwd_uses_smem(p) || MODE == M_HARD) {
+  const size_t ul_smem = (size_t)U_CB_G * 2 * U_THREADS * 4 + (size_t)(ntx * 4 + 4) * sizeof(double);
+  if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled() && p.scratch != nullptr && ul_smem <= kUSmemMax) {
+    if ((e = set_smem_u(k_until_unt_lse_bwd, ul_smem)) != cudaSuccess) return e;
+    const long long ntiles = (long long)ntx * p.B;
+    long long grid = (long long)until_sm_count() * U_PERSIST_PER_SM;
+    if (grid > ntiles) grid = ntiles;
+    k_until_unt_lse_bwd<<<(unsigned)grid, UL_T, ul_smem, st>>>(p, ntx, ntiles);
+  } else if (bwd_uses_smem(p) || MODE == M_HARD) {
     size_t smem = (MODE == M_HARD) ? fwd_smem(p) : bwd_smem(p);
     if (smem <= kUSmemMax) {
       if ((e = set_smem_u(k_until_bwd<MODE>, smem)) != cudaSuccess) return e;

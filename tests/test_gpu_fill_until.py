@@ -83,3 +83,54 @@ def test_untimed_lse_until_long_signal(cuda):
     assert rel_err(tr, ref_tr) <= 1e-5
     for k in ("x", "y"):
         assert rel_err(g[k], ref_g[k]) <= 1e-5, k
+
+
+@pytest.mark.parametrize("T", [1, 2, 31, 32, 33, 127, 128, 129, 161, 300, 513])
+@pytest.mark.parametrize("tau", [1.0, 10.0])
+def test_untimed_lse_until_ragged(cuda, T, tau):
+    """Untimed LSE Until (reciprocal-form kernels, csrc/until.cu) at lengths around the
+    32-column chunks and 128-output tiles, AR(1) and iid rows, signed cotangents."""
+    P = cuda
+    orc = _oracle()
+    rng = np.random.default_rng(T * 7 + int(tau))
+    B = 3
+    x = rng.normal(0, 1, (B, T))
+    x[1] = np.cumsum(0.3 * rng.normal(0, 1, T))
+    y = rng.normal(0, 1, (B, T))
+    x = np.asarray(x, dtype=np.float32).astype(np.float64)
+    y = np.asarray(y, dtype=np.float32).astype(np.float64)
+    f = P.Until(P.Pred("x", ">", 0.2), P.Pred("y", "<", 0.5))
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(tau))
+    cot = rng.normal(0, 1, (B, T))
+    tr, g, _ = run_device(f, {"x": x, "y": y}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x, "y": y}, cfg, cot)
+    assert rel_err(tr, ref_tr) <= 1e-5
+    for k in ("x", "y"):
+        assert rel_err(g[k], ref_g[k]) <= 1e-5, k
+
+
+def test_untimed_lse_until_wide_range_rows(cuda):
+    """Rows whose values span more than the reciprocal form's 400 log2 units take the
+    per-pair path inside the same launch; mixed with narrow rows and with tiles whose
+    cotangent is zero (skipped)."""
+    P = cuda
+    orc = _oracle()
+    T = 700
+    rng = np.random.default_rng(77)
+    x = rng.normal(0, 1, (4, T))
+    y = rng.normal(0, 1, (4, T))
+    x[1] *= 8.0  # tau2 * range > 400 at tau = 10 (fp32 inputs of this size carry ~1e-5 anyway)
+    y[2] = np.linspace(-30, 30, T)
+    x = np.asarray(x, dtype=np.float32).astype(np.float64)
+    y = np.asarray(y, dtype=np.float32).astype(np.float64)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0))
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(10.0))
+    cot = rng.normal(0, 1, (4, T))
+    cot[3, 128:384] = 0.0
+    cot[0, :] = 0.0
+    cot[0, 5] = 1.0
+    tr, g, _ = run_device(f, {"x": x, "y": y}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x, "y": y}, cfg, cot)
+    assert rel_err(tr, ref_tr) <= 1e-5
+    for k in ("x", "y"):
+        assert rel_err(g[k], ref_g[k]) <= 1e-5, k

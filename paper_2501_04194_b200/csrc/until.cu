@@ -795,6 +795,9 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
 constexpr int UL_T = 128;
 constexpr int UL_C = 32;
 constexpr float UL_RANGE = 400.f;
+#ifndef UL_MINB
+#define UL_MINB 3  // backward: 168 registers, no spills (the default 128 spills)
+#endif
 
 struct UlStage {
   double ex[UL_T], E[UL_T];  // e^{-tau l}, e^{-tau r} under the tile frame F
@@ -942,22 +945,24 @@ __global__ void __launch_bounds__(UL_T) k_until_unt_lse_fwd(const __grid_constan
 }
 
 // 32 values per lane -> lane i holds the warp's sum of value i
-template <int S>
-__device__ __forceinline__ void rs_step(float (&v)[UL_C]) {
-  const bool up = threadIdx.x & S;
+// column sums of a warp's 32 x 32 block through a padded shared transpose (row
+// stride 36 floats: conflict-free 128-bit row stores and column loads); lane i
+// returns the sum of value i over the warp
+__device__ __forceinline__ float warp_colsum(const float (&v)[UL_C], float* buf) {
+  const int lane = threadIdx.x & 31;
+  float* rowp = buf + lane * 36;
 #pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const float send = up ? v[j] : v[j + S];
-    const float keep = up ? v[j + S] : v[j];
-    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, S);
+  for (int m = 0; m < UL_C / 4; ++m)
+    *reinterpret_cast<float4*>(rowp + 4 * m) = make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+  __syncwarp();
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int l = 0; l < 32; l += 2) {
+    s0 += buf[l * 36 + lane];
+    s1 += buf[(l + 1) * 36 + lane];
   }
-}
-__device__ __forceinline__ void warp_reduce_scatter(float (&v)[UL_C]) {
-  rs_step<16>(v);
-  rs_step<8>(v);
-  rs_step<4>(v);
-  rs_step<2>(v);
-  rs_step<1>(v);
+  __syncwarp();
+  return s0 + s1;
 }
 
 // descending pass over one off-diagonal chunk: column sums of
@@ -966,7 +971,7 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[UL_C]) {
 // carried in fp64 across chunks (Rt64, frame gprev)
 __device__ __forceinline__ void ul_chunk_bwd(const UlStage& S, int c, int n, double base, double A, float gt,
                                              double& dtail, double& Rt64, int& gprev, float* colP,
-                                             float* colQ) {
+                                             float* colQ, float* wbuf) {
   const int lane = threadIdx.x & 31;
   const double den = base + S.bmin[c];
   const double dmin = fmin(den, dtail);
@@ -982,33 +987,49 @@ __device__ __forceinline__ void ul_chunk_bwd(const UlStage& S, int c, int n, dou
   const float* eta = S.eta + c * UL_C;
   float P[UL_C], Q[UL_C];
   float rr = 0.f;
+  auto pair = [&](int j, float b, float r, float e) {
+    const float t1 = fminf(b * scale, 0x1p120f);  // B_k in the frame
+    const float q = rcp_approx(t1 + bb);          // 1 / D_k
+    const float gq = gl * q;
+    P[j] = gq * (r * t1 * q);
+    rr = fmaf(q, q, rr);
+    Q[j] = gl * (e * t1) * (rt + rr);
+  };
+  if (n == UL_C) {
 #pragma unroll
-  for (int j = UL_C - 1; j >= 0; --j) {
-    if (j < n) {
-      const float t1 = fminf(bk[j] * scale, 0x1p120f);  // B_k in the frame
-      const float q = rcp_approx(t1 + bb);              // 1 / D_k
-      const float gq = gl * q;
-      P[j] = gq * (rho[j] * t1 * q);
-      rr = fmaf(q, q, rr);
-      Q[j] = gl * (eta[j] * t1) * (rt + rr);
-    } else {
-      P[j] = 0.f;
-      Q[j] = 0.f;
+    for (int m = UL_C / 4 - 1; m >= 0; --m) {
+      const float4 b4 = reinterpret_cast<const float4*>(bk)[m];
+      const float4 r4 = reinterpret_cast<const float4*>(rho)[m];
+      const float4 e4 = reinterpret_cast<const float4*>(eta)[m];
+      pair(4 * m + 3, b4.w, r4.w, e4.w);
+      pair(4 * m + 2, b4.z, r4.z, e4.z);
+      pair(4 * m + 1, b4.y, r4.y, e4.y);
+      pair(4 * m, b4.x, r4.x, e4.x);
+    }
+  } else {
+#pragma unroll
+    for (int j = UL_C - 1; j >= 0; --j) {
+      if (j < n) {
+        pair(j, bk[j], rho[j], eta[j]);
+      } else {
+        P[j] = 0.f;
+        Q[j] = 0.f;
+      }
     }
   }
   Rt64 += (double)rr;
   dtail = dmin;
-  warp_reduce_scatter(P);
-  warp_reduce_scatter(Q);
-  atomicAdd(colP + c * UL_C + lane, P[0]);
-  atomicAdd(colQ + c * UL_C + lane, Q[0]);
+  atomicAdd(colP + c * UL_C + lane, warp_colsum(P, wbuf));
+  atomicAdd(colQ + c * UL_C + lane, warp_colsum(Q, wbuf));
 }
 
 // persistent grid; tiles that fail the range check run the per-pair backward with
 // its checkpoints in the global slab (same layout as k_until_bwd_g)
-__global__ void __launch_bounds__(UL_T) k_until_unt_lse_bwd(const __grid_constant__ UParams p, int ntx,
+__global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __grid_constant__ UParams p, int ntx,
                                                              long long ntiles) {
-  extern __shared__ __align__(16) float dsm[];  // block buffer [U_CB_G][2][UL_T], then CQ[nch]
+  // block buffer of the per-pair fallback [U_CB_G][2][UL_T] (the fast path's per-warp
+  // transpose tiles [4][32][36] when the tile takes the fast path), then CQ[nch]
+  extern __shared__ __align__(16) float dsm[];
   __shared__ UlStage S;
   __shared__ float colP[UL_T], colQ[UL_T];
   __shared__ float red[8];
@@ -1116,7 +1137,7 @@ __global__ void __launch_bounds__(UL_T) k_until_unt_lse_bwd(const __grid_constan
         } else {
           bc = head + CQ[4 * s + c];
         }
-        ul_chunk_bwd(S, c, n, bc, A, gt, dtail, Rt64, gprev, colP, colQ);
+        ul_chunk_bwd(S, c, n, bc, A, gt, dtail, Rt64, gprev, colP, colQ, dsm + w * (32 * 36));
       }
       __syncthreads();
       const long long k = k0 + tid;
@@ -1230,7 +1251,11 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled() && p.scratch != nullptr && ul_smem <= kUSmemMax) {
     if ((e = set_smem_u(k_until_unt_lse_bwd, ul_smem)) != cudaSuccess) return e;
     const long long ntiles = (long long)ntx * p.B;
-    long long grid = (long long)until_sm_count() * U_PERSIST_PER_SM;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_until_unt_lse_bwd, UL_T, ul_smem) != cudaSuccess ||
+        occ <= 0)
+      occ = 1;
+    long long grid = (long long)until_sm_count() * min(occ, U_PERSIST_PER_SM);
     if (grid > ntiles) grid = ntiles;
     k_until_unt_lse_bwd<<<(unsigned)grid, UL_T, ul_smem, st>>>(p, ntx, ntiles);
   } else if (bwd_uses_smem(p) || MODE == M_HARD) {

@@ -119,8 +119,8 @@ def test_untimed_lse_until_wide_range_rows(cuda):
     rng = np.random.default_rng(77)
     x = rng.normal(0, 1, (4, T))
     y = rng.normal(0, 1, (4, T))
-    x[1] *= 8.0  # tau2 * range > 400 at tau = 10 (fp32 inputs of this size carry ~1e-5 anyway)
-    y[2] = np.linspace(-30, 30, T)
+    x[1] = np.cumsum(0.2 * x[1])
+    y[2] = np.linspace(-30, 30, T)  # tau2 * range ~ 870 log2 units > 400: per-pair path
     x = np.asarray(x, dtype=np.float32).astype(np.float64)
     y = np.asarray(y, dtype=np.float32).astype(np.float64)
     f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0))

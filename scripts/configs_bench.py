@@ -78,7 +78,11 @@ def modes_of(names):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="comma-separated configs, e.g. C2,C4")
     a = ap.parse_args()
+
+    def want(c):
+        return not a.only or c in a.only.split(",")
     g = torch.Generator(device=dev).manual_seed(0)
 
     def randn(B, T):
@@ -86,7 +90,7 @@ def main():
 
     # C1: Always[0,50](x > 0.5), Hard (reference CPU case) and the same formula at B=1024, T=10k
     f1 = P.Always(P.Pred("x", ">", 0.5), P.StepInterval(0, 50))
-    for B, T in ((1, 1000), (1024, 10_000)):
+    for B, T in ((1, 1000), (1024, 10_000)) if want("C1") else ():
         comp = compile_formula(f1, ["x"], P.SemanticsConfig(mode=P.Hard()))
         fm, bm = timed(comp, {"x": randn(B, T)}, B, T)
         emit("C1", "hard", B, T, fm, bm, alg_bytes_per_unit=16)
@@ -97,7 +101,7 @@ def main():
     p = torch.tensor(np.asarray(rng.uniform(-1, 1, (B, 1, 2)) + np.cumsum(0.05 * rng.normal(0, 1, (B, T, 2)), 1),
                                 dtype=np.float32), device=dev)
     f2 = P.Eventually(P.NormPred(("px", "py"), "<", 0.5), P.StepInterval(10, 100))
-    for mname, m in modes_of(["lse10", "hard", "soft10"]):
+    for mname, m in modes_of(["lse10", "hard", "soft10"] if want("C2") else []):
         comp = compile_formula(f2, ["px", "py"], P.SemanticsConfig(mode=m))
         fm, bm = timed(comp, {"px": p[..., 0], "py": p[..., 1]}, B, T)
         emit("C2", mname, B, T, fm, bm, alg_bytes_per_unit=24)
@@ -107,7 +111,7 @@ def main():
     f3 = P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 200))),
                P.Until(P.Pred("y", "<", 1.0), P.Pred("z", ">", 0.0)))
     c3 = {"x": randn(B, T), "y": randn(B, T), "z": randn(B, T)}
-    for mname, m in modes_of(["hard", "lse10"]):
+    for mname, m in modes_of(["hard", "lse10"] if want("C3") else []):
         comp = compile_formula(f3, ["x", "y", "z"], P.SemanticsConfig(mode=m))
         fm, bm = timed(comp, c3, B, T, reps=3 if mname != "hard" else 5)
         emit("C3", mname, B, T, fm, bm)
@@ -118,11 +122,12 @@ def main():
     f4 = P.Always(P.Pred("x", ">", 0.0), si)
     comp = compile_formula(f4, ["x"], P.SemanticsConfig(mode=P.LogSumExp(5.0)))
     x4 = torch.cumsum(0.1 * randn(B, T), dim=1)
-    fm, bm = timed(comp, {"x": x4}, B, T, smooth=(si.a, si.b, si.c), reps=3)
-    emit("C4", "lse5", B, T, fm, bm, grads="x and (a, b, c)")
+    if want("C4"):
+        fm, bm = timed(comp, {"x": x4}, B, T, smooth=(si.a, si.b, si.c), reps=3)
+        emit("C4", "lse5", B, T, fm, bm, grads="x and (a, b, c)")
 
     # C5: long-horizon sweep (subset): F[0,100], untimed F, U[0,100], untimed U; Hard / LSE(10)
-    Ts = (1_000, 10_000, 100_000) if not a.quick else (10_000,)
+    Ts = ((1_000, 10_000, 100_000) if not a.quick else (10_000,)) if want("C5") else ()
     for T in Ts:
         B = min(16384, int(1.6e9 // (2 * T)), 4096)
         xs = {"x": randn(B, T), "y": randn(B, T)}

@@ -29,6 +29,26 @@ constexpr int S_RP = 8;     // rows per CTA in the d/dw pass
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+// fold a group of n log2-scores v[] with group max gm (>= m) into (m, s):
+// s <- s 2^(m - gm) + sum 2^(v_i - gm).  NaN scores propagate through the sum
+// (fmaxf drops them from gm), -inf scores add 0, an all -inf state stays (-inf, 0).
+__device__ __forceinline__ void lse_group(float& m, float& s, const float* v, int n, float gm) {
+  if (gm == -INFINITY) {  // empty state, no finite score: only a NaN can change s
+    float a = 0.f;
+    for (int i = 0; i < n; ++i) a += ex2f(v[i]);
+    s += a;
+    return;
+  }
+  s *= ex2f(m - gm);  // m = -inf (empty state) -> 0
+  m = gm;
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < n; i += 2) {
+    a0 += ex2f(v[i] - gm);
+    a1 += ex2f(v[i + 1] - gm);
+  }
+  s += a0 + a1;
+}
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SParams p) {
   __shared__ float U[S_T + S_CH];
@@ -40,7 +60,8 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
   const float sg = p.sg, tau2 = p.mp.tau2;
   const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
   const int t = t0 + threadIdx.x;
-  float m = -INFINITY, s = 0.f, d = 0.f, u0 = 0.f;
+  float m = -INFINITY, s = 0.f, uc = 0.f;
+  double S64 = 0.0, D64 = 0.0;  // softmax running sums
   bool first = true;
   for (int k0 = 0; k0 < K; k0 += S_CH) {
     const int kc = min(S_CH, K - k0);
@@ -51,44 +72,81 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
     }
     for (int q = threadIdx.x; q < kc; q += S_T) LW[q] = p.lw2[p.i_lo + k0 + q];
     __syncthreads();
-    if (t < L) {
-      for (int k = 0; k < kc; ++k) {
-        float u = U[threadIdx.x + k];
-        float v = fmaf(tau2, u, LW[k]);  // log2 of w_i e^{tau u}
-        if (first) {
-          m = v;
-          s = 1.f;
-          u0 = u;
-          d = 0.f;
-          first = false;
+    if (MODE == M_LSE && t < L) {
+      // groups of SG offsets: scores to registers, one max, one rescale of s,
+      // then one ex2 + add per pair (~6 issue slots per pair instead of ~10 for
+      // the per-pair online update: the loop is MUFU-bound, not issue-bound)
+      constexpr int SG = 32;
+      int k = 0;
+      for (; k + SG <= kc; k += SG) {
+        float v[SG];
+        float gm = m;
+#pragma unroll
+        for (int i = 0; i < SG; ++i) {
+          v[i] = fmaf(tau2, U[threadIdx.x + k + i], LW[k + i]);
+          gm = fmaxf(gm, v[i]);
+        }
+        lse_group(m, s, v, SG, gm);
+      }
+      if (k < kc) {
+        float v[SG];
+        float gm = m;
+#pragma unroll
+        for (int i = 0; i < SG; ++i) {
+          v[i] = (k + i < kc) ? fmaf(tau2, U[threadIdx.x + k + i], LW[k + i]) : -INFINITY;
+          gm = fmaxf(gm, v[i]);
+        }
+        lse_group(m, s, v, SG, gm);
+      }
+      first = false;
+    } else if (MODE != M_LSE && t < L) {
+      // softmax: the same groups; the payload sum D = sum e (u - uc) uses a fixed
+      // centre uc (no re-centering when the max moves), group partials in fp32 and
+      // the running (S, D) in fp64: only SG terms ever meet in one fp32 sum
+      constexpr int SG = 32;
+      if (first) {
+        uc = U[threadIdx.x];
+        first = false;
+      }
+      for (int k = 0; k < kc; k += SG) {
+        float v[SG];
+        float gm = m;
+#pragma unroll
+        for (int i = 0; i < SG; ++i) {
+          v[i] = (k + i < kc) ? fmaf(tau2, U[threadIdx.x + k + i], LW[k + i]) : -INFINITY;
+          gm = fmaxf(gm, v[i]);
+        }
+        if (gm == -INFINITY) {  // empty state, no finite score: only a NaN can change S
+          float a = 0.f;
+          for (int i = 0; i < SG; ++i) a += ex2f(v[i]);
+          S64 += a;
           continue;
         }
-        if (MODE == M_LSE) {
-          lse_add(m, s, v, 1.f);
-        } else {
-          // online softmax; payload centred on the current top-scoring sample u0
-          float dv = v - m;
-          float e = ex2f(-fabsf(dv));
-          bool up = dv > 0.f;
-          float du = u - u0;
-          float s_up = fmaf(s, e, 1.f), d_up = e * fmaf(-du, s, d);
-          float s_dn = s + e, d_dn = fmaf(du, e, d);
-          s = up ? s_up : s_dn;
-          d = up ? d_up : d_dn;
-          u0 = up ? u : u0;
-          m = up ? v : m;
+        const double sc = (double)ex2f(m - gm);
+        m = gm;
+        float gs0 = 0.f, gs1 = 0.f, gd0 = 0.f, gd1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < SG; i += 2) {
+          const float e0 = ex2f(v[i] - gm), e1 = ex2f(v[i + 1] - gm);
+          const float d0 = (k + i < kc) ? U[threadIdx.x + k + i] - uc : 0.f;
+          const float d1 = (k + i + 1 < kc) ? U[threadIdx.x + k + i + 1] - uc : 0.f;
+          gs0 += e0;
+          gs1 += e1;
+          gd0 = fmaf(e0, d0, gd0);
+          gd1 = fmaf(e1, d1, gd1);
         }
+        S64 = fma(S64, sc, (double)(gs0 + gs1));
+        D64 = fma(D64, sc, (double)(gd0 + gd1));
       }
     }
     __syncthreads();
   }
   if (t < L) {
-    float lse = (m + lg2f(s)) * p.mp.inv_tau2;  // log(sum w e^{tau u}) / tau, u units
     if (MODE == M_LSE) {
-      p.out[row * L + t] = sg * lse;
+      p.out[row * L + t] = sg * ((m + lg2f(s)) * p.mp.inv_tau2);  // log(sum w e^{tau u}) / tau
     } else {
-      p.out[row * L + t] = sg * (u0 + d / s);
-      p.aux[row * L + t] = lse;
+      p.out[row * L + t] = sg * (uc + (float)(D64 / S64));
+      p.aux[row * L + t] = (m + lg2f((float)S64)) * p.mp.inv_tau2;
     }
   }
 }
@@ -121,17 +179,36 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
   for (int k0 = 0; k0 < K; k0 += S_CH) {
     const int kc = min(S_CH, K - k0);
     const int tlo = j0 - p.i_lo - k0 - (kc - 1);
+    int allnz = 1;
     for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) {
       int tt = tlo + q;
       bool v = tt >= 0 && tt < L;
       float g = v ? cot[tt] : 0.f;
+      allnz &= (g != 0.f) | !v;
       Gt[q] = g;
-      Mt[q] = (v && g != 0.f) ? sg * outr[tt] : 0.f;
+      // LSE: a staged M of +inf turns an out-of-range t into a 0 weight (branch-free path)
+      Mt[q] = (v && g != 0.f) ? sg * outr[tt] : (MODE == M_LSE ? INFINITY : 0.f);
       if (MODE == M_SOFT) Lt[q] = (v && g != 0.f) ? p.aux_in[row * L + tt] : 0.f;
     }
     for (int q = threadIdx.x; q < kc; q += S_T) LW[q] = p.lw2[p.i_lo + k0 + q];
-    __syncthreads();
-    if (j <= jmax) {
+    // dense cotangent over the staged range (e.g. the trace-mode ones seed):
+    // no per-pair zero test, 4 issue slots + 2 loads per pair
+    const int dense = __syncthreads_and(allnz);
+    if (MODE == M_LSE && dense && fabsf(uj) < INFINITY) {  // (an infinite u_j takes the exact path)
+      if (j <= jmax) {
+        float a0 = 0.f, a1 = 0.f;
+        const float* gq = Gt + threadIdx.x + kc - 1;
+        const float* mq = Mt + threadIdx.x + kc - 1;
+        int k = 0;
+#pragma unroll 8
+        for (; k + 1 < kc; k += 2) {
+          a0 = fmaf(gq[-k], ex2f(fmaf(tau2, uj - mq[-k], LW[k])), a0);
+          a1 = fmaf(gq[-k - 1], ex2f(fmaf(tau2, uj - mq[-k - 1], LW[k + 1])), a1);
+        }
+        if (k < kc) a0 = fmaf(gq[-k], ex2f(fmaf(tau2, uj - mq[-k], LW[k])), a0);
+        acc += a0 + a1;
+      }
+    } else if (j <= jmax) {
       // t = j - i_lo - k0 - k  ->  index into the staged range: (kc - 1 - k) + threadIdx.x
       for (int k = 0; k < kc; ++k) {
         int q = threadIdx.x + kc - 1 - k;
@@ -172,7 +249,9 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SParams p) {
   __shared__ float U[S_T + S_CH];
-  __shared__ float Gt[S_T], Mt[S_T], Lt[S_T];
+  __shared__ __align__(16) float Gt[S_T];
+  __shared__ __align__(16) float Mt[S_T];
+  __shared__ float Lt[S_T];
   const int L = (int)p.L;
   const int t0 = blockIdx.x * S_T;
   const int K = p.i_hi - p.i_lo + 1;
@@ -183,9 +262,9 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
   for (int k0 = 0; k0 < K; k0 += S_CH) {
     const int kc = min(S_CH, K - k0);
     // each thread owns offsets i = i_lo + k0 + k, k = threadIdx.x + S_T * c
-    float acc[S_CH / S_T];
+    double acc[S_CH / S_T];  // per-row tile partials (<= 256 terms) meet in fp64
 #pragma unroll
-    for (int c = 0; c < S_CH / S_T; ++c) acc[c] = 0.f;
+    for (int c = 0; c < S_CH / S_T; ++c) acc[c] = 0.0;
     for (long long row = r0; row < r1; ++row) {
       const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
       const int base = t0 + p.i_lo + k0;
@@ -193,6 +272,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
         int idx = base + q;
         U[q] = sg * (idx < L ? expr_eval<MODE>(p.child, row, idx, p.mp) : padv);
       }
+      int nz = 1;
       if (threadIdx.x < S_T) {
         int tt = t0 + threadIdx.x;
         bool v = tt < L;
@@ -200,13 +280,30 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
         Gt[threadIdx.x] = g;
         Mt[threadIdx.x] = v ? sg * p.out_in[row * L + tt] : 0.f;
         Lt[threadIdx.x] = (MODE == M_SOFT && v) ? p.aux_in[row * L + tt] : 0.f;
+        nz = (g != 0.f) | !v;
       }
-      __syncthreads();
+      // dense cotangent row tile: no per-pair zero test, (G, M) read 4 at a time
+      const int dense = __syncthreads_and(nz);
 #pragma unroll
       for (int c = 0; c < S_CH / S_T; ++c) {
         int k = threadIdx.x + S_T * c;
         if (k >= kc) break;
         float a = 0.f;
+        if (MODE == M_LSE && dense) {
+          float a1 = 0.f;
+          int q = 0;
+          for (; q + 4 <= nt; q += 4) {
+            const float4 g4 = *reinterpret_cast<const float4*>(Gt + q);
+            const float4 m4 = *reinterpret_cast<const float4*>(Mt + q);
+            a = fmaf(g4.x, ex2f(tau2 * (U[q + k] - m4.x)), a);
+            a1 = fmaf(g4.y, ex2f(tau2 * (U[q + k + 1] - m4.y)), a1);
+            a = fmaf(g4.z, ex2f(tau2 * (U[q + k + 2] - m4.z)), a);
+            a1 = fmaf(g4.w, ex2f(tau2 * (U[q + k + 3] - m4.w)), a1);
+          }
+          for (; q < nt; ++q) a = fmaf(Gt[q], ex2f(tau2 * (U[q + k] - Mt[q])), a);
+          acc[c] += (double)a + (double)a1;
+          continue;
+        }
         for (int q = 0; q < nt; ++q) {
           float g = Gt[q];
           if (g == 0.f) continue;
@@ -214,7 +311,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
           if (MODE == M_LSE) a = fmaf(g, ex2f(tau2 * (u - Mt[q])), a);
           else a = fmaf(g * ex2f(tau2 * (u - Lt[q])), u - Mt[q], a);
         }
-        acc[c] += a;
+        acc[c] += (double)a;
       }
       __syncthreads();
     }
@@ -224,7 +321,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       if (k >= kc) break;
       int i = p.i_lo + k0 + k;
       if (p.lw2[i] == -INFINITY) continue;
-      double v = (double)(sg * acc[c]) * (MODE == M_LSE ? (double)itau : 1.0);
+      double v = (double)sg * acc[c] * (MODE == M_LSE ? (double)itau : 1.0);
       if (v != 0.0) atomicAdd(p.dw64 + i, v);
     }
   }

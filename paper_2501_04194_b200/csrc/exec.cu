@@ -269,7 +269,7 @@ int validate_nodes(const stlg_node* nodes, int n, int n_ch, int n_smooth) {
 struct Bufs {
   float* slots;   // n_slots * B * T
   float* aux;     // n_aux * B * T
-  float* tables;  // n_tables * T (log2 smooth weights)
+  float* tables;  // n_tables * 2T (log2 smooth weights, log2 suffix sums)
   float* gslots;  // n_slots * B * T (backward)
   float* scratch; // 3 * B * T (backward)
   float* uslab;   // Until backward checkpoint slab (persistent kernel)
@@ -286,7 +286,7 @@ void fwd_layout(const stlg_plan* p, long long BT, size_t* slots_b, size_t* aux_b
   *aux_b = align256(sizeof(float) * (size_t)p->n_aux * BT);
 }
 size_t tables_bytes(const stlg_plan* p, long long T) {
-  return align256(sizeof(float) * (size_t)p->n_tables * (size_t)T);
+  return align256(sizeof(float) * 2 * (size_t)p->n_tables * (size_t)T);
 }
 
 // Smooth-interval weights on the host in fp64, exactly as the reference forms
@@ -296,8 +296,12 @@ double sigmoid_h(double z) {
   double ez = std::exp(z);
   return ez / (1.0 + ez);
 }
+// lw2[i] = log2 w_i (i < L), then lw2[L + m] = log2 sum_{i >= max(m, i_lo)} w_i, the
+// suffix sums the backward's padded-tail term uses (one O(T) pass per row instead of
+// a window loop per virtual pad position)
 bool smooth_table(const stlg_smooth& sp, long long L, std::vector<float>& lw2, int* i_lo, int* i_hi) {
-  lw2.assign((size_t)L, -INFINITY);
+  lw2.assign((size_t)(2 * L), -INFINITY);
+  std::vector<double> w64((size_t)L, 0.0);
   int lo = -1, hi = -1;
   const double Lf = (double)L;
   for (long long i = 0; i < L; ++i) {
@@ -306,9 +310,15 @@ bool smooth_table(const stlg_smooth& sp, long long L, std::vector<float>& lw2, i
     double w = a - b - sp.eps;
     if (w > 0) {
       lw2[(size_t)i] = (float)std::log2(w);
+      w64[(size_t)i] = w;
       if (lo < 0) lo = (int)i;
       hi = (int)i;
     }
+  }
+  double suf = 0.0;
+  for (long long m = L - 1; m >= 0; --m) {
+    suf += w64[(size_t)m];
+    lw2[(size_t)(L + m)] = suf > 0.0 ? (float)std::log2(suf) : -INFINITY;
   }
   *i_lo = lo;
   *i_hi = hi;
@@ -587,8 +597,8 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
   int i_lo, i_hi;
   if (!smooth_table(sp, T, lw2, &i_lo, &i_hi))
     return fail(STLG_E_EMPTY_WINDOW, "smooth interval produced an all-zero weight vector");
-  float* tab = bf.tables + (size_t)e.table * (size_t)T;
-  cudaError_t ce = cudaMemcpyAsync(tab, lw2.data(), sizeof(float) * (size_t)T,
+  float* tab = bf.tables + (size_t)e.table * 2 * (size_t)T;
+  cudaError_t ce = cudaMemcpyAsync(tab, lw2.data(), sizeof(float) * 2 * (size_t)T,
                                    cudaMemcpyHostToDevice, st);
   int rc;
   if ((rc = cuda_status(ce, "weight upload"))) return rc;

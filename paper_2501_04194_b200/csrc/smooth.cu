@@ -161,17 +161,15 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
   __shared__ float Mt[S_T + S_CH];
   __shared__ float Lt[(MODE == M_SOFT) ? S_T + S_CH : 1];
   __shared__ float LW[S_CH];
-  __shared__ float red[S_T / 32];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
   const int j0 = blockIdx.x * S_T;
   const int K = p.i_hi - p.i_lo + 1;
   const float sg = p.sg, tau2 = p.mp.tau2, tau = p.mp.tau;
   const int j = j0 + threadIdx.x;
-  const int jmax = L - 1 + p.i_hi;  // last position any window reaches
-  const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+  const int jmax = L - 1;  // real positions only (virtual pad positions: k_smooth_bwd_pad)
   float uj = 0.f;
-  if (j <= jmax) uj = sg * (j < L ? expr_eval<MODE>(p.child, row, j, p.mp) : padv);
+  if (j <= jmax) uj = sg * expr_eval<MODE>(p.child, row, j, p.mp);
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
   float acc = 0.f;
@@ -229,15 +227,44 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
     if (j == L - 1) atomicAdd(gb + j, acc);
     else gb[j] = acc;
   }
-  // virtual pad positions: sum into c[L-1] ('last'); dropped for const padding
-  float v = (j >= L && j <= jmax && p.pad_last) ? acc : 0.f;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+}
+
+// ---------------------------------------------------------------------------
+// backward 1b ('last' padding): every virtual pad position j >= L holds the same
+// value u_pad and sums into c[L-1], so their total is, per output t,
+//   g_t * F_t * sum_{i >= max(L - t, i_lo)} w_i        (one term per t, lw2[L + m])
+// with F_t = 2^{tau2 (u_pad - M_t)} (LSE) or 2^{tau2 (u_pad - L_t)} (1 + tau (u_pad - M_t))
+// (softmax), both combined with the log2 suffix sum inside one ex2.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(S_T) k_smooth_bwd_pad(const __grid_constant__ SParams p) {
+  __shared__ float red[S_T / 32];
+  const long long row = blockIdx.x;
+  const int L = (int)p.L;
+  const float sg = p.sg, tau2 = p.mp.tau2, tau = p.mp.tau;
+  const float up = sg * expr_eval<MODE>(p.child, row, L - 1, p.mp);
+  const float* cot = p.cot + row * L;
+  const float* outr = p.out_in + row * L;
+  const float* lws = p.lw2 + L;
+  float acc = 0.f;
+  for (int t = max(0, L - p.i_hi) + (int)threadIdx.x; t < L; t += S_T) {
+    const float g = cot[t];
+    if (g == 0.f) continue;
+    const float ls = lws[max(L - t, p.i_lo)];
+    if (MODE == M_LSE) {
+      acc = fmaf(g, ex2f(fmaf(tau2, up - sg * outr[t], ls)), acc);
+    } else {
+      const float w = ex2f(fmaf(tau2, up - p.aux_in[row * L + t], ls));
+      acc = fmaf(g * w, fmaf(tau, up - sg * outr[t], 1.f), acc);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     float sum = 0.f;
     for (int w = 0; w < S_T / 32; ++w) sum += red[w];
-    if (sum != 0.f) atomicAdd(gb + (L - 1), sum);
+    if (sum != 0.f) atomicAdd(p.gbuf + row * L + (L - 1), sum);
   }
 }
 
@@ -392,12 +419,19 @@ cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st) {
 cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
-  long long span = p.L + p.i_hi;  // child positions incl. virtual pad positions
-  dim3 g1((unsigned)((span + S_T - 1) / S_T), (unsigned)p.B);
+  // real child positions only: the virtual pad positions (j >= L) are summed in
+  // closed form by k_smooth_bwd_pad ('last') or dropped (constant padding)
+  dim3 g1((unsigned)((p.L + S_T - 1) / S_T), (unsigned)p.B);
   if (mode == M_LSE) k_smooth_bwd_child<M_LSE><<<g1, S_T, 0, st>>>(p);
   else k_smooth_bwd_child<M_SOFT><<<g1, S_T, 0, st>>>(p);
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (p.pad_last) {
+    if (mode == M_LSE) k_smooth_bwd_pad<M_LSE><<<(unsigned)p.B, S_T, 0, st>>>(p);
+    else k_smooth_bwd_pad<M_SOFT><<<(unsigned)p.B, S_T, 0, st>>>(p);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   if (p.dw64 != nullptr) {
     dim3 g2((unsigned)((p.L + S_T - 1) / S_T), (unsigned)((p.B + S_RP - 1) / S_RP));
     if (mode == M_LSE) k_smooth_bwd_w<M_LSE><<<g2, S_T, 0, st>>>(p);

@@ -651,7 +651,7 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
   }
   if ((rc = cuda_status(launch_smooth_bwd(mode, p, st), "smooth backward launch"))) return rc;
   if (d_smooth) {
-    ce = launch_smooth_abc(dw64, T, sp.a, sp.b, sp.c, sp.eps, d_smooth + 3 * e.smooth_slot, st);
+    ce = launch_smooth_abc(dw64, tab, T, sp.a, sp.b, sp.c, sp.eps, d_smooth + 3 * e.smooth_slot, st);
     if ((rc = cuda_status(ce, "smooth d(a,b,c)"))) return rc;
   }
   return STLG_OK;

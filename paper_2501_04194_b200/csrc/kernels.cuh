@@ -67,8 +67,8 @@ struct SParams {
 };
 
 // fp64 weight table and its (a, b, c) partials -> d_abc (one smooth slot)
-cudaError_t launch_smooth_abc(const double* dw64, long long L, double a, double b, double c,
-                              double eps, double* d_abc, cudaStream_t st);
+cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,
+                              double c, double eps, double* d_abc, cudaStream_t st);
 
 // launchers (return cudaError_t)
 cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st);

@@ -269,8 +269,10 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_pad(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
-// backward 2: d out / d w_i summed over t and rows (thread per offset i)
-//   LSE:  exp(tau (u_{t+i} - M_t)) / tau        softmax: exp(tau (u - L_t)) (u - M_t)
+// backward 2: w_i * d out / d w_i summed over t and rows (thread per offset i)
+//   LSE:  w_i exp(tau (u_{t+i} - M_t)) / tau     softmax: w_i exp(tau (u - L_t)) (u - M_t)
+// (the weight rides inside the ex2 as log2 w_i: the bare derivative reaches 1e300 on
+// 1e-300 tail weights and overflows fp32; k_smooth_abc divides by the same 2^{lw2_i})
 // (zero where w_i == 0: the reference masks those entries before exp, tape.py:372)
 // ---------------------------------------------------------------------------
 template <int MODE>
@@ -290,8 +292,13 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
     const int kc = min(S_CH, K - k0);
     // each thread owns offsets i = i_lo + k0 + k, k = threadIdx.x + S_T * c
     double acc[S_CH / S_T];  // per-row tile partials (<= 256 terms) meet in fp64
+    float lwi[S_CH / S_T];   // log2 w_i of the thread's offsets, folded into every ex2
 #pragma unroll
-    for (int c = 0; c < S_CH / S_T; ++c) acc[c] = 0.0;
+    for (int c = 0; c < S_CH / S_T; ++c) {
+      acc[c] = 0.0;
+      const int k = threadIdx.x + S_T * c;
+      lwi[c] = k < kc ? p.lw2[p.i_lo + k0 + k] : -INFINITY;
+    }
     for (long long row = r0; row < r1; ++row) {
       const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
       const int base = t0 + p.i_lo + k0;
@@ -315,6 +322,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       for (int c = 0; c < S_CH / S_T; ++c) {
         int k = threadIdx.x + S_T * c;
         if (k >= kc) break;
+        const float lw = lwi[c];
         float a = 0.f;
         if (MODE == M_LSE && dense) {
           float a1 = 0.f;
@@ -322,12 +330,12 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
           for (; q + 4 <= nt; q += 4) {
             const float4 g4 = *reinterpret_cast<const float4*>(Gt + q);
             const float4 m4 = *reinterpret_cast<const float4*>(Mt + q);
-            a = fmaf(g4.x, ex2f(tau2 * (U[q + k] - m4.x)), a);
-            a1 = fmaf(g4.y, ex2f(tau2 * (U[q + k + 1] - m4.y)), a1);
-            a = fmaf(g4.z, ex2f(tau2 * (U[q + k + 2] - m4.z)), a);
-            a1 = fmaf(g4.w, ex2f(tau2 * (U[q + k + 3] - m4.w)), a1);
+            a = fmaf(g4.x, ex2f(fmaf(tau2, U[q + k] - m4.x, lw)), a);
+            a1 = fmaf(g4.y, ex2f(fmaf(tau2, U[q + k + 1] - m4.y, lw)), a1);
+            a = fmaf(g4.z, ex2f(fmaf(tau2, U[q + k + 2] - m4.z, lw)), a);
+            a1 = fmaf(g4.w, ex2f(fmaf(tau2, U[q + k + 3] - m4.w, lw)), a1);
           }
-          for (; q < nt; ++q) a = fmaf(Gt[q], ex2f(tau2 * (U[q + k] - Mt[q])), a);
+          for (; q < nt; ++q) a = fmaf(Gt[q], ex2f(fmaf(tau2, U[q + k] - Mt[q], lw)), a);
           acc[c] += (double)a + (double)a1;
           continue;
         }
@@ -335,8 +343,8 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
           float g = Gt[q];
           if (g == 0.f) continue;
           float u = U[q + k];
-          if (MODE == M_LSE) a = fmaf(g, ex2f(tau2 * (u - Mt[q])), a);
-          else a = fmaf(g * ex2f(tau2 * (u - Lt[q])), u - Mt[q], a);
+          if (MODE == M_LSE) a = fmaf(g, ex2f(fmaf(tau2, u - Mt[q], lw)), a);
+          else a = fmaf(g * ex2f(fmaf(tau2, u - Lt[q], lw)), u - Mt[q], a);
         }
         acc[c] += (double)a;
       }
@@ -364,14 +372,15 @@ __device__ __forceinline__ double sigmoid_d(double z) {
   return ez / (1.0 + ez);
 }
 
-__global__ void k_smooth_abc(const double* __restrict__ dw64, long long L, double a, double b,
-                             double c, double eps, double* d_abc) {
+__global__ void k_smooth_abc(const double* __restrict__ dw64, const float* __restrict__ lw2, long long L,
+                             double a, double b, double c, double eps, double* d_abc) {
   __shared__ double red[3][32];
   double da = 0, db = 0, dc = 0;
   const double Lf = (double)L;
   for (long long i = threadIdx.x; i < L; i += blockDim.x) {
     double g = dw64[i];
     if (g == 0.0) continue;
+    g /= exp2((double)lw2[i]);  // dw64 holds w_i d out / d w_i under the fp32 table weight
     double lo = sigmoid_d((i - a * Lf) * c);
     double hi = sigmoid_d((i - b * Lf) * c);
     if (!(lo - hi - eps > 0)) continue;  // relu gradient is 0 where the clamp is active
@@ -448,9 +457,9 @@ cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st) {
   return launch_pointwise_vjp(mode, q, p.gbuf, st);
 }
 
-cudaError_t launch_smooth_abc(const double* dw64, long long L, double a, double b, double c,
-                              double eps, double* d_abc, cudaStream_t st) {
-  k_smooth_abc<<<1, 1024, 0, st>>>(dw64, L, a, b, c, eps, d_abc);
+cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,
+                              double c, double eps, double* d_abc, cudaStream_t st) {
+  k_smooth_abc<<<1, 1024, 0, st>>>(dw64, lw2, L, a, b, c, eps, d_abc);
   count_launch();
   return cudaGetLastError();
 }

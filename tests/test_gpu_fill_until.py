@@ -8,6 +8,8 @@ numerically active in the smooth modes (the reference's documented hazard,
 core.py:260-265), so the sweep checks the sentinel algebra, not just its underflow.
 """
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -43,7 +45,8 @@ def _oracle():
 def test_masked_fill_until_vs_oracle(cuda, mode, iv, pad, sent, L):
     P = cuda
     orc = _oracle()
-    rng = np.random.default_rng(hash((mode, iv, pad, sent, L)) % 2**32)
+    # str hash() is salted per process (PYTHONHASHSEED): derive a stable seed instead
+    rng = np.random.default_rng(zlib.crc32(repr((mode, iv, pad, sent, L)).encode()))
     x = np.asarray(rng.normal(0, 1.5, (2, L)), dtype=np.float32).astype(np.float64)
     y = np.asarray(rng.normal(0.2, 1.5, (2, L)), dtype=np.float32).astype(np.float64)
     if mode == "hard":  # ties for the first-index rules

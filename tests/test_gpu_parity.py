@@ -265,21 +265,25 @@ def test_batch_beyond_one_launch_grid(cuda):
     assert torch.equal(gx[rows], gs)
 
 
+@pytest.mark.parametrize("pad", [P.PaddingPolicy.last_value(), P.PaddingPolicy.constant(0.75)],
+                         ids=["last", "const"])
 @pytest.mark.parametrize("zero_frac", [0.0, 0.5, 0.995])
 @pytest.mark.parametrize("mode", [P.LogSumExp(5.0), P.SoftMax(2.0)])
-def test_smooth_interval_cotangent_density(cuda, mode, zero_frac):
+def test_smooth_interval_cotangent_density(cuda, mode, zero_frac, pad):
     """Smooth-interval VJP with dense, half-sparse and nearly one-hot cotangents: the
     backward kernels switch per staged tile between a branch-free dense loop and the
-    zero-skipping loop (csrc/smooth.cu); both must match the oracle (masking.py:207-215)."""
+    zero-skipping loop (csrc/smooth.cu); both must match the oracle (masking.py:207-215).
+    'last' padding exercises the closed-form pad tail (k_smooth_bwd_pad), constant
+    padding the dropped virtual pad positions (masking.py:94-148)."""
     rng = np.random.default_rng(1234)
     B, L = 4, 1500
     if type(mode).__name__ == "LogSumExp":  # random walks, |x| up to ~10
         x = np.cumsum(np.asarray(rng.normal(0, 0.3, (B, L)), dtype=np.float32), axis=1).astype(np.float64)
-    else:  # softmax: iid N(0,1) (random walks: see DESIGN §11, softmax smooth-interval gradients)
+    else:  # softmax: iid N(0,1)
         x = np.asarray(rng.normal(0, 1, (B, L)), dtype=np.float32).astype(np.float64)
     si = P.SmoothInterval(0.2, 0.6, 9.0)
     f = P.Always(P.Pred("x", ">", 0.0), si)
-    cfg = P.SemanticsConfig(mode=mode)
+    cfg = P.SemanticsConfig(mode=mode, padding=pad)
     # positive weights: the child gradient is then a sum of same-sign terms, so the
     # elementwise tolerance measures the kernel, not fp32 cancellation over ~600 terms
     cot = rng.uniform(0.25, 1.75, (B, L))

@@ -10,6 +10,8 @@ hard gradients exact for the ones cotangent; LSE within 1e-5 relative
 (tape.py:346-348).
 """
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -105,7 +107,8 @@ def test_child_layouts(cuda, mode, ab, layout):
     import torch
     P = cuda
     orc = _oracle()
-    rng = np.random.default_rng(hash((mode, ab, layout)) % 2**32)
+    # str hash() is salted per process (PYTHONHASHSEED): derive a stable seed instead
+    rng = np.random.default_rng(zlib.crc32(repr((mode, ab, layout)).encode()))
     B, L = 2, 7000
     xy = np.asarray(np.cumsum(rng.normal(0, 0.05, (B, L, 2)), axis=1), dtype=np.float32)
     iv = P.StepInterval(*ab)

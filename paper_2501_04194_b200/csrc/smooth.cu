@@ -51,8 +51,9 @@ __device__ __forceinline__ void lse_group(float& m, float& s, const float* v, in
 }
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SParams p) {
-  __shared__ float U[S_T + S_CH];
-  __shared__ float LW[S_CH];
+  __shared__ __align__(16) float U[S_T + S_CH];
+  __shared__ __align__(16) float LW[S_CH];
+  __shared__ float Red[3][S_T / 32];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
   const int t0 = blockIdx.x * S_T;
@@ -72,6 +73,64 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
     }
     for (int q = threadIdx.x; q < kc; q += S_T) LW[q] = p.lw2[p.i_lo + k0 + q];
     __syncthreads();
+    if (MODE == M_LSE && K <= S_CH) {
+      // factorised window sum: w_i e^{tau u_{t+i}} = (2^{lw_i - lwmax}) (2^{tau2 (u_{t+i} - umax)})
+      // x 2^{lwmax + tau2 umax}, so a tile whose staged u span is <= 96 / tau2 needs one
+      // ex2 per staged element and one FMA per pair.  Every window holds the largest
+      // weight, so its best term is >= 2^-96; a factor or product only flushes below
+      // 2^-126, i.e. < 2^-30 of that term, below fp32 resolution of the sum.  Wider tiles
+      // (or non-finite values) take the exact grouped path below.
+      float umax = -INFINITY, umin = INFINITY, lwmax = -INFINITY;
+      for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) {
+        umax = fmaxf(umax, U[q]);
+        umin = fminf(umin, U[q]);
+      }
+      for (int q = threadIdx.x; q < kc; q += S_T) lwmax = fmaxf(lwmax, LW[q]);
+      for (int o = 16; o > 0; o >>= 1) {
+        umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+        umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+        lwmax = fmaxf(lwmax, __shfl_xor_sync(0xffffffffu, lwmax, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        Red[0][threadIdx.x >> 5] = umax;
+        Red[1][threadIdx.x >> 5] = umin;
+        Red[2][threadIdx.x >> 5] = lwmax;
+      }
+      __syncthreads();
+      umax = Red[0][0];
+      umin = Red[1][0];
+      lwmax = Red[2][0];
+      for (int w = 1; w < S_T / 32; ++w) {
+        umax = fmaxf(umax, Red[0][w]);
+        umin = fminf(umin, Red[1][w]);
+        lwmax = fmaxf(lwmax, Red[2][w]);
+      }
+      const float span = tau2 * (umax - umin);  // NaN / inf -> exact path
+      if (span <= 96.f && lwmax > -INFINITY) {
+        __syncthreads();  // every thread has read Red
+        for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) U[q] = ex2f(tau2 * (U[q] - umax));
+        for (int q = threadIdx.x; q < kc; q += S_T) LW[q] = ex2f(LW[q] - lwmax);
+        __syncthreads();
+        if (t < L) {
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          const float* ut = U + threadIdx.x;
+          int k = 0;
+#pragma unroll 4
+          for (; k + 4 <= kc; k += 4) {
+            s0 = fmaf(LW[k], ut[k], s0);
+            s1 = fmaf(LW[k + 1], ut[k + 1], s1);
+            s2 = fmaf(LW[k + 2], ut[k + 2], s2);
+            s3 = fmaf(LW[k + 3], ut[k + 3], s3);
+          }
+          for (; k < kc; ++k) s0 = fmaf(LW[k], ut[k], s0);
+          m = fmaf(tau2, umax, lwmax);
+          s = (s0 + s1) + (s2 + s3);
+        }
+        first = false;
+        __syncthreads();
+        continue;  // K <= S_CH: this was the only chunk
+      }
+    }
     if (MODE == M_LSE && t < L) {
       // groups of SG offsets: scores to registers, one max, one rescale of s,
       // then one ex2 + add per pair (~6 issue slots per pair instead of ~10 for

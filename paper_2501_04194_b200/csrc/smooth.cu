@@ -51,8 +51,8 @@ __device__ __forceinline__ void lse_group(float& m, float& s, const float* v, in
 }
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SParams p) {
-  __shared__ __align__(16) float U[S_T + S_CH];
-  __shared__ __align__(16) float LW[S_CH];
+  __shared__ __align__(16) float U[S_T + S_CH + 8];
+  __shared__ __align__(16) float LW[S_CH + 4];  // (>= 4 S_T: the fast path's group sums)
   __shared__ float Red[3][S_T / 32];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
@@ -108,23 +108,39 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
       const float span = tau2 * (umax - umin);  // NaN / inf -> exact path
       if (span <= 96.f && lwmax > -INFINITY) {
         __syncthreads();  // every thread has read Red
-        for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) U[q] = ex2f(tau2 * (U[q] - umax));
-        for (int q = threadIdx.x; q < kc; q += S_T) LW[q] = ex2f(LW[q] - lwmax);
+        // factors in place; zero tails so the 4-wide loads below read finite zeros
+        for (int q = threadIdx.x; q < S_T + kc + 7; q += S_T)
+          U[q] = q < S_T + kc - 1 ? ex2f(tau2 * (U[q] - umax)) : 0.f;
+        for (int q = threadIdx.x; q < kc + 4; q += S_T) LW[q] = q < kc ? ex2f(LW[q] - lwmax) : 0.f;
         __syncthreads();
-        if (t < L) {
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-          const float* ut = U + threadIdx.x;
-          int k = 0;
-#pragma unroll 4
-          for (; k + 4 <= kc; k += 4) {
-            s0 = fmaf(LW[k], ut[k], s0);
-            s1 = fmaf(LW[k + 1], ut[k + 1], s1);
-            s2 = fmaf(LW[k + 2], ut[k + 2], s2);
-            s3 = fmaf(LW[k + 3], ut[k + 3], s3);
+        // register-blocked correlation: thread (g, o) sums 4 outputs 4o .. 4o+3 over a
+        // quarter g of the offsets; per 4 offsets 3 conflict-free LDS.128 feed 16 FMAs
+        {
+          const int o = threadIdx.x & (S_T / 4 - 1), g = threadIdx.x / (S_T / 4);
+          const int kc4 = (kc + 3) & ~3;
+          const int chunk = ((kc4 >> 2) + 3) & ~3;
+          const int kb = g * chunk, ke = min(kc4, kb + chunk);
+          const float4* U4 = reinterpret_cast<const float4*>(U);
+          const float4* W4 = reinterpret_cast<const float4*>(LW);
+          float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
+          for (int k = kb; k < ke; k += 4) {
+            const float4 w = W4[k >> 2];
+            const float4 a = U4[o + (k >> 2)], b = U4[o + (k >> 2) + 1];
+            r0 = fmaf(w.x, a.x, fmaf(w.y, a.y, fmaf(w.z, a.z, fmaf(w.w, a.w, r0))));
+            r1 = fmaf(w.x, a.y, fmaf(w.y, a.z, fmaf(w.z, a.w, fmaf(w.w, b.x, r1))));
+            r2 = fmaf(w.x, a.z, fmaf(w.y, a.w, fmaf(w.z, b.x, fmaf(w.w, b.y, r2))));
+            r3 = fmaf(w.x, a.w, fmaf(w.y, b.x, fmaf(w.z, b.y, fmaf(w.w, b.z, r3))));
           }
-          for (; k < kc; ++k) s0 = fmaf(LW[k], ut[k], s0);
+          __syncthreads();  // LW is reused as the cross-group reduction buffer
+          LW[g * S_T + 4 * o] = r0;
+          LW[g * S_T + 4 * o + 1] = r1;
+          LW[g * S_T + 4 * o + 2] = r2;
+          LW[g * S_T + 4 * o + 3] = r3;
+          __syncthreads();
+        }
+        if (t < L) {
           m = fmaf(tau2, umax, lwmax);
-          s = (s0 + s1) + (s2 + s3);
+          s = (LW[threadIdx.x] + LW[S_T + threadIdx.x]) + (LW[2 * S_T + threadIdx.x] + LW[3 * S_T + threadIdx.x]);
         }
         first = false;
         __syncthreads();

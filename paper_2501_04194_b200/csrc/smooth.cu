@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
   __shared__ __align__(16) float Gt[S_T];
   __shared__ __align__(16) float Mt[S_T];
   __shared__ float Lt[S_T];
+  __shared__ float Rw[4][S_T / 32];
   const int L = (int)p.L;
   const int t0 = blockIdx.x * S_T;
   const int K = p.i_hi - p.i_lo + 1;
@@ -393,6 +394,68 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       }
       // dense cotangent row tile: no per-pair zero test, (G, M) read 4 at a time
       const int dense = __syncthreads_and(nz);
+      bool done = false;
+      if (MODE == M_LSE) {
+        // factorised: g_t 2^{tau2 (u_{t+i} - M_t)} = A_t E_{t+i} 2^{tau2 (umax - Mmax)} with
+        // A_t = g_t 2^{tau2 (Mmax - M_t)} in [1, 2^100] |g| and E_j = 2^{tau2 (u_j - umax)} in
+        // [2^-100, 1]: no factor or product leaves the fp32 range, so one ex2 per staged
+        // element and one FMA per pair replace the per-pair ex2
+        float umx = -INFINITY, umn = INFINITY, mmx = -INFINITY, mmn = INFINITY;
+        for (int q = threadIdx.x; q < nt + kc - 1; q += S_T) {
+          umx = fmaxf(umx, U[q]);
+          umn = fminf(umn, U[q]);
+        }
+        if (threadIdx.x < nt && Gt[threadIdx.x] != 0.f) mmx = mmn = Mt[threadIdx.x];
+        for (int o = 16; o > 0; o >>= 1) {
+          umx = fmaxf(umx, __shfl_xor_sync(0xffffffffu, umx, o));
+          umn = fminf(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+          mmx = fmaxf(mmx, __shfl_xor_sync(0xffffffffu, mmx, o));
+          mmn = fminf(mmn, __shfl_xor_sync(0xffffffffu, mmn, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+          Rw[0][threadIdx.x >> 5] = umx;
+          Rw[1][threadIdx.x >> 5] = umn;
+          Rw[2][threadIdx.x >> 5] = mmx;
+          Rw[3][threadIdx.x >> 5] = mmn;
+        }
+        __syncthreads();
+        umx = Rw[0][0], umn = Rw[1][0], mmx = Rw[2][0], mmn = Rw[3][0];
+        for (int w = 1; w < S_T / 32; ++w) {
+          umx = fmaxf(umx, Rw[0][w]);
+          umn = fminf(umn, Rw[1][w]);
+          mmx = fmaxf(mmx, Rw[2][w]);
+          mmn = fminf(mmn, Rw[3][w]);
+        }
+        if (tau2 * (umx - umn) <= 100.f && tau2 * (mmx - mmn) <= 100.f && mmx > -INFINITY) {  // NaN / inf / no g -> exact
+          __syncthreads();  // every thread has read Rw; U / Gt are rewritten below
+          for (int q = threadIdx.x; q < nt + kc - 1; q += S_T) U[q] = ex2f(tau2 * (U[q] - umx));
+          if (threadIdx.x < S_T) {
+            const float g = Gt[threadIdx.x];
+            Gt[threadIdx.x] = (threadIdx.x < nt && g != 0.f) ? g * ex2f(tau2 * (mmx - Mt[threadIdx.x])) : 0.f;
+          }
+          __syncthreads();
+          const double cexp = (double)tau2 * ((double)umx - (double)mmx);
+#pragma unroll
+          for (int c = 0; c < S_CH / S_T; ++c) {
+            const int k = threadIdx.x + S_T * c;
+            if (k >= kc) break;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int q = 0;
+            for (; q + 4 <= nt; q += 4) {
+              const float4 g4 = *reinterpret_cast<const float4*>(Gt + q);
+              a0 = fmaf(g4.x, U[q + k], a0);
+              a1 = fmaf(g4.y, U[q + k + 1], a1);
+              a2 = fmaf(g4.z, U[q + k + 2], a2);
+              a3 = fmaf(g4.w, U[q + k + 3], a3);
+            }
+            for (; q < nt; ++q) a0 = fmaf(Gt[q], U[q + k], a0);
+            // w_i d out / d w_i convention (k_smooth_abc divides by 2^{lw2_i})
+            acc[c] += (double)((a0 + a1) + (a2 + a3)) * exp2(cexp + (double)lwi[c]);
+          }
+          done = true;
+        }
+      }
+      if (!done) {
 #pragma unroll
       for (int c = 0; c < S_CH / S_T; ++c) {
         int k = threadIdx.x + S_T * c;
@@ -422,6 +485,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
           else a = fmaf(g * ex2f(fmaf(tau2, u - Lt[q], lw)), u - Mt[q], a);
         }
         acc[c] += (double)a;
+      }
       }
       __syncthreads();
     }

@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_pad(const __grid_constant__ 
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SParams p) {
-  __shared__ float U[S_T + S_CH];
+  __shared__ __align__(16) float U[S_T + S_CH];
   __shared__ __align__(16) float Gt[S_T];
   __shared__ __align__(16) float Mt[S_T];
   __shared__ float Lt[S_T];
@@ -374,6 +374,13 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       acc[c] = 0.0;
       const int k = threadIdx.x + S_T * c;
       lwi[c] = k < kc ? p.lw2[p.i_lo + k0 + k] : -INFINITY;
+    }
+    double accf[4] = {0.0, 0.0, 0.0, 0.0};  // LSE factorised path: offsets 4 tid + r
+    float lwf[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = 4 * (int)threadIdx.x + r;
+      lwf[r] = k < kc ? p.lw2[p.i_lo + k0 + k] : -INFINITY;
     }
     for (long long row = r0; row < r1; ++row) {
       const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
@@ -428,29 +435,35 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
         }
         if (tau2 * (umx - umn) <= 100.f && tau2 * (mmx - mmn) <= 100.f && mmx > -INFINITY) {  // NaN / inf / no g -> exact
           __syncthreads();  // every thread has read Rw; U / Gt are rewritten below
-          for (int q = threadIdx.x; q < nt + kc - 1; q += S_T) U[q] = ex2f(tau2 * (U[q] - umx));
+          // E in place; zeros past the staged range (read by the 4-wide loads, times A = 0)
+          for (int q = threadIdx.x; q < S_T + S_CH; q += S_T)
+            U[q] = q < nt + kc - 1 ? ex2f(tau2 * (U[q] - umx)) : 0.f;
           if (threadIdx.x < S_T) {
             const float g = Gt[threadIdx.x];
             Gt[threadIdx.x] = (threadIdx.x < nt && g != 0.f) ? g * ex2f(tau2 * (mmx - Mt[threadIdx.x])) : 0.f;
           }
           __syncthreads();
           const double cexp = (double)tau2 * ((double)umx - (double)mmx);
-#pragma unroll
-          for (int c = 0; c < S_CH / S_T; ++c) {
-            const int k = threadIdx.x + S_T * c;
-            if (k >= kc) break;
+          // register-blocked: thread owns offsets 4 tid .. 4 tid + 3; per 4 outputs one
+          // broadcast LDS.128 of A and two conflict-free LDS.128 of E feed 16 FMAs
+          const int kq = 4 * threadIdx.x;
+          if (kq < kc) {
+            const float4* G4 = reinterpret_cast<const float4*>(Gt);
+            const float4* E4 = reinterpret_cast<const float4*>(U);
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-            int q = 0;
-            for (; q + 4 <= nt; q += 4) {
-              const float4 g4 = *reinterpret_cast<const float4*>(Gt + q);
-              a0 = fmaf(g4.x, U[q + k], a0);
-              a1 = fmaf(g4.y, U[q + k + 1], a1);
-              a2 = fmaf(g4.z, U[q + k + 2], a2);
-              a3 = fmaf(g4.w, U[q + k + 3], a3);
+            for (int q = 0; q < nt; q += 4) {
+              const float4 g = G4[q >> 2];
+              const float4 x = E4[(q + kq) >> 2], y = E4[((q + kq) >> 2) + 1];
+              a0 = fmaf(g.x, x.x, fmaf(g.y, x.y, fmaf(g.z, x.z, fmaf(g.w, x.w, a0))));
+              a1 = fmaf(g.x, x.y, fmaf(g.y, x.z, fmaf(g.z, x.w, fmaf(g.w, y.x, a1))));
+              a2 = fmaf(g.x, x.z, fmaf(g.y, x.w, fmaf(g.z, y.x, fmaf(g.w, y.y, a2))));
+              a3 = fmaf(g.x, x.w, fmaf(g.y, y.x, fmaf(g.z, y.y, fmaf(g.w, y.z, a3))));
             }
-            for (; q < nt; ++q) a0 = fmaf(Gt[q], U[q + k], a0);
             // w_i d out / d w_i convention (k_smooth_abc divides by 2^{lw2_i})
-            acc[c] += (double)((a0 + a1) + (a2 + a3)) * exp2(cexp + (double)lwi[c]);
+            accf[0] += (double)a0 * exp2(cexp + (double)lwf[0]);
+            accf[1] += (double)a1 * exp2(cexp + (double)lwf[1]);
+            accf[2] += (double)a2 * exp2(cexp + (double)lwf[2]);
+            accf[3] += (double)a3 * exp2(cexp + (double)lwf[3]);
           }
           done = true;
         }
@@ -497,6 +510,14 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       if (p.lw2[i] == -INFINITY) continue;
       double v = (double)sg * acc[c] * (MODE == M_LSE ? (double)itau : 1.0);
       if (v != 0.0) atomicAdd(p.dw64 + i, v);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = 4 * (int)threadIdx.x + r;
+      if (k >= kc || accf[r] == 0.0) continue;
+      const int i = p.i_lo + k0 + k;
+      if (p.lw2[i] == -INFINITY) continue;
+      atomicAdd(p.dw64 + i, (double)sg * accf[r] * (double)itau);
     }
   }
 }

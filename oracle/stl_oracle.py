@@ -630,3 +630,73 @@ def value_and_grad(f, arrays, cfg, si=None):
     tr, grads, dabc = trace_and_grad(f, arrays, cfg, cot, smooth_binding=binding,
                                      eps_override=None if si is None else si.eps)
     return float(tr[0]), grads, dabc
+
+
+# ---------------------------------------------------------------------------
+# O(L)-memory restatements for long signals (same semantics, checked against the
+# tape oracle above at small L by tests/test_oracle_long.py)
+# ---------------------------------------------------------------------------
+
+def until_untimed_hard(left, right, cot):
+    """Hard untimed Until over child traces (rows, L), masking.py:238-293 with iv=None.
+
+    Per output t the reference stacks, for k = 0..L-1-t, pm_k = min(l[t..t+k]) built
+    incrementally (a tie keeps pm_{k-1}, i.e. the earliest arg-min) and
+    term_k = min(pm_k, r[t+k]) (a tie keeps pm, the first stacked operand), then takes
+    the first arg-max over k (tape.py:338-357 one-hot rule); min is -max(-x), so every
+    value is a selected input, signed zeros included.  Entries with t+k > L-1 carry
+    weight 0 and never win.  Returns (trace, d_left, d_right) for cotangent ``cot``;
+    O(L) memory and O(L^2) time per row.
+    """
+    left = np.atleast_2d(np.asarray(left, dtype=np.float64))
+    right = np.atleast_2d(np.asarray(right, dtype=np.float64))
+    cot = np.atleast_2d(np.asarray(cot, dtype=np.float64))
+    R, L = left.shape
+    out = np.empty((R, L))
+    dl = np.zeros((R, L))
+    dr = np.zeros((R, L))
+    ar = np.arange(L)
+    for t in range(L):
+        ls = left[:, t:]
+        rs = right[:, t:]
+        n = L - t
+        # earliest arg-min prefix: a new minimum only on a strict decrease
+        pmv = np.minimum.accumulate(ls, axis=1)
+        new = np.ones((R, n), dtype=bool)
+        new[:, 1:] = ls[:, 1:] < pmv[:, :-1]
+        pidx = np.maximum.accumulate(np.where(new, ar[None, :n], 0), axis=1)
+        pm = np.take_along_axis(ls, pidx, axis=1)
+        take_pm = pm <= rs
+        term = np.where(take_pm, pm, rs)
+        k = np.argmax(term, axis=1)
+        rows = np.arange(R)
+        out[:, t] = term[rows, k]
+        via_pm = take_pm[rows, k]
+        src_l = t + pidx[rows, k]
+        src_r = t + k
+        np.add.at(dl, (rows[via_pm], src_l[via_pm]), cot[rows[via_pm], t])
+        np.add.at(dr, (rows[~via_pm], src_r[~via_pm]), cot[rows[~via_pm], t])
+    return out, dl, dr
+
+
+def suffix_hard(x, cot, kind="max"):
+    """Untimed hard F (kind='max') / G ('min') over (rows, L), tape.py:475-491: reverse
+    running extremum, the gradient of out[t] routed to the FIRST extremum at or after t.
+    Vectorised form of ``_suffix`` (O(L) numpy passes)."""
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    cot = np.atleast_2d(np.asarray(cot, dtype=np.float64))
+    v = x if kind == "max" else -x
+    R, L = v.shape
+    rv = v[:, ::-1]
+    best = np.maximum.accumulate(rv, axis=1)
+    # scanning from the end, a later-in-time (earlier-in-scan) index is replaced on >=
+    new = np.ones((R, L), dtype=bool)
+    new[:, 1:] = rv[:, 1:] >= best[:, :-1]
+    ridx = np.maximum.accumulate(np.where(new, np.arange(L)[None, :], 0), axis=1)
+    sel = (L - 1 - ridx)[:, ::-1]
+    val = np.take_along_axis(v, sel, axis=1)
+    g = np.zeros((R, L))
+    np.add.at(g, (np.repeat(np.arange(R), L), sel.ravel()), cot.ravel())
+    if kind == "max":
+        return val, g
+    return -val, g

@@ -19,3 +19,15 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+def import_reference():
+    """The unmodified reference package for the engine-hook tests: baseline/_ref (the
+    offline install that travels to the GPU box) or, in the dev container, the
+    reference tree.  Skips the test when neither is present."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "stlmask")):
+            if path not in sys.path:
+                sys.path.append(path)
+            break
+    return pytest.importorskip("stlmask")

@@ -8,7 +8,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from paper_2501_04194_b200.core import (Hard, LogSumExp, PaddingPolicy, SemanticsConfig,
+from paper_2501_04194_b200.core import (Hard, LogSumExp, PaddingPolicy, SemanticsConfig, StepInterval,
                                         SmoothInterval, SoftMax)
 from paper_2501_04194_b200.formula import from_json
 
@@ -60,3 +60,28 @@ def load(name: str) -> list[Case]:
 
 def load_all() -> list[Case]:
     return load("kats") + load("random") + load("smooth_norm")
+
+
+@dataclass
+class ApiCase:
+    """One reference call of the public wrappers (tests/golden/make_api_golden.py)."""
+    meta: dict
+    arrays: dict
+
+    @property
+    def cfg(self):
+        return cfg_from_json(self.meta["cfg"])
+
+    def interval(self, key):
+        d = self.meta.get(key)
+        if d is None:
+            return None
+        if "step" in d:
+            return StepInterval(*[int(v) for v in d["step"]])
+        return SmoothInterval(*d["smooth"])
+
+
+def load_api() -> list[ApiCase]:
+    z = np.load(os.path.join(GOLDEN, "api.npz"))
+    meta = json.loads(str(z["meta"]))
+    return [ApiCase(m, {k: z[f"c{i}_{k}"] for k in m["arrays"]}) for i, m in enumerate(meta)]

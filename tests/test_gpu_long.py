@@ -1,0 +1,223 @@
+"""BASELINE configurations at their stated sizes and the multi-tile paths, on the device,
+against the oracle (VERDICT r1 "check every BASELINE config and every multi-tile path").
+
+* C1 exactly as BASELINE configs[0] states it (Always[0,50](x > 0.5), Hard, T=1000);
+* C3 at B=256, T=4000 (Hard bit-exact on sampled rows; LSE(10) on one row);
+* untimed F/G past the 4096-sample tiles of csrc/fg_unt.cu (T = 4097, 8193, 100000),
+  tie-heavy data so the first-arg-max rule crosses tile carries;
+* hard untimed Until past its 2048-sample tile (csrc/until.cu), tie-heavy;
+* C5 corners: timed F/G[0,100] at T=100k, U[0,100] and untimed U at T=30k.
+
+Rows are independent, so full-size batches run on the device and sampled rows go to the
+oracle; at lengths where the tape oracle's O(L^2) Until / suffix windows do not fit, the
+O(L)-memory restatements (stl_oracle.until_untimed_hard / suffix_hard, pinned to the tape
+oracle by tests/test_oracle_long.py) check them.  Tolerances as test_gpu_parity.py.
+"""
+
+import numpy as np
+import pytest
+
+import stl_oracle
+from devhelp import assert_hard_equal, rel_err
+
+import paper_2501_04194_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _run(f, arrays, cfg, cot=None):
+    """Full-batch device trace + VJP; returns host float64 arrays."""
+    import torch
+    dev = torch.device("cuda", 0)
+    chans = {k: torch.tensor(np.asarray(v, dtype=np.float32), device=dev).requires_grad_(True)
+             for k, v in arrays.items()}
+    out = P.trace(f, chans, cfg)
+    c = torch.ones_like(out) if cot is None else torch.tensor(np.asarray(cot, dtype=np.float32), device=dev)
+    grads = torch.autograd.grad(out, list(chans.values()), c, allow_unused=True)
+    g = {k: (np.zeros(out.shape) if gi is None else gi.double().cpu().numpy())
+         for k, gi in zip(chans, grads)}
+    return out.detach().double().cpu().numpy(), g
+
+
+def _ties(rng, shape, levels=2):
+    v = rng.integers(-levels, levels + 1, shape).astype(np.float32)
+    v[rng.random(shape) < 0.05] = -0.0
+    return v
+
+
+def test_c1_exact_baseline_config(cuda):
+    """BASELINE configs[0]: Always[0,50](x > 0.5), hard, 1-D, batch 1, T=1000, last pad."""
+    x = np.asarray(np.random.default_rng(0).normal(0, 1, (1, 1000)), dtype=np.float32)
+    f = P.Always(P.Pred("x", ">", 0.5), P.StepInterval(0, 50))
+    cfg = P.SemanticsConfig(mode=P.Hard())
+    tr, g = _run(f, {"x": x}, cfg)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x.astype(np.float64)}, cfg)
+    assert_hard_equal(tr, ref_tr.astype(np.float32))
+    np.testing.assert_array_equal(g["x"], ref_g["x"])
+    # robustness mode (value_and_grad, autodiff.py:64) on the same case
+    vg = P.value_and_grad(f, P.NamedSignals.from_arrays({"x": x[0]}), cfg)
+    rv, rg, _ = stl_oracle.value_and_grad(f, {"x": x[0].astype(np.float64)}, cfg)
+    assert np.float32(vg.value) == np.float32(rv)
+    np.testing.assert_array_equal(vg.d_signal["x"], rg["x"][0] if rg["x"].ndim == 2 else rg["x"])
+
+
+def _c3_data():
+    rng = np.random.default_rng(2)
+    return {k: np.asarray(rng.normal(0, 1, (256, 4000)), dtype=np.float32) for k in ("x", "y", "z")}
+
+
+C3 = P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 200))),
+           P.Until(P.Pred("y", "<", 1.0), P.Pred("z", ">", 0.0)))
+
+
+def test_c3_full_size_hard_rows_bit_exact(cuda):
+    data = _c3_data()
+    cfg = P.SemanticsConfig(mode=P.Hard())
+    tr, g = _run(C3, data, cfg)
+    for r in (0, 131, 255):
+        rows = {k: v[r:r + 1].astype(np.float64) for k, v in data.items()}
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(C3, rows, cfg)
+        assert_hard_equal(tr[r:r + 1], ref_tr.astype(np.float32))
+        for k in data:
+            np.testing.assert_array_equal(g[k][r:r + 1], ref_g[k])
+    # size-independent: every output routes its unit cotangent to exactly one sample
+    total = sum(g[k] for k in data)
+    assert np.all(np.abs(total).sum(axis=1) == 4000)
+
+
+def test_c3_full_size_lse_row(cuda):
+    data = _c3_data()
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(10.0))
+    tr, g = _run(C3, data, cfg)
+    r = 77
+    rows = {k: v[r:r + 1].astype(np.float64) for k, v in data.items()}
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(C3, rows, cfg)
+    assert rel_err(tr[r:r + 1], ref_tr) <= TOL
+    for k in data:
+        assert rel_err(g[k][r:r + 1], ref_g[k]) <= TOL, k
+
+
+@pytest.mark.parametrize("T", [4097, 8193, 100_000])
+@pytest.mark.parametrize("op", ["F", "G"])
+@pytest.mark.parametrize("ties", [False, True], ids=["noise", "ties"])
+def test_untimed_hard_fg_across_tiles(cuda, T, op, ties):
+    rng = np.random.default_rng(T + (op == "G") + 2 * ties)
+    x = _ties(rng, (3, T)) if ties else np.asarray(rng.normal(0, 1, (3, T)), dtype=np.float32)
+    cot = np.asarray(rng.normal(0, 1, (3, T)), dtype=np.float32)
+    node = P.Eventually if op == "F" else P.Always
+    f = node(P.Pred("x", ">", 0.0))
+    cfg = P.SemanticsConfig()
+    tr, g = _run(f, {"x": x}, cfg)
+    ref, rg = stl_oracle.suffix_hard(x.astype(np.float64) - 0.0, np.ones((3, T)), "max" if op == "F" else "min")
+    assert_hard_equal(tr, ref.astype(np.float32))
+    np.testing.assert_array_equal(g["x"], rg)
+    tr2, g2 = _run(f, {"x": x}, cfg, cot)
+    _, rg2 = stl_oracle.suffix_hard(x.astype(np.float64), cot.astype(np.float64), "max" if op == "F" else "min")
+    assert rel_err(g2["x"], rg2) <= 1e-6
+
+
+@pytest.mark.parametrize("T", [4097, 8193, 100_000])
+@pytest.mark.parametrize("op", ["F", "G"])
+def test_untimed_lse_fg_across_tiles(cuda, T, op):
+    rng = np.random.default_rng(7 * T + (op == "G"))
+    # random walks: the suffix LSE changes scale along the signal
+    x = np.cumsum(np.asarray(rng.normal(0, 0.2, (2, T)), dtype=np.float32), axis=1, dtype=np.float32)
+    cot = np.asarray(rng.uniform(0.5, 1.5, (2, T)), dtype=np.float32)
+    node = P.Eventually if op == "F" else P.Always
+    f = node(P.Pred("x", ">", 0.25))
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(10.0))
+    tr, g = _run(f, {"x": x}, cfg, cot)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x.astype(np.float64)}, cfg, cot.astype(np.float64))
+    assert rel_err(tr, ref_tr) <= TOL
+    assert rel_err(g["x"], ref_g["x"]) <= TOL
+
+
+def test_untimed_softmax_fg_across_tiles(cuda):
+    rng = np.random.default_rng(41)
+    T = 4097
+    x = np.asarray(rng.normal(0, 1, (1, T)), dtype=np.float32)
+    f = P.Eventually(P.Pred("x", ">", 0.0))
+    cfg = P.SemanticsConfig(mode=P.SoftMax(2.0))
+    tr, g = _run(f, {"x": x}, cfg)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x.astype(np.float64)}, cfg)
+    assert rel_err(tr, ref_tr) <= TOL
+    assert rel_err(g["x"], ref_g["x"]) <= TOL
+
+
+@pytest.mark.parametrize("T", [2049, 4000, 10_000])
+def test_hard_untimed_until_across_tiles(cuda, T):
+    rng = np.random.default_rng(T)
+    x, y = _ties(rng, (2, T), 3), _ties(rng, (2, T), 3)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", "<", 0.0))
+    cfg = P.SemanticsConfig()
+    tr, g = _run(f, {"x": x, "y": y}, cfg)
+    ref, dl, dr = stl_oracle.until_untimed_hard(x.astype(np.float64) - 0.0, -y.astype(np.float64) + 0.0,
+                                                np.ones((2, T)))
+    assert_hard_equal(tr, ref.astype(np.float32))
+    np.testing.assert_array_equal(g["x"], dl)
+    np.testing.assert_array_equal(g["y"], -dr)
+    cot = np.asarray(rng.normal(0, 1, (2, T)), dtype=np.float32)
+    _, g2 = _run(f, {"x": x, "y": y}, cfg, cot)
+    _, dl2, dr2 = stl_oracle.until_untimed_hard(x.astype(np.float64), -y.astype(np.float64),
+                                                cot.astype(np.float64))
+    assert rel_err(g2["x"], dl2) <= 1e-6
+    assert rel_err(g2["y"], -dr2) <= 1e-6
+
+
+@pytest.mark.parametrize("mode", [P.Hard(), P.LogSumExp(10.0)], ids=["hard", "lse"])
+@pytest.mark.parametrize("op", ["F", "G"])
+def test_c5_timed_window_T100k(cuda, mode, op):
+    rng = np.random.default_rng(100 + (op == "G"))
+    B, T = 64, 100_000
+    x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    node = P.Eventually if op == "F" else P.Always
+    f = node(P.Pred("x", ">", 0.0), P.StepInterval(0, 100))
+    cfg = P.SemanticsConfig(mode=mode)
+    tr, g = _run(f, {"x": x}, cfg)
+    for r in (0, 63):
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x[r:r + 1].astype(np.float64)}, cfg)
+        if type(mode).__name__ == "Hard":
+            assert_hard_equal(tr[r:r + 1], ref_tr.astype(np.float32))
+            np.testing.assert_array_equal(g["x"][r:r + 1], ref_g["x"])
+        else:
+            assert rel_err(tr[r:r + 1], ref_tr) <= TOL
+            assert rel_err(g["x"][r:r + 1], ref_g["x"]) <= TOL
+
+
+@pytest.mark.parametrize("mode", [P.Hard(), P.LogSumExp(10.0)], ids=["hard", "lse"])
+def test_c5_timed_until_T30k(cuda, mode):
+    rng = np.random.default_rng(30)
+    B, T = 64, 30_000
+    x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    y = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0), P.StepInterval(0, 100))
+    cfg = P.SemanticsConfig(mode=mode)
+    tr, g = _run(f, {"x": x, "y": y}, cfg)
+    r = 40
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x[r:r + 1].astype(np.float64),
+                                                     "y": y[r:r + 1].astype(np.float64)}, cfg)
+    if type(mode).__name__ == "Hard":
+        assert_hard_equal(tr[r:r + 1], ref_tr.astype(np.float32))
+        for k in ("x", "y"):
+            np.testing.assert_array_equal(g[k][r:r + 1], ref_g[k])
+    else:
+        assert rel_err(tr[r:r + 1], ref_tr) <= TOL
+        for k in ("x", "y"):
+            assert rel_err(g[k][r:r + 1], ref_g[k]) <= TOL
+
+
+def test_c5_untimed_until_T30k_hard(cuda):
+    rng = np.random.default_rng(31)
+    B, T = 64, 30_000
+    x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    y = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0))
+    tr, g = _run(f, {"x": x, "y": y}, P.SemanticsConfig())
+    r = 17
+    ref, dl, dr = stl_oracle.until_untimed_hard(x[r:r + 1].astype(np.float64), y[r:r + 1].astype(np.float64),
+                                                np.ones((1, T)))
+    assert_hard_equal(tr[r:r + 1], ref.astype(np.float32))
+    np.testing.assert_array_equal(g["x"][r:r + 1], dl)
+    np.testing.assert_array_equal(g["y"][r:r + 1], dr)

@@ -192,3 +192,58 @@ def test_anneal_schedule_matches_reference_formula():
     assert AnnealSchedule("constant", 7.0, 7.0, 1).value(123) == 7.0
     with pytest.raises(ValueError):
         AnnealSchedule("cubic", 1.0, 2.0, 3)
+
+
+# --- reference error paths of the public wrappers (raised before any device call) ----
+
+def test_value_and_grad_binding_errors():
+    """autodiff.py:77-83 (test_autodiff.py:149-158): si= without a smooth node, and
+    distinct smooth intervals without si=, raise ValueError; missing channels raise
+    ValidationError (masking.py:353-355)."""
+    sig = P.NamedSignals.from_arrays({"s": [1.0, 2.0]})
+    with pytest.raises(ValueError, match="no smooth-interval node"):
+        P.value_and_grad(P.Eventually(P.Pred("s", ">", 0.0)), sig, si=P.SmoothInterval(0.2, 0.8, 4.0))
+    f = P.And(P.Always(P.Pred("s", ">", 0.0), P.SmoothInterval(0.1, 0.5, 4.0)),
+              P.Eventually(P.Pred("s", ">", 0.0), P.SmoothInterval(0.2, 0.9, 4.0)))
+    with pytest.raises(ValueError, match="multiple distinct smooth intervals"):
+        P.value_and_grad(f, P.NamedSignals.from_arrays({"s": np.ones(8)}),
+                         P.SemanticsConfig(mode=P.LogSumExp(5.0)))
+    with pytest.raises(P.ValidationError):
+        P.value_and_grad(P.Eventually(P.Pred("q", ">", 0.0)), sig)
+    with pytest.raises(P.ValidationError):
+        P.robustness_trace(P.Eventually(P.Pred("q", ">", 0.0)), sig)
+
+
+def test_trace_wrapper_shape_errors():
+    """masking.py:370-374, 398-399 (test_masking.py:177-179): empty traces and length
+    mismatches raise ShapeError; a smooth Until raises TypeError (masking.py:239-240)."""
+    with pytest.raises(P.ShapeError):
+        P.eventually_trace([], P.StepInterval(0, 1))
+    with pytest.raises(P.ShapeError):
+        P.always_trace(np.zeros(0), None)
+    with pytest.raises(P.ShapeError):
+        P.until_trace([1.0, 2.0], [1.0], None)
+    with pytest.raises(P.ShapeError):
+        P.until_trace([], [], None)
+    with pytest.raises(TypeError):
+        P.until_trace([1.0, 2.0], [1.0, 0.0], P.SmoothInterval(0.1, 0.5))
+
+
+def test_engine_hook_registers_b200_choice(tmp_path):
+    """the reference CLI gains --engine b200 (cli.py:190-191) and its other
+    engines keep working unchanged."""
+    from conftest import import_reference
+    import_reference()
+    import json
+    import stlmask.cli as cli
+    from paper_2501_04194_b200 import stlmask_engine
+    stlmask_engine.install(cli)
+    stlmask_engine.install(cli)  # idempotent
+    p = cli.build_parser()
+    args = p.parse_args(["trace", "F[0,2] (x > 0)", "s.csv", "--engine", "b200"])
+    assert args.engine == "b200"
+    csv = tmp_path / "s.csv"
+    csv.write_text("x\n1\n3\n2\n0\n")
+    out = tmp_path / "o.json"
+    assert cli.main(["trace", "F[0,2] (x > 0)", str(csv), "--engine", "masking", "--out", str(out)]) == 0
+    assert json.loads(out.read_text()) == [3.0, 3.0, 0.0, 0.0]  # overrun -> last (masking.py:180-192)

@@ -21,7 +21,8 @@ from .engine import (Compiled, Gradients, always_trace, compile_formula, eventua
 
 __version__ = "0.1.0"
 
-from .mining import AnnealSchedule, MiningConfig, grid_eval_mining, mine_interval, mining_objective
+from .mining import (AnnealSchedule, MiningConfig, grid_eval_mining, mine_interval, mining_objective,
+                     synth_step_dataset)
 from .planning import (PlannerConfig, box_formula, plan_trajectory, planning_formula, planning_objective,
                        rollout_single_integrator)
 
@@ -36,6 +37,7 @@ __all__ = [
     "Compiled", "Gradients", "always_trace", "compile_formula", "eventually_trace", "robustness",
     "robustness_trace", "trace", "until_trace", "value_and_grad",
     "AnnealSchedule", "MiningConfig", "grid_eval_mining", "mine_interval", "mining_objective",
+    "synth_step_dataset",
     "PlannerConfig", "box_formula", "plan_trajectory", "planning_formula", "planning_objective",
     "rollout_single_integrator",
 ]

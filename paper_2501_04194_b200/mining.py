@@ -72,6 +72,24 @@ class MiningConfig:
             raise ValueError("steps must be >= 1")
 
 
+def synth_step_dataset(seed: int, n: int = 64, length: int = 20,
+                       truth: tuple = (0.23, 0.59), value_noise: float = 0.05) -> np.ndarray:
+    """Noisy step signals, 1 inside the truth window and 0 outside, each window edge
+    jittered by one sample (apps.py:252-269; same generator calls, so the same data for a
+    seed).  The mining dataset and the C4 benchmark input (seed 3,
+    n=4096, length=2000)."""
+    rng = np.random.default_rng(seed)
+    lo = int(math.ceil(truth[0] * length))
+    hi = int(math.floor(truth[1] * length))
+    data = np.zeros((n, length))
+    for row in range(n):
+        jlo = lo + int(rng.integers(-1, 2))
+        jhi = hi + int(rng.integers(-1, 2))
+        data[row, max(jlo, 0):min(jhi, length - 1) + 1] = 1.0
+    data += rng.normal(0.0, value_noise, (n, length))
+    return data
+
+
 def _sigmoid(z: float) -> float:
     if z >= 0:
         return 1.0 / (1.0 + math.exp(-z))

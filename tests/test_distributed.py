@@ -91,3 +91,47 @@ def test_allreduce_of_interval_grads_equals_full_batch():
     _, _, full = stl_oracle.trace_and_grad(f, {"x": x}, cfg, smooth_binding=(si.a, si.b, si.c))
     for r in range(world):
         np.testing.assert_allclose(res[r], full, rtol=1e-12, atol=1e-12)
+
+
+def _none_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    params = [torch.tensor(v, dtype=torch.float64, requires_grad=True) for v in (0.3, 0.65, 9.0)]
+    if rank == 0:  # rank 1 has no interval gradient at all (e.g. its rows skipped the binding)
+        for p_, g in zip(params, (1.0, 2.0, 3.0)):
+            p_.grad = torch.tensor(g, dtype=torch.float64)
+        allreduce_interval_grads(params)
+    else:
+        allreduce_interval_grads([None, params[1], None])
+    out_q.put((rank, [None if p_.grad is None else float(p_.grad) for p_ in params]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_allreduce_joins_ranks_without_grads():
+    """a rank without gradients must still join the collective (zeros)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_none_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert res[0] == [1.0, 2.0, 3.0]
+    assert res[1] == [None, 2.0, None]
+
+
+def test_sharded_trace_argument_checks():
+    import paper_2501_04194_b200 as P
+    from paper_2501_04194_b200.distributed import sharded_trace
+    f = P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 3))
+    with pytest.raises(ValueError, match="cannot be sharded"):
+        sharded_trace(f, {"x": torch.zeros(16)}, P.SemanticsConfig(), rank=0, world=2)
+    with pytest.raises(ValueError, match="batch size"):
+        sharded_trace(f, {"x": torch.zeros(4, 16), "y": torch.zeros(3, 16)}, P.SemanticsConfig(),
+                      rank=0, world=2)

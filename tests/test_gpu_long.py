@@ -82,9 +82,11 @@ def test_c3_full_size_hard_rows_bit_exact(cuda):
         assert_hard_equal(tr[r:r + 1], ref_tr.astype(np.float32))
         for k in data:
             np.testing.assert_array_equal(g[k][r:r + 1], ref_g[k])
-    # size-independent: every output routes its unit cotangent to exactly one sample
-    total = sum(g[k] for k in data)
-    assert np.all(np.abs(total).sum(axis=1) == 4000)
+    # size-independent: every output routes its unit cotangent to exactly one sample, and
+    # each channel's predicate has one sign (x > 0, z > 0: +1; y < 1: -1)
+    total = sum(np.abs(g[k]).sum(axis=1) for k in data)
+    assert np.all(total == 4000)
+    assert np.all(g["x"] >= 0) and np.all(g["z"] >= 0) and np.all(g["y"] <= 0)
 
 
 def test_c3_full_size_lse_row(cuda):

@@ -247,3 +247,12 @@ def test_engine_hook_registers_b200_choice(tmp_path):
     out = tmp_path / "o.json"
     assert cli.main(["trace", "F[0,2] (x > 0)", str(csv), "--engine", "masking", "--out", str(out)]) == 0
     assert json.loads(out.read_text()) == [3.0, 3.0, 0.0, 0.0]  # overrun -> last (masking.py:180-192)
+
+
+def test_synth_step_dataset_matches_reference():
+    """apps.py:252-269: the C4 / mining input generator reproduces the reference's data."""
+    from conftest import import_reference
+    import_reference()
+    from stlmask.apps import synth_step_dataset as ref
+    for seed, n, L in ((3, 8, 2000), (0, 64, 20)):
+        assert np.array_equal(P.synth_step_dataset(seed, n, L), ref(seed, n=n, length=L))

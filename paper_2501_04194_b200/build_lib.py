@@ -13,8 +13,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 LIB = os.path.join(HERE, "libstlg.so")
-SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_reg_bwd.cu", "fg_unt.cu", "until.cu", "smooth.cu", "mining.cu"]
+SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_unt.cu", "until.cu", "smooth.cu", "mining.cu"]
+# (object name, source, defines): fg_reg_inst.cu once per tile width and direction
+VARIANTS = [(f"fg_reg_{'b' if bwd else 'f'}{nw}", "fg_reg_inst.cu", [f"-DREG_NW={nw}", f"-DREG_BWD={bwd}"])
+            for bwd in (1, 0) for nw in (4, 5, 6, 7, 8)]
 HEADERS = ["common.cuh", "kernels.cuh", "fg_reg.cuh", "fg_cav.cuh"]
+UNITS = [(os.path.splitext(s)[0], s, []) for s in SOURCES] + VARIANTS
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -35,7 +39,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "stlg.h")]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS + ["fg_reg_inst.cu"]] + [os.path.join(INCLUDE, "stlg.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -53,16 +57,30 @@ def build(force: bool = False, verbose: bool = True, out: str | None = None, ext
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)] + list(extra or [])
 
-    def compile_one(src):
-        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
-        cmd = [_nvcc(), *compile_flags, "-I", INCLUDE, "-c", "-o", obj, os.path.join(CSRC, src)]
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+    hdr_t = max(hdr_t, os.path.getmtime(os.path.join(INCLUDE, "stlg.h")), os.path.getmtime(__file__))
+    import time
+
+    def compile_one(unit):
+        name, src, defs = unit
+        obj = os.path.join(objdir, name + ".o")
+        srcp = os.path.join(CSRC, src)
+        # incremental: an object newer than its source, every header and this file is kept
+        # (force=True rebuilds everything)
+        if (not force and out is None and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(srcp), hdr_t)):
+            return obj
+        cmd = [_nvcc(), *compile_flags, *defs, "-I", INCLUDE, "-c", "-o", obj, srcp]
         if verbose:
             print(" ".join(cmd), flush=True)
+        t0 = time.time()
         subprocess.run(cmd, check=True)
+        if verbose:
+            print(f"  {name}: {time.time() - t0:.0f} s", flush=True)
         return obj
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    with ThreadPoolExecutor(max_workers=min(len(UNITS), os.cpu_count() or 8)) as ex:
+        objs = list(ex.map(compile_one, sorted(UNITS, key=lambda u: u[1] != "fg_reg_inst.cu")))
     tmp = lib_out + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs]

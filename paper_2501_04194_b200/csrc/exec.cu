@@ -470,7 +470,8 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     // 2^{tau2 (u - M)} do not inherit the fp32 rounding of M amplified by tau
     if ((cfg->mode == STLG_MODE_SOFTMAX &&
          (e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED || e.kind == E_FG_SMOOTH)) ||
-        (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_TIMED))
+        (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_TIMED) ||
+        (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_UNTIMED && !cfg->masked_fill))
       e.aux_slot = plan->n_aux++;
     e.out_slot = (i == root) ? -1 : C.new_slot();
     C.slot_of[i] = e.out_slot;

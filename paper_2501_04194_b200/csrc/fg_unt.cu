@@ -85,10 +85,15 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
     for (int w = UN_NW - 1; w > 0; --w)
       if (w > warp) cw = rcomb<RK>(WS[w], cw, tau2);
     const RSt cin = lane < 31 ? rcomb<RK>(ex, cw, tau2) : cw;
+    float lo[RK == RK_LSE ? RG_EPT : 1];
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) {
       const RSt o = rcomb<RK>(S[k], cin, tau2);
-      const float val = (RK == RK_HARDV) ? o.m : fmaf(lg2f(o.s), itau2, o.m);
+      const float l2 = (RK == RK_HARDV) ? 0.f : lg2f(o.s);
+      const float val = (RK == RK_HARDV) ? o.m : fmaf(l2, itau2, o.m);
+      // LSE: residual of the fp32 trace (double-float M = val + lo, as k_cav_fwd), so the
+      // backward's weights 2^{tau2 (u - M)} do not inherit tau |M| eps32
+      if (RK == RK_LSE) lo[k] = sg * fmaf(l2, itau2, o.m - val);
       P[q0 + k] = sg * val;  // own slots: read by the coalesced store after the barrier
     }
     {
@@ -103,6 +108,16 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < nt) op[k * T] = src[k * SS];
+    if (RK == RK_LSE && p.aux != nullptr) {  // the low words leave through the same buffer
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < RG_EPT; ++k) P[q0 + k] = lo[k];
+      __syncthreads();
+      float* ap = p.aux + row * L + c0 + tid;
+#pragma unroll
+      for (int k = 0; k < RG_EPT; ++k)
+        if (tid + k * T < nt) ap[k * T] = src[k * SS];
+    }
   }
 }
 
@@ -122,6 +137,7 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
+  const float* lor = p.aux_in != nullptr ? p.aux_in + row * L : nullptr;  // trace low word
   Ev<M_LSE, EK> ev(p.child, row, p.mp);
   const RSt id = rident<RK_GLSE>();
   RSt carry = id;  // fold of every output before the current tile
@@ -130,14 +146,19 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
     const int nt = (L - c0 < N) ? L - c0 : N;
 #pragma unroll
     for (int h = 0; h < RG_EPT; h += 8) {
-      float gv[8], mv[8];
+      float gv[8], mv[8], lv[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int t = c0 + tid + (h + k) * T;
         const int tc = t < L ? t : L - 1;
         gv[k] = ld_na(cot + tc);
         mv[k] = ld_na(outr + tc);
+        lv[k] = lor != nullptr ? ld_na(lor + tc) : 0.f;
       }
+      // M = hi + lo: the low word rides in the weight, g 2^{-tau2 lo} (|tau2 lo| << 1)
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (lor != nullptr) gv[k] *= ex2f(-tau2 * sg * lv[k]);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const bool v = tid + (h + k) * T < nt;

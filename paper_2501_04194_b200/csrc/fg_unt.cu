@@ -221,6 +221,177 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
   }
 }
 
+// Untimed hard backward (tape.py:481-491): out[t] routes its cotangent to the FIRST
+// arg-max a(t) of u over [t, L-1].  a(t) is non-decreasing in t and a(i) = i for every
+// target i, so the outputs sending to i form one contiguous run [t_start, i]: with the
+// positions walked in descending t, the run starts at its target and ends at t_start.
+// Every run total is accumulated in fp64 by a segmented scan (threads, warps and the
+// carry of the tiles already done, which lie at larger t) and written ONCE, by the
+// thread that owns the run's last position t_start, through the fused child VJP at i —
+// deterministic (no atomics, no memset, no pointwise pass) and exact to one fp32
+// rounding of the fp64 sum.  Every non-target position gets a zero gradient from its
+// owner, so each gradient element is written exactly once.
+struct HRun {
+  int kf, kl;   // key (arg-max target) at the highest / lowest position of the range
+  double tail;  // cotangent sum of the lowest run of the range (key kl)
+  int whole;    // one key over the whole range
+};
+// hi covers larger t than lo
+__device__ __forceinline__ HRun hrun_comb(HRun hi, HRun lo) {
+  if (hi.kf < 0) return lo;
+  if (lo.kf < 0) return hi;
+  const bool join = lo.whole && lo.kf == hi.kl;
+  return HRun{hi.kf, lo.kl, join ? hi.tail + lo.tail : lo.tail, hi.whole && lo.whole && lo.kf == hi.kl};
+}
+__device__ __forceinline__ HRun hrun_shfl_down(HRun v, int o) {
+  HRun r;
+  r.kf = __shfl_down_sync(0xffffffffu, v.kf, o);
+  r.kl = __shfl_down_sync(0xffffffffu, v.kl, o);
+  r.tail = __shfl_down_sync(0xffffffffu, v.tail, o);
+  r.whole = __shfl_down_sync(0xffffffffu, v.whole, o);
+  return r;
+}
+
+template <int EK>
+__global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constant__ FGParams p) {
+  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
+  __shared__ float U[NP];  // child values (max space), then the arg-max keys
+  __shared__ float G[NP];  // cotangents
+  __shared__ HRun WS[UN_NW];
+  __shared__ RSt WM[UN_NW];
+  const long long row = blockIdx.x;
+  const int L = (int)p.L;
+  const float sg = p.sg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* cot = p.cot + row * L;
+  Ev<M_HARD, EK> ev(p.child, row, p.mp);
+  const RSt idm = rident<RK_HARDI>();
+  RSt mcarry = idm;                 // (max, first arg-max) of every position after the tile
+  HRun rcarry{-1, -1, 0.0, 1};      // run state of every position after the tile
+  const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
+  for (int c0 = ((L - 1) / N) * N; c0 >= 0; c0 -= N) {
+    const int nt = (L - c0 < N) ? L - c0 : N;
+    {
+      const int jb = c0 + tid;
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<M_HARD, EK>::Raw r[8];
+        float gv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = jb + (h + k) * T;
+          const int jc = j < L ? j : L - 1;
+          r[k] = ev.load(jc);
+          gv[k] = ld_na(cot + jc);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = jb + (h + k) * T;
+          U[so + (h + k) * SS] = sg * ev.value(j < L ? j : L - 1, r[k]);
+          G[so + (h + k) * SS] = gv[k];
+        }
+      }
+    }
+    __syncthreads();
+    // suffix first-arg-max over the thread's chunk (ties keep the earlier position)
+    RSt S[RG_EPT];
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k)
+      S[k] = (i0 + k < nt) ? RSt{U[q0 + k], __int_as_float(c0 + i0 + k), 0.f} : idm;
+#pragma unroll
+    for (int k = RG_EPT - 2; k >= 0; --k) S[k] = rcomb<RK_HARDI>(S[k], S[k + 1], 0.f);
+    RSt v = S[0];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      RSt w{__shfl_down_sync(0xffffffffu, v.m, o), __shfl_down_sync(0xffffffffu, v.s, o), 0.f};
+      if (lane + o < 32) v = rcomb<RK_HARDI>(v, w, 0.f);
+    }
+    RSt ex{__shfl_down_sync(0xffffffffu, v.m, 1), __shfl_down_sync(0xffffffffu, v.s, 1), 0.f};
+    if (lane == 0) WM[warp] = v;
+    __syncthreads();
+    RSt cw = mcarry;
+#pragma unroll
+    for (int w = UN_NW - 1; w > 0; --w)
+      if (w > warp) cw = rcomb<RK_HARDI>(WM[w], cw, 0.f);
+    const RSt cin = lane < 31 ? rcomb<RK_HARDI>(ex, cw, 0.f) : cw;
+    int key[RG_EPT];
+    float gk[RG_EPT];
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) {
+      key[k] = (i0 + k < nt) ? __float_as_int(rcomb<RK_HARDI>(S[k], cin, 0.f).s) : -1;
+      gk[k] = G[q0 + k];
+    }
+    {
+      RSt tile = WM[UN_NW - 1];
+#pragma unroll
+      for (int w = UN_NW - 2; w >= 0; --w) tile = rcomb<RK_HARDI>(WM[w], tile, 0.f);
+      mcarry = rcomb<RK_HARDI>(tile, mcarry, 0.f);
+    }
+    // the thread's run state over its chunk, then the segmented scan over later threads
+    HRun mine{-1, -1, 0.0, 1};
+#pragma unroll
+    for (int k = RG_EPT - 1; k >= 0; --k)
+      if (key[k] >= 0) mine = hrun_comb(mine, HRun{key[k], key[k], (double)gk[k], 1});
+    HRun rv = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      HRun w = hrun_shfl_down(rv, o);
+      if (lane + o < 32) rv = hrun_comb(w, rv);
+    }
+    HRun rex = hrun_shfl_down(rv, 1);
+    if (lane == 31) rex = HRun{-1, -1, 0.0, 1};
+    if (lane == 0) WS[warp] = rv;
+    __syncthreads();  // WS / WM visible; U / G reads done (keys go into U below)
+    HRun rw = rcarry;  // later tiles, then the later warps of this tile, in descending t
+#pragma unroll
+    for (int w = UN_NW - 1; w > 0; --w)
+      if (w > warp) rw = hrun_comb(rw, WS[w]);
+    const HRun prev = hrun_comb(rw, rex);  // everything at larger t than the thread's chunk
+    {
+      HRun tile = WS[UN_NW - 1];
+#pragma unroll
+      for (int w = UN_NW - 2; w >= 0; --w) tile = hrun_comb(tile, WS[w]);
+      rcarry = hrun_comb(rcarry, tile);
+    }
+    // walk the chunk downwards; a run that ends here (the next lower position has another
+    // key) is complete: write its total at its target through the child VJP
+    int pk = prev.kl;
+    double ps = prev.tail;
+#pragma unroll
+    for (int k = RG_EPT - 1; k >= 0; --k) {
+      if (key[k] < 0) continue;
+      if (key[k] != pk) {
+        if (pk >= 0) ev.grad(pk, ev.load(pk), (float)ps);
+        pk = key[k];
+        ps = 0.0;
+      }
+      ps += (double)gk[k];
+      U[q0 + k] = __int_as_float(key[k]);
+    }
+    if (c0 == 0 && tid == 0 && pk >= 0) ev.grad(pk, ev.load(pk), (float)ps);  // row start
+    __syncthreads();
+    // zero gradient at every non-target position (coalesced)
+    {
+      const int jb = c0 + tid;
+#pragma unroll
+      for (int h = 0; h < RG_EPT; h += 8) {
+        typename Ev<M_HARD, EK>::Raw r[8];
+        bool z[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = jb + (h + u) * T;
+          z[u] = tid + (h + u) * T < nt && __float_as_int(U[so + (h + u) * SS]) != j;
+          if (z[u]) r[u] = ev.load(j);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z[u]) ev.grad(jb + (h + u) * T, r[u], 0.f);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 #define UNT_DISPATCH_EK(EKV, ...)      \
   if ((EKV) == EK_AFF1) {              \
     constexpr int EK = EK_AFF1;        \
@@ -257,11 +428,15 @@ bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   return true;
 }
 
-// register-blocked untimed LSE backward (no masked_fill); false: not handled
+// register-blocked untimed backward, LSE and hard (no masked_fill); false: not handled
 bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
-  if (p.fill || mode != M_LSE || p.L >= (1LL << 30)) return false;
+  if (p.fill || (mode != M_LSE && mode != M_HARD) || p.L >= (1LL << 30)) return false;
   const int ek = expr_kind(p.child);
-  UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
+  if (mode == M_HARD) {
+    UNT_DISPATCH_EK(ek, (k_unt_bwd_hard<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
+  } else {
+    UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
+  }
   count_launch();
   err = cudaGetLastError();
   return true;

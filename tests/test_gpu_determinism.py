@@ -1,0 +1,55 @@
+"""Bitwise reproducibility of the backward under a general (random) cotangent
+(SURVEY §7.6): two runs on the same inputs must give identical
+gradients and d(a, b, c) — no float atomics whose order varies between runs on any
+path a general cotangent flows through.  The multi-GPU all-reduce sums these
+per-rank partials, so they must be reproducible first."""
+
+import numpy as np
+import pytest
+
+import paper_2501_04194_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+SI = P.SmoothInterval(0.3, 0.65, 9.0)
+CASES = [
+    ("F_untimed_hard", P.Eventually(P.Pred("x", ">", 0.0)), P.Hard()),
+    ("G_untimed_lse", P.Always(P.Pred("x", ">", 0.0)), P.LogSumExp(5.0)),
+    ("F_timed_hard", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(3, 60)), P.Hard()),
+    ("G_timed_lse", P.Always(P.Pred("x", ">", 0.0), P.StepInterval(0, 40)), P.LogSumExp(5.0)),
+    ("F_timed_soft", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(2, 30)), P.SoftMax(2.0)),
+    ("U_untimed_hard", P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0)), P.Hard()),
+    ("U_timed_hard", P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0), P.StepInterval(0, 20)), P.Hard()),
+    ("U_timed_lse", P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0), P.StepInterval(1, 20)), P.LogSumExp(3.0)),
+    ("U_untimed_lse", P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0)), P.LogSumExp(3.0)),
+    ("G_smooth_lse", P.Always(P.Pred("x", ">", 0.0), SI), P.LogSumExp(5.0)),
+    ("F_smooth_soft", P.Eventually(P.Pred("x", ">", 0.0), SI), P.SoftMax(2.0)),
+    ("nested_hard", P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 30))),
+                          P.Until(P.Pred("y", "<", 1.0), P.Pred("x", ">", 0.0))), P.Hard()),
+]
+
+
+@pytest.mark.parametrize("name,f,mode", CASES, ids=[c[0] for c in CASES])
+def test_backward_bitwise_reproducible(cuda, name, f, mode):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(5)
+    B, T = 64, 1500
+    x = torch.randn(B, T, device="cuda", generator=g)
+    y = torch.randn(B, T, device="cuda", generator=g)
+    if "hard" in name:  # ties, so the first-arg-max runs are long and cross tiles
+        x, y = torch.round(x * 2), torch.round(y * 2)
+    cot = torch.randn(B, T, device="cuda", generator=g)
+    names = sorted(P.variables(f))
+    runs = []
+    for _ in range(2):
+        chans = {"x": x.clone().requires_grad_(True), "y": y.clone().requires_grad_(True)}
+        chans = {k: chans[k] for k in names}
+        smooth = "smooth" in name
+        abc = tuple(torch.tensor(v, dtype=torch.float64, device="cuda", requires_grad=True)
+                    for v in (SI.a, SI.b, SI.c)) if smooth else None
+        out = P.trace(f, chans, P.SemanticsConfig(mode=mode), smooth_binding=abc)
+        leaves = list(chans.values()) + (list(abc) if abc else [])
+        grads = torch.autograd.grad(out, leaves, cot)
+        runs.append([t.detach().cpu().numpy() for t in (out, *grads)])
+    for a, b in zip(*runs):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), name

@@ -272,6 +272,8 @@ struct Bufs {
   float* tables;  // n_tables * 2T (log2 smooth weights, log2 suffix sums)
   float* gslots;  // n_slots * B * T (backward)
   float* scratch; // 3 * B * T (backward)
+  double* dw64;    // [T] d out / d w_i (smooth backward)
+  double* dwpart;  // [smooth_dw_parts(B), T] its per-row-tile partials
   float* uslab;   // Until backward checkpoint slab (persistent kernel)
   long long BT;
   float* slot(int s) const { return slots + (long long)s * BT; }
@@ -522,6 +524,14 @@ static size_t until_slab_bytes(const stlg_plan* plan, long long T) {
   return align256(m);
 }
 
+// d/dw region of the backward workspace: dw64 [T] plus, for plans with a smooth interval,
+// the per-row-tile partials [smooth_dw_parts(B), T] of the deterministic d/dw pass
+static size_t dw_bytes(const stlg_plan* plan, long long B, long long T) {
+  size_t b = align256(sizeof(double) * (size_t)T);
+  if (plan->n_tables > 0) b += align256(sizeof(double) * (size_t)smooth_dw_parts(B) * (size_t)T);
+  return b;
+}
+
 int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fwd_bytes,
                          size_t* bwd_bytes) {
   if (!plan) return fail(STLG_E_INVALID, "null plan");
@@ -532,7 +542,7 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + 256;
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
-                 align256(sizeof(float) * 3 * (size_t)BT) + align256(sizeof(double) * (size_t)T) +
+                 align256(sizeof(float) * 3 * (size_t)BT) + dw_bytes(plan, B, T) +
                  until_slab_bytes(plan, T) + 1024;
   return STLG_OK;
 }
@@ -553,13 +563,15 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.gslots = nullptr;
   bf.scratch = nullptr;
   bf.uslab = nullptr;
+  bf.dw64 = bf.dwpart = nullptr;
   if (bwd_ws) {
     if (bwd_bytes < need_b) return fail(STLG_E_INVALID, "backward workspace too small");
     uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
     bf.gslots = (float*)bb;
     bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
-    bf.uslab = (float*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT) +
-                        align256(sizeof(double) * (size_t)T) + 256);
+    bf.dw64 = (double*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT));
+    bf.dwpart = bf.dw64 + align256(sizeof(double) * (size_t)T) / sizeof(double);
+    bf.uslab = (float*)((uintptr_t)bf.dw64 + dw_bytes(plan, B, T) + 256);
   }
   return STLG_OK;
 }
@@ -645,11 +657,8 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
   p.aux_in = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
   p.cot = cot;
   p.gbuf = bf.scratch;
-  p.dw64 = d_smooth ? dw64 : nullptr;
-  if (d_smooth) {
-    ce = cudaMemsetAsync(dw64, 0, sizeof(double) * (size_t)T, st);
-    if ((rc = cuda_status(ce, "memset"))) return rc;
-  }
+  p.dw64 = d_smooth ? dw64 : nullptr;  // every entry written by k_smooth_dw_reduce
+  p.dwpart = bf.dwpart;
   if ((rc = cuda_status(launch_smooth_bwd(mode, p, st), "smooth backward launch"))) return rc;
   if (d_smooth) {
     ce = launch_smooth_abc(dw64, tab, T, sp.a, sp.b, sp.c, sp.eps, d_smooth + 3 * e.smooth_slot, st);
@@ -773,7 +782,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH
       if ((rc = run_smooth(plan, e, channels, d_channels, B, T, smooth_params, bf, nullptr, out_in,
-                           g, d_smooth, (double*)(((uintptr_t)(bf.scratch + 3 * bf.BT) + 7) & ~(uintptr_t)7), st, true)))
+                           g, d_smooth, bf.dw64, st, true)))
         return rc;
     }
     if ((rc = cuda_status(ce, "backward launch"))) return rc;

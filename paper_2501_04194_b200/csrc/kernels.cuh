@@ -56,7 +56,8 @@ struct SParams {
   float* out;
   float* aux;          // forward, softmax
   const float* lw2;    // log2 w_i (fp32; -inf where w_i == 0), i = 0..L-1
-  double* dw64;        // backward: d out / d w_i summed over rows and t [L] (fp64, accumulated)
+  double* dw64;        // backward: d out / d w_i summed over rows and t [L] (fp64)
+  double* dwpart;      // backward: per-row-tile partials of dw64 [smooth_dw_parts(B), L]
   float* gbuf;         // backward scratch: cotangent of the child [B, L]
   long long B, L;
   int i_lo, i_hi;      // kept index range {i : w_i > 0}
@@ -65,6 +66,11 @@ struct SParams {
   float pad_value;
   ModeP mp;
 };
+
+// rows per CTA of the d/dw pass; each CTA writes one partial row of d out / d w_i and a
+// second pass sums the partials in a fixed order (deterministic d(a, b, c))
+constexpr int SMOOTH_RP = 4;
+inline long long smooth_dw_parts(long long B) { return (B + SMOOTH_RP - 1) / SMOOTH_RP; }
 
 // fp64 weight table and its (a, b, c) partials -> d_abc (one smooth slot)
 cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,

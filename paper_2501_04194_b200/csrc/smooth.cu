@@ -24,7 +24,7 @@ namespace stlg {
 
 constexpr int S_T = 256;    // outputs (or child elements) per CTA
 constexpr int S_CH = 1024;  // window offsets staged per chunk
-constexpr int S_RP = 8;     // rows per CTA in the d/dw pass
+constexpr int S_RP = SMOOTH_RP;  // rows per CTA in the d/dw pass (kernels.cuh)
 
 // ---------------------------------------------------------------------------
 // forward
@@ -356,14 +356,13 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
   __shared__ __align__(16) float Gt[S_T];
   __shared__ __align__(16) float Mt[S_T];
   __shared__ float Lt[S_T];
-  __shared__ float Rw[4][S_T / 32];
+  __shared__ float Rw[5][S_T / 32];
+  __shared__ double red[S_CH];
   const int L = (int)p.L;
-  const int t0 = blockIdx.x * S_T;
   const int K = p.i_hi - p.i_lo + 1;
   const float sg = p.sg, tau2 = p.mp.tau2, itau = 1.f / p.mp.tau;
-  const long long r0 = (long long)blockIdx.y * S_RP;
+  const long long r0 = (long long)blockIdx.x * S_RP;
   const long long r1 = min(r0 + S_RP, p.B);
-  const int nt = min(S_T, L - t0);
   for (int k0 = 0; k0 < K; k0 += S_CH) {
     const int kc = min(S_CH, K - k0);
     // each thread owns offsets i = i_lo + k0 + k, k = threadIdx.x + S_T * c
@@ -382,7 +381,10 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       const int k = 4 * (int)threadIdx.x + r;
       lwf[r] = k < kc ? p.lw2[p.i_lo + k0 + k] : -INFINITY;
     }
+    // the CTA walks every output tile of its rows: one partial row per CTA
+    for (int t0 = 0; t0 < L; t0 += S_T)
     for (long long row = r0; row < r1; ++row) {
+      const int nt = min(S_T, L - t0);
       const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
       const int base = t0 + p.i_lo + k0;
       for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) {
@@ -407,43 +409,58 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
         // A_t = g_t 2^{tau2 (Mmax - M_t)} in [1, 2^100] |g| and E_j = 2^{tau2 (u_j - umax)} in
         // [2^-100, 1]: no factor or product leaves the fp32 range, so one ex2 per staged
         // element and one FMA per pair replace the per-pair ex2
-        float umx = -INFINITY, umn = INFINITY, mmx = -INFINITY, mmn = INFINITY;
+        // |g| enters through a power-of-two scale 2^-ge (exact), so A_t stays within
+        // [2^-1, 2^100] for every cotangent magnitude and ge is added back in fp64
+        float umx = -INFINITY, umn = INFINITY, mmx = -INFINITY, mmn = INFINITY, gmx = 0.f;
+        bool bad = false;  // NaN child samples: the exact path (fmaxf / fminf drop NaN)
         for (int q = threadIdx.x; q < nt + kc - 1; q += S_T) {
           umx = fmaxf(umx, U[q]);
           umn = fminf(umn, U[q]);
+          bad |= U[q] != U[q];
         }
-        if (threadIdx.x < nt && Gt[threadIdx.x] != 0.f) mmx = mmn = Mt[threadIdx.x];
+        if (threadIdx.x < nt && Gt[threadIdx.x] != 0.f) {
+          mmx = mmn = Mt[threadIdx.x];
+          gmx = fabsf(Gt[threadIdx.x]);
+        }
         for (int o = 16; o > 0; o >>= 1) {
           umx = fmaxf(umx, __shfl_xor_sync(0xffffffffu, umx, o));
           umn = fminf(umn, __shfl_xor_sync(0xffffffffu, umn, o));
           mmx = fmaxf(mmx, __shfl_xor_sync(0xffffffffu, mmx, o));
           mmn = fminf(mmn, __shfl_xor_sync(0xffffffffu, mmn, o));
+          gmx = fmaxf(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
         }
         if ((threadIdx.x & 31) == 0) {
           Rw[0][threadIdx.x >> 5] = umx;
           Rw[1][threadIdx.x >> 5] = umn;
           Rw[2][threadIdx.x >> 5] = mmx;
           Rw[3][threadIdx.x >> 5] = mmn;
+          Rw[4][threadIdx.x >> 5] = gmx;
         }
-        __syncthreads();
-        umx = Rw[0][0], umn = Rw[1][0], mmx = Rw[2][0], mmn = Rw[3][0];
+        bad = __syncthreads_or(bad);
+        umx = Rw[0][0], umn = Rw[1][0], mmx = Rw[2][0], mmn = Rw[3][0], gmx = Rw[4][0];
         for (int w = 1; w < S_T / 32; ++w) {
           umx = fmaxf(umx, Rw[0][w]);
           umn = fminf(umn, Rw[1][w]);
           mmx = fmaxf(mmx, Rw[2][w]);
           mmn = fminf(mmn, Rw[3][w]);
+          gmx = fmaxf(gmx, Rw[4][w]);
         }
-        if (tau2 * (umx - umn) <= 100.f && tau2 * (mmx - mmn) <= 100.f && mmx > -INFINITY) {  // NaN / inf / no g -> exact
+        // (a NaN / inf span fails the comparisons: exact path)
+        if (!bad && tau2 * (umx - umn) <= 100.f && tau2 * (mmx - mmn) <= 100.f && mmx > -INFINITY &&
+            gmx > 0.f && gmx < INFINITY) {
           __syncthreads();  // every thread has read Rw; U / Gt are rewritten below
           // E in place; zeros past the staged range (read by the 4-wide loads, times A = 0)
           for (int q = threadIdx.x; q < S_T + S_CH; q += S_T)
             U[q] = q < nt + kc - 1 ? ex2f(tau2 * (U[q] - umx)) : 0.f;
+          int ge;
+          frexpf(gmx, &ge);  // gmx in [2^(ge-1), 2^ge)
           if (threadIdx.x < S_T) {
             const float g = Gt[threadIdx.x];
-            Gt[threadIdx.x] = (threadIdx.x < nt && g != 0.f) ? g * ex2f(tau2 * (mmx - Mt[threadIdx.x])) : 0.f;
+            Gt[threadIdx.x] = (threadIdx.x < nt && g != 0.f)
+                                  ? ldexpf(g, -ge) * ex2f(tau2 * (mmx - Mt[threadIdx.x])) : 0.f;
           }
           __syncthreads();
-          const double cexp = (double)tau2 * ((double)umx - (double)mmx);
+          const double cexp = (double)tau2 * ((double)umx - (double)mmx) + (double)ge;
           // register-blocked: thread owns offsets 4 tid .. 4 tid + 3; per 4 outputs one
           // broadcast LDS.128 of A and two conflict-free LDS.128 of E feed 16 FMAs
           const int kq = 4 * threadIdx.x;
@@ -502,23 +519,45 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
       }
       __syncthreads();
     }
+    // the CTA's partial row, combined in a fixed order (exact-path owner, then the
+    // factorised-path owner of each offset): no atomics, reproducible d(a, b, c)
+    for (int q = threadIdx.x; q < kc; q += S_T) red[q] = 0.0;
+    __syncthreads();
 #pragma unroll
     for (int c = 0; c < S_CH / S_T; ++c) {
-      int k = threadIdx.x + S_T * c;
-      if (k >= kc) break;
-      int i = p.i_lo + k0 + k;
-      if (p.lw2[i] == -INFINITY) continue;
-      double v = (double)sg * acc[c] * (MODE == M_LSE ? (double)itau : 1.0);
-      if (v != 0.0) atomicAdd(p.dw64 + i, v);
+      const int k = threadIdx.x + S_T * c;
+      if (k < kc) red[k] += (double)sg * acc[c] * (MODE == M_LSE ? (double)itau : 1.0);
     }
+    __syncthreads();
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int k = 4 * (int)threadIdx.x + r;
-      if (k >= kc || accf[r] == 0.0) continue;
-      const int i = p.i_lo + k0 + k;
-      if (p.lw2[i] == -INFINITY) continue;
-      atomicAdd(p.dw64 + i, (double)sg * accf[r] * (double)itau);
+      if (k < kc) red[k] += (double)sg * accf[r] * (double)itau;
     }
+    __syncthreads();
+    double* part = p.dwpart + (long long)blockIdx.x * L + p.i_lo + k0;
+    for (int q = threadIdx.x; q < kc; q += S_T) part[q] = p.lw2[p.i_lo + k0 + q] == -INFINITY ? 0.0 : red[q];
+    __syncthreads();
+  }
+}
+
+// dw64[i] = sum over the partial rows in a fixed order (32 offsets x 8 partial strides
+// per CTA, then a fixed-shape tree): deterministic
+__global__ void __launch_bounds__(256) k_smooth_dw_reduce(const double* __restrict__ part, long long parts,
+                                                          long long L, int i_lo, int i_hi, double* dw64) {
+  __shared__ double s[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (i >= i_lo && i <= i_hi)
+    for (long long q = w; q < parts; q += 8) acc += part[q * L + i];
+  s[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && i < L) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += s[k][lane];
+    dw64[i] = t;
   }
 }
 
@@ -602,9 +641,13 @@ cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st) {
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (p.dw64 != nullptr) {
-    dim3 g2((unsigned)((p.L + S_T - 1) / S_T), (unsigned)((p.B + S_RP - 1) / S_RP));
-    if (mode == M_LSE) k_smooth_bwd_w<M_LSE><<<g2, S_T, 0, st>>>(p);
-    else k_smooth_bwd_w<M_SOFT><<<g2, S_T, 0, st>>>(p);
+    const long long parts = smooth_dw_parts(p.B);
+    if (mode == M_LSE) k_smooth_bwd_w<M_LSE><<<(unsigned)parts, S_T, 0, st>>>(p);
+    else k_smooth_bwd_w<M_SOFT><<<(unsigned)parts, S_T, 0, st>>>(p);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_smooth_dw_reduce<<<(unsigned)((p.L + 31) / 32), 256, 0, st>>>(p.dwpart, parts, p.L, p.i_lo, p.i_hi,
+                                                                     p.dw64);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -195,7 +195,8 @@ class _TraceFn(torch.autograd.Function):
         d_total = None
         for (r0, r1), fws, bb in zip(_row_chunks(B), fws_list, ctx.bwd_bytes):
             d_smooth = None
-            if comp.n_smooth:
+            # the d/dw pass runs only when a bound (a, b, c) tensor asks for its gradient
+            if comp.n_smooth and ctx.needs_input_grad[2]:
                 d_smooth = torch.zeros(3 * comp.n_smooth, dtype=torch.float64, device=dev)
             bws = torch.empty(bb, dtype=torch.uint8, device=dev)
             comp.backward([c[r0:r1] for c in chans], ctx.params, out[r0:r1], g[r0:r1],

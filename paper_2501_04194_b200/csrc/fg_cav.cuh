@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   const int s0 = t0 + p.a;
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   const float czero = p.canon ? 0.f : -0.f;  // x + (-0) == x for every x: canon is one add
+  (void)d, (void)c, (void)tau2, (void)itau2;  // unused by some instantiations
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   float* outr = p.out + row * L;

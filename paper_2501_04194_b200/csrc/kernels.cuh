@@ -72,6 +72,11 @@ struct SParams {
 constexpr int SMOOTH_RP = 4;
 inline long long smooth_dw_parts(long long B) { return (B + SMOOTH_RP - 1) / SMOOTH_RP; }
 
+// hard timed Until in O(T) (until_ht.cu): applicability, forward, backward into gl / gr
+bool until_ht_applicable(const UParams& p);
+cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st);
+cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st);
+
 // fp64 weight table and its (a, b, c) partials -> d_abc (one smooth slot)
 cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,
                               double c, double eps, double* d_abc, cudaStream_t st);

@@ -1213,6 +1213,7 @@ size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int
 
 template <int MODE>
 static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
+  if (MODE == M_HARD && until_ht_applicable(p)) return launch_until_ht_fwd(p, st);  // O(T), until_ht.cu
   if (p.untimed && MODE == M_HARD && !p.fill) {
     k_until_unt_hard_fwd<MODE><<<(unsigned)p.B, UH_T, 0, st>>>(p);
     count_launch();
@@ -1244,6 +1245,9 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   cudaError_t e;
+  if (MODE == M_HARD && until_ht_applicable(p)) {  // O(T), deterministic (until_ht.cu)
+    if ((e = launch_until_ht_bwd(p, st)) != cudaSuccess) return e;
+  } else {
   if ((e = cudaMemsetAsync(p.gl, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p.gr, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
@@ -1283,6 +1287,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   }
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   // child VJPs from the accumulated cotangents (left first: first-writer order)
   FGParams q;
   memset(&q, 0, sizeof(q));

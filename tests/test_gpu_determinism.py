@@ -50,6 +50,6 @@ def test_backward_bitwise_reproducible(cuda, name, f, mode):
         out = P.trace(f, chans, P.SemanticsConfig(mode=mode), smooth_binding=abc)
         leaves = list(chans.values()) + (list(abc) if abc else [])
         grads = torch.autograd.grad(out, leaves, cot)
-        runs.append([t.detach().cpu().numpy() for t in (out, *grads)])
+        runs.append([np.atleast_1d(t.detach().cpu().numpy()) for t in (out, *grads)])
     for a, b in zip(*runs):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), name

@@ -225,3 +225,28 @@ def test_c5_untimed_until_T30k_hard(cuda):
     assert_hard_equal(tr[r:r + 1], ref.astype(np.float32))
     np.testing.assert_array_equal(g["x"][r:r + 1], dl)
     np.testing.assert_array_equal(g["y"][r:r + 1], dr)
+
+
+@pytest.mark.parametrize("pad", ["last", "const"])
+@pytest.mark.parametrize("a,K,L", [(0, 1, 50), (0, 2, 300), (1, 5, 300), (3, 64, 1500), (0, 101, 1500),
+                                   (17, 101, 2500), (2, 300, 5000), (40, 7, 900), (0, 1100, 2600)])
+def test_hard_timed_until_sweep(cuda, a, K, L, pad):
+    """O(T) hard timed Until (csrc/until_ht.cu) vs the oracle: tie-heavy inputs (integers
+    and signed zeros), left- and right-sourced outputs, overrun tails, both paddings,
+    values bit-exact and gradients exact (ones) / 1e-6 (random cotangent)."""
+    rng = np.random.default_rng(a * 1000 + K + L + (pad == "last"))
+    x, y = _ties(rng, (2, L), 3), _ties(rng, (2, L), 3)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", "<", 0.5), P.StepInterval(a, a + K - 1))
+    padding = P.PaddingPolicy.last_value() if pad == "last" else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(padding=padding)
+    arrays = {"x": x.astype(np.float64), "y": y.astype(np.float64)}
+    tr, g = _run(f, {"x": x, "y": y}, cfg)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, arrays, cfg)
+    assert_hard_equal(tr, ref_tr.astype(np.float32))
+    for k in ("x", "y"):
+        np.testing.assert_array_equal(g[k], ref_g[k])
+    cot = np.asarray(rng.normal(0, 1, (2, L)), dtype=np.float32)
+    _, g2 = _run(f, {"x": x, "y": y}, cfg, cot)
+    _, ref_g2, _ = stl_oracle.trace_and_grad(f, arrays, cfg, cot.astype(np.float64))
+    for k in ("x", "y"):
+        assert rel_err(g2[k], ref_g2[k]) <= 1e-6, k

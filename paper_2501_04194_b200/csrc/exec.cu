@@ -274,6 +274,8 @@ struct Bufs {
   float* scratch; // 3 * B * T (backward)
   double* dw64;    // [T] d out / d w_i (smooth backward)
   double* dwpart;  // [smooth_dw_parts(B), T] its per-row-tile partials
+  unsigned long long* dacc;  // [4][B, T] reproducible Until accumulators
+  int* dscale;               // [B] their per-row grid exponents
   float* uslab;   // Until backward checkpoint slab (persistent kernel)
   long long BT;
   float* slot(int s) const { return slots + (long long)s * BT; }
@@ -532,6 +534,17 @@ static size_t dw_bytes(const stlg_plan* plan, long long B, long long T) {
   return b;
 }
 
+// reproducible Until accumulators (detacc.cuh): 4 int64 planes [B, T] + per-row exponents
+static bool plan_has_until(const stlg_plan* plan) {
+  for (const Entry& e : plan->entries)
+    if (e.kind == E_UNTIL) return true;
+  return false;
+}
+static size_t det_bytes(const stlg_plan* plan, long long B, long long T) {
+  if (!plan_has_until(plan)) return 0;
+  return align256(sizeof(unsigned long long) * 4 * (size_t)B * (size_t)T) + align256(sizeof(int) * (size_t)B);
+}
+
 int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fwd_bytes,
                          size_t* bwd_bytes) {
   if (!plan) return fail(STLG_E_INVALID, "null plan");
@@ -543,7 +556,7 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
                  align256(sizeof(float) * 3 * (size_t)BT) + dw_bytes(plan, B, T) +
-                 until_slab_bytes(plan, T) + 1024;
+                 det_bytes(plan, B, T) + until_slab_bytes(plan, T) + 1024;
   return STLG_OK;
 }
 
@@ -564,6 +577,8 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.scratch = nullptr;
   bf.uslab = nullptr;
   bf.dw64 = bf.dwpart = nullptr;
+  bf.dacc = nullptr;
+  bf.dscale = nullptr;
   if (bwd_ws) {
     if (bwd_bytes < need_b) return fail(STLG_E_INVALID, "backward workspace too small");
     uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
@@ -571,7 +586,12 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
     bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
     bf.dw64 = (double*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT));
     bf.dwpart = bf.dw64 + align256(sizeof(double) * (size_t)T) / sizeof(double);
-    bf.uslab = (float*)((uintptr_t)bf.dw64 + dw_bytes(plan, B, T) + 256);
+    uintptr_t dp = (uintptr_t)bf.dw64 + dw_bytes(plan, B, T);
+    if (plan_has_until(plan)) {
+      bf.dacc = (unsigned long long*)dp;
+      bf.dscale = (int*)(dp + align256(sizeof(unsigned long long) * 4 * (size_t)BT));
+    }
+    bf.uslab = (float*)(dp + det_bytes(plan, B, T) + 256);
   }
   return STLG_OK;
 }
@@ -778,6 +798,8 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.fill = plan->cfg.masked_fill;
       p.sent = (float)plan->cfg.sentinel;
       p.scratch = bf.uslab;
+      p.dacc = bf.dacc;
+      p.dscale = bf.dscale;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH

@@ -44,6 +44,8 @@ struct UParams {
   int fill;    // masked_fill compat: sentinel-filled columns, no overrun rule (masking.py:261-270)
   float sent;  // SemanticsConfig.sentinel
   float* scratch;  // backward: per-thread checkpoint slab of the persistent kernel (or null)
+  unsigned long long* dacc;  // backward: reproducible accumulators [4][B, L] (detacc.cuh)
+  int* dscale;               // backward: per-row grid exponents [B]
   ModeP mp;
 };
 

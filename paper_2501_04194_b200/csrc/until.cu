@@ -25,6 +25,7 @@
 //     backward finds each output's gradient source locally (terminator test
 //     with the stored out[t+1]) and sums cotangents over runs — no atomics,
 //     the child VJPs are fused.
+#include "detacc.cuh"
 #include "kernels.cuh"
 
 namespace stlg {
@@ -283,7 +284,7 @@ struct Systolic {
     cur = -1;
   }
   // called by all 32 lanes with the same k (warp-uniform); dst = row base pointer
-  __device__ __forceinline__ void step(float val, long long base, int k, float* dst, long long L) {
+  __device__ __forceinline__ void step(float val, long long base, int k, const DetRow& dst, long long L) {
     const int lane = threadIdx.x & 31;
     int src = (lane - k) & 31;
     float got = __shfl_sync(0xffffffffu, val, src);
@@ -298,13 +299,13 @@ struct Systolic {
   // padded positions (masked_fill windows past the end) feed element L - 1 under
   // 'last' padding (pad_last is set by the caller) and nothing under a constant pad
   int pad_last = 0;
-  __device__ __forceinline__ void put(float* dst, long long L) {
+  __device__ __forceinline__ void put(const DetRow& dst, long long L) {
     if (cur >= 0 && acc != 0.f) {
-      if (cur < L) atomicAdd(dst + cur, acc);
-      else if (pad_last) atomicAdd(dst + L - 1, acc);
+      if (cur < L) dst.add(cur, acc);
+      else if (pad_last) dst.add(L - 1, acc);
     }
   }
-  __device__ __forceinline__ void flush(float* dst, long long L) {
+  __device__ __forceinline__ void flush(const DetRow& dst, long long L) {
     put(dst, L);
     reset();
   }
@@ -350,8 +351,9 @@ __device__ __forceinline__ void until_bwd_tile(const UParams& p, long long row, 
   const int tid = threadIdx.x;
   const long long t = t0 + tid;
   const bool active = t < nvalid;
-  float* gl = p.gl + row * L;
-  float* gr = p.gr + row * L;
+  const long long BL = p.B * L;
+  const DetRow gl = det_row(p.dacc, p.dacc + BL, p.dscale, row, L);
+  const DetRow gr = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L);
   const float* cot = p.cot + row * L;
   if (t0 < L) {
     // overrun outputs route to the pad sources (last padding): left if pl <= pr
@@ -360,7 +362,7 @@ __device__ __forceinline__ void until_bwd_tile(const UParams& p, long long row, 
       if (g != 0.f) {
         float pl = expr_eval<MODE>(p.left, row, L - 1, p.mp);
         float pr = expr_eval<MODE>(p.right, row, L - 1, p.mp);
-        atomicAdd((pl <= pr ? gl : gr) + (L - 1), g);
+        (pl <= pr ? gl : gr).add(L - 1, g);
       }
     }
   }
@@ -411,7 +413,7 @@ __device__ __forceinline__ void until_bwd_tile(const UParams& p, long long row, 
       if (!p.pad_last) return;
       j = L - 1;
     }
-    atomicAdd(((bsrc & (1 << 30)) ? gr : gl) + j, g);
+    ((bsrc & (1 << 30)) ? gr : gl).add(j, g);
     return;
   }
 
@@ -1019,8 +1021,10 @@ __device__ __forceinline__ void ul_chunk_bwd(const UlStage& S, int c, int n, dou
   }
   Rt64 += (double)rr;
   dtail = dmin;
-  atomicAdd(colP + c * UL_C + lane, warp_colsum(P, wbuf));
-  atomicAdd(colQ + c * UL_C + lane, warp_colsum(Q, wbuf));
+  // per-warp slots (summed in warp order after the stage): no shared float atomics
+  const int w = threadIdx.x >> 5;
+  colP[w * UL_T + c * UL_C + lane] = warp_colsum(P, wbuf);
+  colQ[w * UL_T + c * UL_C + lane] = warp_colsum(Q, wbuf);
 }
 
 // persistent grid; tiles that fail the range check run the per-pair backward with
@@ -1031,7 +1035,7 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
   // transpose tiles [4][32][36] when the tile takes the fast path), then CQ[nch]
   extern __shared__ __align__(16) float dsm[];
   __shared__ UlStage S;
-  __shared__ float colP[UL_T], colQ[UL_T];
+  __shared__ float colP[(UL_T / 32) * UL_T], colQ[(UL_T / 32) * UL_T];  // [warp][column]
   __shared__ float red[8];
   const long long stride = (long long)gridDim.x * U_THREADS;
   UScr scr{p.scratch, dsm, stride, (long long)blockIdx.x * U_THREADS + threadIdx.x, U_THREADS,
@@ -1088,14 +1092,14 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
     double dtail = INFINITY, Rt64 = 0.0;
     int gprev = 0;
     const int nstage = (int)((L - t0 + UL_T - 1) / UL_T);
-    float* gl_row = p.gl + row * L;
-    float* gr_row = p.gr + row * L;
+    const long long BL = p.B * L;
+    const DetRow gl_row = det_row(p.dacc, p.dacc + BL, p.dscale, row, L);
+    const DetRow gr_row = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L);
     for (int s = nstage - 1; s >= 0; --s) {
       const long long k0 = t0 + (long long)s * UL_T;
       __syncthreads();
       ul_stage<true>(p, row, k0, F, S);
-      colP[tid] = 0.f;
-      colQ[tid] = 0.f;
+      for (int q = tid; q < (UL_T / 32) * UL_T; q += UL_T) colP[q] = colQ[q] = 0.f;
       __syncthreads();
       const bool diag = s == 0;
 #pragma unroll 1
@@ -1123,9 +1127,9 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
               pv += __shfl_xor_sync(0xffffffffu, pv, o);
               qv += __shfl_xor_sync(0xffffffffu, qv, o);
             }
-            if (lane == 0) {  // other warps add this chunk's off-diagonal sums concurrently
-              atomicAdd(colP + c * UL_C + k, pv);
-              atomicAdd(colQ + c * UL_C + k, qv);
+            if (lane == 0) {  // this warp's slot of the column (summed in warp order below)
+              colP[w * UL_T + c * UL_C + k] += pv;
+              colQ[w * UL_T + c * UL_C + k] += qv;
             }
           }
           continue;
@@ -1142,8 +1146,14 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
       __syncthreads();
       const long long k = k0 + tid;
       if (k < L) {
-        if (colP[tid] != 0.f) atomicAdd(gr_row + k, colP[tid]);
-        if (colQ[tid] != 0.f) atomicAdd(gl_row + k, colQ[tid]);
+        float sp = 0.f, sq = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < UL_T / 32; ++ww) {
+          sp += colP[ww * UL_T + tid];
+          sq += colQ[ww * UL_T + tid];
+        }
+        gr_row.add(k, sp);
+        gl_row.add(k, sq);
       }
     }
   }
@@ -1211,6 +1221,51 @@ size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int
   return (size_t)(nck * 3) * stride * 4;
 }
 
+// ---------------------------------------------------------------------------
+// reproducible accumulation (detacc.cuh)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_det_row_scale(const float* __restrict__ cot, long long L,
+                                                       int* __restrict__ S) {
+  __shared__ float red[8];
+  const long long row = blockIdx.x;
+  float m = 0.f;
+  for (long long t = threadIdx.x; t < L; t += 256) m = fmaxf(m, fabsf(cot[row * L + t]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+    S[row] = (m > 0.f && m < INFINITY) ? 28 - ilogbf(m) : 0;
+  }
+}
+
+__global__ void k_det_finish(const unsigned long long* __restrict__ hi, const unsigned long long* __restrict__ lo,
+                             const int* __restrict__ S, long long B, long long L, float* __restrict__ out) {
+  const long long n = B * L;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int s = S[i / L];
+    out[i] = (float)((double)(long long)hi[i] * ldexp(1.0, -s) + (double)(long long)lo[i] * ldexp(1.0, -s - 40));
+  }
+}
+
+static cudaError_t det_begin(const UParams& p, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(p.dacc, 0, sizeof(unsigned long long) * 4 * (size_t)(p.B * p.L), st);
+  if (e != cudaSuccess) return e;
+  k_det_row_scale<<<(unsigned)p.B, 256, 0, st>>>(p.cot, p.L, p.dscale);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t det_end(const UParams& p, cudaStream_t st) {
+  const long long n = p.B * p.L;
+  const unsigned grid = (unsigned)min((n + 255) / 256, 148LL * 16);
+  k_det_finish<<<grid, 256, 0, st>>>(p.dacc, p.dacc + n, p.dscale, p.B, p.L, p.gl);
+  count_launch();
+  k_det_finish<<<grid, 256, 0, st>>>(p.dacc + 2 * n, p.dacc + 3 * n, p.dscale, p.B, p.L, p.gr);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int MODE>
 static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
   if (MODE == M_HARD && until_ht_applicable(p)) return launch_until_ht_fwd(p, st);  // O(T), until_ht.cu
@@ -1248,8 +1303,8 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if (MODE == M_HARD && until_ht_applicable(p)) {  // O(T), deterministic (until_ht.cu)
     if ((e = launch_until_ht_bwd(p, st)) != cudaSuccess) return e;
   } else {
-  if ((e = cudaMemsetAsync(p.gl, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(p.gr, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
+  if (p.dacc == nullptr || p.dscale == nullptr) return cudaErrorInvalidValue;
+  if ((e = det_begin(p, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
   const size_t ul_smem = (size_t)U_CB_G * 2 * U_THREADS * 4 + (size_t)(ntx * 4 + 4) * sizeof(double);
   if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled() && p.scratch != nullptr && ul_smem <= kUSmemMax) {
@@ -1287,6 +1342,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   }
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = det_end(p, st)) != cudaSuccess) return e;
   }
   // child VJPs from the accumulated cotangents (left first: first-writer order)
   FGParams q;

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 LIB = os.path.join(HERE, "libstlg.so")
-SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_unt.cu", "until.cu", "until_ht.cu", "smooth.cu", "mining.cu"]
+SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_unt.cu", "fg_soft64.cu", "until.cu", "until_ht.cu", "smooth.cu", "mining.cu"]
 # (object name, source, defines): fg_reg_inst.cu once per tile width and direction
 VARIANTS = [(f"fg_reg_{'b' if bwd else 'f'}{nw}", "fg_reg_inst.cu", [f"-DREG_NW={nw}", f"-DREG_BWD={bwd}"])
             for bwd in (1, 0) for nw in (4, 5, 6, 7, 8)]

@@ -511,6 +511,10 @@ struct Ev<MODE, EK_AFF> : LeafRegs {
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + (long long)j * es1)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
+  // the reference's float64 value (fp32 inputs / constants are exact in fp64)
+  __device__ __forceinline__ double value64(int, Raw r) const {
+    return (double)s_out * fma((double)s_in, (double)r.x, (double)c);
+  }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put(g1, ges1, j, g * (s_out * s_in), st1); }
   template <bool ST>
   __device__ __forceinline__ void grad_t(int j, Raw r, float g) const { grad(j, r, g); }
@@ -524,6 +528,9 @@ struct Ev<MODE, EK_AFF1> : LeafRegs {
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * __fadd_rn(s_in * r.x, c); }
+  __device__ __forceinline__ double value64(int, Raw r) const {
+    return (double)s_out * fma((double)s_in, (double)r.x, (double)c);
+  }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * (s_out * s_in), st1); }
   template <bool ST>
   __device__ __forceinline__ void grad_t(int j, Raw, float g) const { put1t<ST>(g1, j, g * (s_out * s_in)); }
@@ -537,6 +544,7 @@ struct Ev<MODE, EK_SRC> : LeafRegs {
   __device__ __forceinline__ Ev(const DExpr& e, long long row, const ModeP&) : LeafRegs(e, row) {}
   __device__ __forceinline__ Raw load(int j) const { return Raw{ld_na(p1 + j)}; }
   __device__ __forceinline__ float value(int, Raw r) const { return s_out * r.x; }
+  __device__ __forceinline__ double value64(int, Raw r) const { return (double)s_out * (double)r.x; }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { put1(g1, j, g * s_out, st1); }
   template <bool ST>
   __device__ __forceinline__ void grad_t(int j, Raw, float g) const { put1t<ST>(g1, j, g * s_out); }
@@ -555,6 +563,10 @@ struct Ev<MODE, EK_NORM> : LeafRegs {
   __device__ __forceinline__ float value(int, Raw r) const {
     float dx = r.x - cx, dy = r.y - cy;
     return s_out * __fadd_rn(s_in * sqrt_fast(fmaf(dx, dx, dy * dy)), c);
+  }
+  __device__ __forceinline__ double value64(int, Raw r) const {
+    const double dx = (double)r.x - (double)cx, dy = (double)r.y - (double)cy;
+    return (double)s_out * fma((double)s_in, sqrt(fma(dx, dx, dy * dy)), (double)c);
   }
   __device__ __forceinline__ void grad(int j, Raw r, float g) const {
     float dx = r.x - cx, dy = r.y - cy;
@@ -594,6 +606,10 @@ struct Ev<MODE, EK_PAIR> : LeafRegs {
     float dx = r.x - cx, dy = r.y - cy;
     return s_out * __fadd_rn(s_in * sqrt_fast(fmaf(dx, dx, dy * dy)), c);
   }
+  __device__ __forceinline__ double value64(int, Raw r) const {
+    const double dx = (double)r.x - (double)cx, dy = (double)r.y - (double)cy;
+    return (double)s_out * fma((double)s_in, sqrt(fma(dx, dx, dy * dy)), (double)c);
+  }
   __device__ __forceinline__ void grad(int j, Raw r, float g) const {
     float dx = r.x - cx, dy = r.y - cy;
     float d2 = fmaf(dx, dx, dy * dy);
@@ -618,6 +634,7 @@ struct Ev<MODE, EK_GEN> {
   __device__ __forceinline__ Ev(const DExpr& ex, long long r, const ModeP& m) : e(&ex), row(r), mp(m) {}
   __device__ __forceinline__ Raw load(int) const { return Raw{}; }
   __device__ __forceinline__ float value(int j, Raw) const { return expr_eval<MODE>(*e, row, j, mp); }
+  __device__ __forceinline__ double value64(int j, Raw) const { return (double)expr_eval<MODE>(*e, row, j, mp); }
   __device__ __forceinline__ void grad(int j, Raw, float g) const { expr_vjp<MODE>(*e, row, j, g, mp); }
   template <bool ST>
   __device__ __forceinline__ void grad_t(int j, Raw r, float g) const { grad(j, r, g); }

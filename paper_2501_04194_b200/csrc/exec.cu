@@ -303,26 +303,18 @@ double sigmoid_h(double z) {
 // lw2[i] = log2 w_i (i < L), then lw2[L + m] = log2 sum_{i >= max(m, i_lo)} w_i, the
 // suffix sums the backward's padded-tail term uses (one O(T) pass per row instead of
 // a window loop per virtual pad position)
-bool smooth_table(const stlg_smooth& sp, long long L, std::vector<float>& lw2, int* i_lo, int* i_hi) {
-  lw2.assign((size_t)(2 * L), -INFINITY);
-  std::vector<double> w64((size_t)L, 0.0);
+// kept range {i : w_i > 0} of a smooth interval (host fp64; the table itself is built on
+// the device by k_smooth_table, smooth.cu); false: every weight is zero
+bool smooth_range(const stlg_smooth& sp, long long L, int* i_lo, int* i_hi) {
   int lo = -1, hi = -1;
   const double Lf = (double)L;
   for (long long i = 0; i < L; ++i) {
     double a = sigmoid_h(((double)i - sp.a * Lf) * sp.c);
     double b = sigmoid_h(((double)i - sp.b * Lf) * sp.c);
-    double w = a - b - sp.eps;
-    if (w > 0) {
-      lw2[(size_t)i] = (float)std::log2(w);
-      w64[(size_t)i] = w;
+    if (a - b - sp.eps > 0) {
       if (lo < 0) lo = (int)i;
       hi = (int)i;
     }
-  }
-  double suf = 0.0;
-  for (long long m = L - 1; m >= 0; --m) {
-    suf += w64[(size_t)m];
-    lw2[(size_t)(L + m)] = suf > 0.0 ? (float)std::log2(suf) : -INFINITY;
   }
   *i_lo = lo;
   *i_hi = hi;
@@ -626,15 +618,13 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
                       cudaStream_t st, bool backward) {
   if (!smooth_params) return fail(STLG_E_INVALID, "smooth parameters required");
   const stlg_smooth& sp = smooth_params[e.smooth_slot];
-  std::vector<float> lw2;
   int i_lo, i_hi;
-  if (!smooth_table(sp, T, lw2, &i_lo, &i_hi))
+  if (!smooth_range(sp, T, &i_lo, &i_hi))
     return fail(STLG_E_EMPTY_WINDOW, "smooth interval produced an all-zero weight vector");
   float* tab = bf.tables + (size_t)e.table * 2 * (size_t)T;
-  cudaError_t ce = cudaMemcpyAsync(tab, lw2.data(), sizeof(float) * 2 * (size_t)T,
-                                   cudaMemcpyHostToDevice, st);
+  cudaError_t ce = launch_smooth_table(sp.a, sp.b, sp.c, sp.eps, T, i_lo, i_hi, tab, st);
   int rc;
-  if ((rc = cuda_status(ce, "weight upload"))) return rc;
+  if ((rc = cuda_status(ce, "weight table"))) return rc;
   const int mode = plan->cfg.mode;
   if (mode == STLG_MODE_HARD) {
     FGParams p;

@@ -749,6 +749,7 @@ static cudaError_t fwd_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t st) 
 }
 
 cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
+  if (mode == M_SOFT && sx_applicable(p)) return launch_sx_fwd(p, st);  // fp64 softmax (fg_soft64.cu)
   if (reg_enabled() && reg_applicable(mode, p, false)) return launch_reg_fwd(mode, expr_kind(p.child), p, st);
   if (use_direct(p.K, mode)) {
     dim3 grid((unsigned)((p.L + 255) / 256), (unsigned)p.B);
@@ -798,6 +799,7 @@ static cudaError_t bwd_hard_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t
 
 cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
   cudaError_t e;
+  if (mode == M_SOFT && sx_applicable(p)) return launch_sx_bwd(p, st);
   if (reg_enabled() && reg_applicable(mode, p, true)) return launch_reg_bwd(mode, expr_kind(p.child), p, st);
   if (use_direct(p.K, mode)) {
     if ((e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;

@@ -74,10 +74,19 @@ struct SParams {
 constexpr int SMOOTH_RP = 4;
 inline long long smooth_dw_parts(long long B) { return (B + SMOOTH_RP - 1) / SMOOTH_RP; }
 
+// timed softmax F / G in fp64 (fg_soft64.cu): applicability, forward, fused backward
+bool sx_applicable(const FGParams& p);
+cudaError_t launch_sx_fwd(FGParams& p, cudaStream_t st);
+cudaError_t launch_sx_bwd(FGParams& p, cudaStream_t st);
+
 // hard timed Until in O(T) (until_ht.cu): applicability, forward, backward into gl / gr
 bool until_ht_applicable(const UParams& p);
 cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st);
 cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st);
+
+// log2 weight table + log2 suffix sums [2L] of one smooth interval, on the device
+cudaError_t launch_smooth_table(double a, double b, double c, double eps, long long L, int i_lo, int i_hi,
+                                float* lw2, cudaStream_t st);
 
 // fp64 weight table and its (a, b, c) partials -> d_abc (one smooth slot)
 cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,

@@ -660,6 +660,52 @@ cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st) {
   return launch_pointwise_vjp(mode, q, p.gbuf, st);
 }
 
+// weight table on the device (fp64, then fp32 log2): lw2[i] = log2 w_i for i in
+// [i_lo, i_hi] (-inf elsewhere), lw2[L + m] = log2 sum_{i >= m} w_i — the kernel form of
+// the host table (no pageable upload, so smooth formulas capture into CUDA graphs)
+__global__ void __launch_bounds__(1024) k_smooth_table(double a, double b, double c, double eps, long long L,
+                                                       int i_lo, int i_hi, float* __restrict__ lw2) {
+  __shared__ double part[1024];
+  const int tid = threadIdx.x;
+  const long long per = (L + 1023) / 1024;
+  const long long m0 = (long long)tid * per, m1 = min(m0 + per, L);
+  const double Lf = (double)L;
+  auto wgt = [&](long long i) -> double {
+    if (i < i_lo || i > i_hi) return 0.0;
+    const double w = sigmoid_d(((double)i - a * Lf) * c) - sigmoid_d(((double)i - b * Lf) * c) - eps;
+    return w > 0.0 ? w : 0.0;
+  };
+  double s = 0.0;
+  for (long long i = m0; i < m1; ++i) {
+    const double w = wgt(i);
+    lw2[i] = w > 0.0 ? (float)log2(w) : -INFINITY;
+    s += w;
+  }
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {  // exclusive suffix totals of the thread segments, in a fixed order
+    double acc = 0.0;
+    for (int k = 1023; k >= 0; --k) {
+      const double v = part[k];
+      part[k] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  double suf = part[tid];
+  for (long long m = m1 - 1; m >= m0; --m) {
+    suf += wgt(m);
+    lw2[L + m] = suf > 0.0 ? (float)log2(suf) : -INFINITY;
+  }
+}
+
+cudaError_t launch_smooth_table(double a, double b, double c, double eps, long long L, int i_lo, int i_hi,
+                                float* lw2, cudaStream_t st) {
+  k_smooth_table<<<1, 1024, 0, st>>>(a, b, c, eps, L, i_lo, i_hi, lw2);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_smooth_abc(const double* dw64, const float* lw2, long long L, double a, double b,
                               double c, double eps, double* d_abc, cudaStream_t st) {
   k_smooth_abc<<<1, 1024, 0, st>>>(dw64, lw2, L, a, b, c, eps, d_abc);

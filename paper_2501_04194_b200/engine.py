@@ -17,6 +17,8 @@ the CPU.
 from __future__ import annotations
 
 import ctypes
+import threading
+from collections import OrderedDict
 from ctypes import byref, c_int32, c_size_t, c_void_p
 from dataclasses import dataclass, replace
 from typing import Mapping, Optional
@@ -125,20 +127,30 @@ class Compiled:
             fws.data_ptr(), fws.numel(), bws.data_ptr(), bws.numel(), stream))
 
 
-_PLANS: dict = {}
+# compiled plans, least recently used first; a plan is freed (stlg_free) when it is
+# evicted and no live autograd graph still holds it
+_PLANS: "OrderedDict" = OrderedDict()
+PLAN_CACHE_SIZE = 256
+_PLANS_LOCK = threading.Lock()
 
 
 def compile_formula(f, channel_names, cfg) -> Compiled:
     names = tuple(channel_names)
     try:
         key = (f, names, cfg_key(cfg))
-        hit = _PLANS.get(key)
+        hash(key)
     except TypeError:  # unhashable duck-typed AST: lower to get a structural key
         key = (lower(f, names).key, names, cfg_key(cfg))
+    with _PLANS_LOCK:
         hit = _PLANS.get(key)
-    if hit is None:
-        hit = Compiled(f, names, cfg)
+        if hit is not None:
+            _PLANS.move_to_end(key)
+            return hit
+    hit = Compiled(f, names, cfg)
+    with _PLANS_LOCK:
         _PLANS[key] = hit
+        while len(_PLANS) > PLAN_CACHE_SIZE:
+            _PLANS.popitem(last=False)
     return hit
 
 

@@ -156,9 +156,5 @@ def test_softmax_windows_vs_oracle(cuda, ab, L, temp):
     tr, g, _ = run_device(f, {"x": x}, cfg, cot=cot)
     ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x}, cfg, cot)
     assert rel_err(tr, ref_tr) <= 1e-5
-    # softmax gradients carry the fp32 cancellation of sum g w (1 + tau (u - M)):
-    # terms of size tau |u - M| w cancel to O(w), so at tau = 10 on signals with
-    # |x| ~ 8 both kernel families land at 1-4e-5 (scripts/soft_err.py);
-    # at tau = 1 the reference's 1e-5 holds
-    tol = 1e-5 if temp <= 1.0 else 5e-5
-    assert rel_err(g["x"], ref_g["x"]) <= tol
+    # the cancellation in sum g w (1 + tau (u - M)) is carried in fp64 (csrc/fg_soft64.cu)
+    assert rel_err(g["x"], ref_g["x"]) <= 1e-5

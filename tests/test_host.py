@@ -256,3 +256,16 @@ def test_synth_step_dataset_matches_reference():
     from stlmask.apps import synth_step_dataset as ref
     for seed, n, L in ((3, 8, 2000), (0, 64, 20)):
         assert np.array_equal(P.synth_step_dataset(seed, n, L), ref(seed, n=n, length=L))
+
+
+def test_plan_cache_is_bounded_lru(monkeypatch):
+    """compile_formula keeps at most PLAN_CACHE_SIZE plans (annealing loops in
+    mining / planning compile a new temperature every step)."""
+    from paper_2501_04194_b200 import engine
+    monkeypatch.setattr(engine, "PLAN_CACHE_SIZE", 4)
+    engine._PLANS.clear()
+    f = P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 3))
+    plans = [engine.compile_formula(f, ["x"], P.SemanticsConfig(mode=P.LogSumExp(1.0 + k))) for k in range(6)]
+    assert len(engine._PLANS) == 4
+    assert engine.compile_formula(f, ["x"], P.SemanticsConfig(mode=P.LogSumExp(6.0))) is plans[-1]
+    assert engine.compile_formula(f, ["x"], P.SemanticsConfig(mode=P.LogSumExp(1.0))) is not plans[0]

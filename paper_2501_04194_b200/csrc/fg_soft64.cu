@@ -9,44 +9,91 @@
 //   * per CTA one frame f = max u, e_i = exp(tau (u_i - f)) and e_i u_i in fp64 once per
 //     staged sample (exp range 700 nat: a tile whose windows underflow takes the
 //     per-window max-shifted path inside the same launch);
-//   * window sums S_t = sum e, Q_t = sum e u (M_t = Q_t / S_t), fp64 adds, register
-//     blocked: lane l of a warp owns outputs base + l + 32 o (o < SX_O), so every staged
-//     element loaded by the warp feeds up to SX_O windows, conflict-free;
+//   * window sums S_t = sum e, Q_t = sum e u (M_t = Q_t / S_t) in fp64 without
+//     subtraction: 32-sample blocks carry warp-scanned prefixes / suffixes and totals,
+//     a window is suffix + whole blocks + prefix (about K / 32 + 2 adds per output);
 //   * backward (gather form, nothing stored by the forward): the CTA owning children
 //     [j0, j0 + SX_N) recomputes S_t, M_t of the outputs t in [j0 - b, j0 + SX_N - a),
 //     alpha_t = g_t / S_t, beta_t = alpha_t M_t, then per child the window sums
 //     A_j = sum alpha, B_j = sum beta and  d c_j = e_j (A_j + tau (u_j A_j - B_j)).
-// Work is O(K) fp64 adds per output (no O(K) exps), which at the C2 window (K = 91) costs
-// about what the fp32 vHGW kernels cost; they remain for masked_fill / padded windows.
+// One fp64 exp per staged sample, O(K / 32) adds per output; the fp32 vHGW kernels
+// remain for masked_fill / padded windows.
 #include "fg_reg.cuh"
 
 namespace stlg {
 
 constexpr int SX_W = 4;            // warps per CTA
 constexpr int SX_T = SX_W * 32;    // threads
-constexpr int SX_O = 4;            // outputs per lane, 32 apart
-constexpr int SX_N = SX_T * SX_O;  // outputs (forward) / children (backward) per CTA
+constexpr int SX_N = 512;          // outputs (forward) / children (backward) per CTA
 constexpr int SX_KMAX = 2048;
 constexpr double SX_TINY = 1e-290;  // smaller window sums: per-window frames
 
-// S[o], Q[o] over staged elements [r0 + 32 o, r0 + 32 o + K) of (A, B)
-__device__ __forceinline__ void sx_sums(const double* A, const double* B, int r0, int K, double S[SX_O],
-                                        double Q[SX_O]) {
+// Window sums without subtraction (no cancellation, fixed order): 32-sample blocks carry
+// their inclusive prefix P and suffix Q (warp shuffle scans) and their total; a window of
+// K >= 33 samples is Q[start] + (whole blocks) + P[end].  K <= 32: a direct sum.
+struct SxBlk {
+  double *PX, *QX, *PY, *QY, *BX, *BY;
+};
+
+__device__ __forceinline__ SxBlk sx_carve(double* base, int n) {
+  const int nb = (n + 31) / 32 + 1;
+  return SxBlk{base, base + n, base + 2 * n, base + 3 * n, base + 4 * n, base + 4 * n + nb};
+}
+__host__ __device__ constexpr int sx_blk_doubles(int n) { return 4 * n + 2 * ((n + 31) / 32 + 1); }
+
+__device__ __forceinline__ void sx_blockify(const double* X, const double* Y, int n, const SxBlk& b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (n + 31) >> 5;
+  for (int bk = warp; bk < nb; bk += SX_W) {
+    const int i = bk * 32 + lane;
+    const double x = i < n ? X[i] : 0.0, y = i < n ? Y[i] : 0.0;
+    double px = x, py = y, qx = x, qy = y;
 #pragma unroll
-  for (int o = 0; o < SX_O; ++o) S[o] = Q[o] = 0.0;
-  const int kend = K + 32 * (SX_O - 1);
-#pragma unroll 4
-  for (int k = 0; k < kend; ++k) {
-    const double x = A[r0 + k], y = B[r0 + k];
-#pragma unroll
-    for (int o = 0; o < SX_O; ++o) {
-      const int kk = k - 32 * o;  // warp-uniform
-      if (kk >= 0 && kk < K) {
-        S[o] += x;
-        Q[o] += y;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ax = __shfl_up_sync(0xffffffffu, px, o), ay = __shfl_up_sync(0xffffffffu, py, o);
+      const double cx = __shfl_down_sync(0xffffffffu, qx, o), cy = __shfl_down_sync(0xffffffffu, qy, o);
+      if (lane >= o) {
+        px += ax;
+        py += ay;
+      }
+      if (lane + o < 32) {
+        qx += cx;
+        qy += cy;
       }
     }
+    if (i < n) {
+      b.PX[i] = px;
+      b.QX[i] = qx;
+      b.PY[i] = py;
+      b.QY[i] = qy;
+    }
+    if (lane == 0) {
+      b.BX[bk] = qx;
+      b.BY[bk] = qy;
+    }
   }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void sx_win(const double* X, const double* Y, const SxBlk& b, int r, int K, double& s,
+                                       double& q) {
+  if (K <= 32) {
+    s = q = 0.0;
+    for (int k = 0; k < K; ++k) {
+      s += X[r + k];
+      q += Y[r + k];
+    }
+    return;
+  }
+  const int e = r + K - 1, qa = r >> 5, qb = e >> 5;
+  s = b.QX[r];
+  q = b.QY[r];
+  for (int m = qa + 1; m < qb; ++m) {
+    s += b.BX[m];
+    q += b.BY[m];
+  }
+  s += b.PX[e];
+  q += b.PY[e];
 }
 
 // block max of v (SX_T threads)
@@ -61,11 +108,11 @@ __device__ __forceinline__ double sx_bmax(double v, double* red) {
   return m;
 }
 
-// stage u (fp64, max space) over positions [s0, s0 + n) (-inf past the signal), then the
-// frame and e, e u; returns the frame
+// stage u (fp64, max space) over positions [s0, s0 + n) (-inf outside the signal), then
+// the frame f = max u and e = exp(tau (u - f)), e u
 template <int EK>
-__device__ __forceinline__ double sx_stage(const Ev<M_SOFT, EK>& ev, float sg, double tau, int s0, int n, int L,
-                                           double* U, double* E, double* EU, double* red) {
+__device__ __forceinline__ void sx_stage(const Ev<M_SOFT, EK>& ev, float sg, double tau, int s0, int n, int L,
+                                         double* U, double* E, double* EU, double* red) {
   double mx = -INFINITY;
   for (int i = threadIdx.x; i < n; i += SX_T) {
     const int pos = s0 + i;
@@ -82,7 +129,6 @@ __device__ __forceinline__ double sx_stage(const Ev<M_SOFT, EK>& ev, float sg, d
     EU[i] = (e > 0.0) ? e * u : 0.0;
   }
   __syncthreads();
-  return f;
 }
 
 // per-window max-shifted sums (tiles whose frame underflows a window)
@@ -116,30 +162,28 @@ __global__ void __launch_bounds__(SX_T) k_sx_fwd(const __grid_constant__ FGParam
     for (int t = t0 + (int)threadIdx.x; t < tend; t += SX_T) outr[t] = __fadd_rn(padv, czero);
     return;
   }
-  const int NS = SX_N + K + 32 * SX_O;  // staged (+ slack read by the blocked sums)
+  const int NS = SX_N + K - 1;  // staged positions [t0 + a, t0 + a + NS): output t's window at t - t0
   double* U = sxs;
   double* E = U + NS;
   double* EU = E + NS;
+  const SxBlk bl = sx_carve(EU + NS, NS);
   sx_stage<EK>(ev, sg, tau, t0 + p.a, NS, L, U, E, EU, red);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = warp * 32 * SX_O + lane;  // staged index of the lane's first window
-  double S[SX_O], Q[SX_O];
-  sx_sums(E, EU, r0, K, S, Q);
+  sx_blockify(E, EU, NS, bl);
   bool fb = false;
-#pragma unroll
-  for (int o = 0; o < SX_O; ++o) fb |= (t0 + r0 + 32 * o < nvalid) && !(S[o] > SX_TINY);
+  for (int r = threadIdx.x; r < tend - t0; r += SX_T) {
+    if (t0 + r >= nvalid) continue;
+    double s, q;
+    sx_win(E, EU, bl, r, K, s, q);
+    fb |= !(s > SX_TINY);
+  }
   fb = __syncthreads_or(fb);
-#pragma unroll
-  for (int o = 0; o < SX_O; ++o) {
-    const int t = t0 + r0 + 32 * o;
-    if (t >= tend) continue;
+  for (int r = threadIdx.x; r < tend - t0; r += SX_T) {
+    const int t = t0 + r;
     float v = padv;
     if (t < nvalid) {
-      double s = S[o], q = Q[o];
-      if (fb) {
-        double m;
-        sx_exact(U, r0 + 32 * o, K, tau, m, s, q);
-      }
+      double s, q, m;
+      if (fb) sx_exact(U, r, K, tau, m, s, q);
+      else sx_win(E, EU, bl, r, K, s, q);
       v = (float)((double)sg * (q / s));
     }
     outr[t] = __fadd_rn(v, czero);
@@ -158,39 +202,34 @@ __global__ void __launch_bounds__(SX_T) k_sx_bwd(const __grid_constant__ FGParam
   const double tau = p.mp.tau;
   Ev<M_SOFT, EK> ev(p.child, row, p.mp);
   const float* cot = p.cot + row * L;
-  const int tb = j0 - b;                       // first output whose window can reach j0
-  const int NO = SX_N + K - 1;                 // outputs [tb, tb + NO)
-  const int NOR = ((NO + SX_N - 1) / SX_N) * SX_N;  // rounded to whole blocked groups
-  const int NS = NOR + K + 32 * SX_O;          // staged positions [tb + a, tb + a + NS)
+  const int tb = j0 - b;         // first output whose window can reach j0
+  const int NO = SX_N + K - 1;   // outputs [tb, tb + NO); output r's window at staged r
+  const int NS = NO + K - 1;     // staged positions [tb + a, tb + a + NS)
   double* U = sxs;
   double* E = U + NS;
   double* EU = E + NS;
-  double* AL = EU + NS;                        // alpha_t (or L_t on per-window frames)
-  double* BE = AL + NOR + K + 32 * SX_O;       // beta_t  (or M_t)
+  double* AL = EU + NS;          // alpha_t = g_t / S_t   (L_t on per-window frames)
+  double* BE = AL + NO;          // beta_t = alpha_t M_t  (M_t on per-window frames)
+  const SxBlk bl = sx_carve(BE + NO, NS);
   sx_stage<EK>(ev, sg, tau, tb + p.a, NS, L, U, E, EU, red);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // phase 1: window sums of the outputs
+  sx_blockify(E, EU, NS, bl);
   bool fb = false;
-  for (int g0 = 0; g0 < NOR; g0 += SX_N) {
-    const int r0 = g0 + warp * 32 * SX_O + lane;
-    double S[SX_O], Q[SX_O];
-    sx_sums(E, EU, r0, K, S, Q);
-#pragma unroll
-    for (int o = 0; o < SX_O; ++o) {
-      const int r = r0 + 32 * o, t = tb + r;
-      const bool live = r < NO && t >= 0 && t < nvalid;
-      const float g = live ? cot[t] : 0.f;
-      fb |= live && g != 0.f && !(S[o] > SX_TINY);
-      AL[r] = live ? (double)g / S[o] : 0.0;
-      BE[r] = live ? ((double)g / S[o]) * (Q[o] / S[o]) : 0.0;
-    }
+  for (int r = threadIdx.x; r < NO; r += SX_T) {
+    const int t = tb + r;
+    const bool live = t >= 0 && t < nvalid;
+    const float g = live ? cot[t] : 0.f;
+    double s = 1.0, q = 0.0;
+    if (live && g != 0.f) sx_win(E, EU, bl, r, K, s, q);
+    fb |= live && g != 0.f && !(s > SX_TINY);
+    const double al = (live && g != 0.f) ? (double)g / s : 0.0;
+    AL[r] = al;
+    BE[r] = al * (q / s);
   }
-  for (int r = NOR + (int)threadIdx.x; r < NOR + K + 32 * SX_O; r += SX_T) AL[r] = BE[r] = 0.0;
   fb = __syncthreads_or(fb);
   if (fb) {  // per-window frames: AL <- L_t (window LSE), BE <- M_t, per-pair exps below
-    for (int r = threadIdx.x; r < NOR; r += SX_T) {
+    for (int r = threadIdx.x; r < NO; r += SX_T) {
       const int t = tb + r;
-      if (r < NO && t >= 0 && t < nvalid) {
+      if (t >= 0 && t < nvalid) {
         double m, s, q;
         sx_exact(U, r, K, tau, m, s, q);
         AL[r] = m + log(s) / tau;
@@ -200,21 +239,21 @@ __global__ void __launch_bounds__(SX_T) k_sx_bwd(const __grid_constant__ FGParam
         BE[r] = 0.0;
       }
     }
-    __syncthreads();
+  } else {
+    sx_blockify(AL, BE, NO, bl);  // (the staged blocks are no longer needed)
   }
-  // phase 2: child j = j0 + c receives from outputs t in [j - b, j - a]: r in [c, c + K)
-  const int r0 = warp * 32 * SX_O + lane;
-  double A[SX_O], Bs[SX_O];
-  if (!fb) sx_sums(AL, BE, r0, K, A, Bs);
-#pragma unroll
-  for (int o = 0; o < SX_O; ++o) {
-    const int c = r0 + 32 * o, j = j0 + c;
-    if (j >= L) continue;
+  __syncthreads();
+  // child j = j0 + c receives from outputs t in [j - b, j - a]: r in [c, c + K)
+  for (int c = threadIdx.x; c < SX_N; c += SX_T) {
+    const int j = j0 + c;
+    if (j >= L) break;
     const int iu = c + K - 1;  // staged index of j (staged base tb + a = j0 - (K - 1))
     const double u = U[iu];
     double G;
     if (!fb) {
-      G = E[iu] * (A[o] + tau * (u * A[o] - Bs[o]));
+      double A, Bs;
+      sx_win(AL, BE, bl, c, K, A, Bs);
+      G = E[iu] * (A + tau * (u * A - Bs));
     } else {
       G = 0.0;
       for (int k = 0; k < K; ++k) {
@@ -231,12 +270,13 @@ __global__ void __launch_bounds__(SX_T) k_sx_bwd(const __grid_constant__ FGParam
   }
 }
 
-static size_t sx_fwd_smem(int K) { return sizeof(double) * 3 * (size_t)(SX_N + K + 32 * SX_O); }
+static size_t sx_fwd_smem(int K) {
+  const int NS = SX_N + K - 1;
+  return sizeof(double) * (size_t)(3 * NS + sx_blk_doubles(NS));
+}
 static size_t sx_bwd_smem(int K) {
-  const int NO = SX_N + K - 1;
-  const int NOR = ((NO + SX_N - 1) / SX_N) * SX_N;
-  const size_t NS = (size_t)NOR + K + 32 * SX_O;
-  return sizeof(double) * (3 * NS + 2 * NS);
+  const int NO = SX_N + K - 1, NS = NO + K - 1;
+  return sizeof(double) * (size_t)(3 * NS + 2 * NO + sx_blk_doubles(NS));
 }
 
 bool sx_applicable(const FGParams& p) {

@@ -65,9 +65,7 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        # STLG_LIB: an alternative build of the same ABI (A/B measurements of compile-time
-        # variants); it must exist like the default one — there is no CPU fallback
-        path = os.environ.get("STLG_LIB") or LIB_PATH
+        path = LIB_PATH
         if not os.path.exists(path):
             raise RuntimeError(
                 f"{path} is missing: build it with `python -m paper_2501_04194_b200.build_lib` "

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 LIB = os.path.join(HERE, "libstlg.so")
-SOURCES = ["exec.cu", "fg.cu", "fg_pipe.cu", "fg_reg_fwd.cu", "fg_unt.cu", "fg_soft64.cu", "until.cu", "until_ht.cu", "smooth.cu", "mining.cu"]
+SOURCES = ["exec.cu", "fg.cu", "fg_reg_fwd.cu", "fg_unt.cu", "fg_soft64.cu", "until.cu", "until_ht.cu", "smooth.cu", "mining.cu"]
 # (object name, source, defines): fg_reg_inst.cu once per tile width and direction
 VARIANTS = [(f"fg_reg_{'b' if bwd else 'f'}{nw}", "fg_reg_inst.cu", [f"-DREG_NW={nw}", f"-DREG_BWD={bwd}"])
             for bwd in (1, 0) for nw in (4, 5, 6, 7, 8)]
@@ -43,19 +43,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True, out: str | None = None, extra: list | None = None) -> str:
-    """Compile each translation unit in parallel, then link libstlg.so.
-
-    `out` / `extra` build a variant library (e.g. extra=["-DCAV_LB=16"]) for A/B
-    measurements through STLG_LIB; the default build uses neither.
-    """
-    lib_out = out or LIB
-    if out is None and not force and not _stale():
+def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile each translation unit in parallel (objects newer than their sources and
+    headers are kept unless force=True), then link libstlg.so."""
+    lib_out = LIB
+    if not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build_obj" if out is None else "build_obj_variant")
+    objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)] + list(extra or [])
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
 
     hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
     hdr_t = max(hdr_t, os.path.getmtime(os.path.join(INCLUDE, "stlg.h")), os.path.getmtime(__file__))
@@ -67,7 +64,7 @@ def build(force: bool = False, verbose: bool = True, out: str | None = None, ext
         srcp = os.path.join(CSRC, src)
         # incremental: an object newer than its source, every header and this file is kept
         # (force=True rebuilds everything)
-        if (not force and out is None and os.path.exists(obj)
+        if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) > max(os.path.getmtime(srcp), hdr_t)):
             return obj
         cmd = [_nvcc(), *compile_flags, *defs, "-I", INCLUDE, "-c", "-o", obj, srcp]

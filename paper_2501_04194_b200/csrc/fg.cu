@@ -34,25 +34,38 @@ namespace stlg {
 // ===========================================================================
 // pointwise expression kernels (root formula / materialised sub-formulas)
 // ===========================================================================
+// grid (t tiles of 1024, rows): 4 samples per thread, 32-bit time index, no division
+constexpr int PW_T = 256, PW_E = 4, PW_N = PW_T * PW_E;
+
 template <int MODE>
-__global__ void __launch_bounds__(256) k_pointwise_fwd(const __grid_constant__ FGParams p) {
-  const long long n = p.B * p.L;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long row = i / p.L, t = i - row * p.L;
-    p.out[i] = expr_eval<MODE>(p.child, row, t, p.mp);
+__global__ void __launch_bounds__(PW_T) k_pointwise_fwd(const __grid_constant__ FGParams p) {
+  const int L = (int)p.L;
+  for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
+    float* out = p.out + row * L;
+#pragma unroll
+    for (int e = 0; e < PW_E; ++e) {
+      const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+      if (t < L) out[t] = expr_eval<MODE>(p.child, row, t, p.mp);
+    }
   }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_pointwise_vjp(const __grid_constant__ FGParams p,
+__global__ void __launch_bounds__(PW_T) k_pointwise_vjp(const __grid_constant__ FGParams p,
                                                        const float* __restrict__ g) {
-  const long long n = p.B * p.L;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long row = i / p.L, t = i - row * p.L;
-    expr_vjp<MODE>(p.child, row, t, g[i], p.mp);
+  const int L = (int)p.L;
+  for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
+    const float* gr = g + row * L;
+#pragma unroll
+    for (int e = 0; e < PW_E; ++e) {
+      const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+      if (t < L) expr_vjp<MODE>(p.child, row, t, gr[t], p.mp);
+    }
   }
+}
+
+static dim3 pw_grid(const FGParams& p) {
+  return dim3((unsigned)((p.L + PW_N - 1) / PW_N), (unsigned)(p.B < 65535 ? p.B : 65535));
 }
 
 __global__ void k_fill_strided(float* p, long long B, long long T, long long rs, long long es,
@@ -81,19 +94,19 @@ static int grid_for(long long n, int threads) {
 }
 
 cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st) {
-  int grid = grid_for(p.B * p.L, 256);
-  if (mode == M_HARD) k_pointwise_fwd<M_HARD><<<grid, 256, 0, st>>>(p);
-  else if (mode == M_LSE) k_pointwise_fwd<M_LSE><<<grid, 256, 0, st>>>(p);
-  else k_pointwise_fwd<M_SOFT><<<grid, 256, 0, st>>>(p);
+  const dim3 grid = pw_grid(p);
+  if (mode == M_HARD) k_pointwise_fwd<M_HARD><<<grid, PW_T, 0, st>>>(p);
+  else if (mode == M_LSE) k_pointwise_fwd<M_LSE><<<grid, PW_T, 0, st>>>(p);
+  else k_pointwise_fwd<M_SOFT><<<grid, PW_T, 0, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cudaStream_t st) {
-  int grid = grid_for(p.B * p.L, 256);
-  if (mode == M_HARD) k_pointwise_vjp<M_HARD><<<grid, 256, 0, st>>>(p, g);
-  else if (mode == M_LSE) k_pointwise_vjp<M_LSE><<<grid, 256, 0, st>>>(p, g);
-  else k_pointwise_vjp<M_SOFT><<<grid, 256, 0, st>>>(p, g);
+  const dim3 grid = pw_grid(p);
+  if (mode == M_HARD) k_pointwise_vjp<M_HARD><<<grid, PW_T, 0, st>>>(p, g);
+  else if (mode == M_LSE) k_pointwise_vjp<M_LSE><<<grid, PW_T, 0, st>>>(p, g);
+  else k_pointwise_vjp<M_SOFT><<<grid, PW_T, 0, st>>>(p, g);
   count_launch();
   return cudaGetLastError();
 }
@@ -673,16 +686,6 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
 // ===========================================================================
 static int odd_stride(int K) { return K | 1; }
 
-// STLG_PIPE=0 selects the non-pipelined timed kernels (A/B measurements)
-bool pipe_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STLG_PIPE");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 // raise the dynamic shared-memory limit once per (kernel, size)
 template <typename KernT>
 static cudaError_t set_smem(KernT k, size_t bytes) {
@@ -750,7 +753,7 @@ static cudaError_t fwd_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t st) 
 
 cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
   if (mode == M_SOFT && sx_applicable(p)) return launch_sx_fwd(p, st);  // fp64 softmax (fg_soft64.cu)
-  if (reg_enabled() && reg_applicable(mode, p, false)) return launch_reg_fwd(mode, expr_kind(p.child), p, st);
+  if (reg_applicable(mode, p, false)) return launch_reg_fwd(mode, expr_kind(p.child), p, st);
   if (use_direct(p.K, mode)) {
     dim3 grid((unsigned)((p.L + 255) / 256), (unsigned)p.B);
     if (mode == M_HARD) k_fg_timed_fwd_direct<M_HARD><<<grid, 256, 0, st>>>(p);
@@ -761,10 +764,6 @@ cudaError_t launch_fg_timed_fwd(int mode, FGParams& p, cudaStream_t st) {
   }
   const int ek = expr_kind(p.child);
   cudaError_t e;
-  if (pipe_enabled()) {
-    e = launch_fgt_fwd_pipe(mode, ek, p, st);
-    if (e != cudaErrorNotSupported) return e;
-  }
   p.Kp = odd_stride(p.K);
   p.NB = pick_nb(p.K, fwd_words(mode));
   long long J = (long long)(p.NB - 1) * p.K;
@@ -800,7 +799,7 @@ static cudaError_t bwd_hard_v2(FGParams& p, size_t smem, dim3 grid, cudaStream_t
 cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
   cudaError_t e;
   if (mode == M_SOFT && sx_applicable(p)) return launch_sx_bwd(p, st);
-  if (reg_enabled() && reg_applicable(mode, p, true)) return launch_reg_bwd(mode, expr_kind(p.child), p, st);
+  if (reg_applicable(mode, p, true)) return launch_reg_bwd(mode, expr_kind(p.child), p, st);
   if (use_direct(p.K, mode)) {
     if ((e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
     dim3 grid((unsigned)((p.L + 255) / 256), (unsigned)p.B);
@@ -824,10 +823,6 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
     DISPATCH_EK(ek, e = (bwd_hard_v2<EK>(p, smem, grid, st)))
     count_launch();
     return e;
-  }
-  if (pipe_enabled()) {
-    e = launch_fgt_bwd_pipe(mode, ek, p, st);
-    if (e != cudaErrorNotSupported) return e;
   }
   const int words = bwd_words(mode);
   int nb = pick_nb(p.K, words);
@@ -1142,7 +1137,7 @@ __global__ void __launch_bounds__(UT_T) k_fg_untimed_bwd_hard(const __grid_const
 
 cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st) {
   cudaError_t err;
-  if (reg_enabled() && launch_unt_fwd(mode, p, st, err)) return err;
+  if (launch_unt_fwd(mode, p, st, err)) return err;
   dim3 grid((unsigned)p.B);
   if (mode == M_HARD) k_fg_untimed_fwd<M_HARD><<<grid, UT_T, 0, st>>>(p);
   else if (mode == M_LSE) k_fg_untimed_fwd<M_LSE><<<grid, UT_T, 0, st>>>(p);
@@ -1154,7 +1149,7 @@ cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st) {
 cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st) {
   {
     cudaError_t err;
-    if (reg_enabled() && launch_unt_bwd(mode, p, st, err)) return err;
+    if (launch_unt_bwd(mode, p, st, err)) return err;
   }
   dim3 grid((unsigned)p.B);
   if (mode == M_HARD) {

@@ -616,12 +616,6 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_hard(cons
 // even with more staged overlap (C2: 0.041 vs 0.043 ms at NW = 7); backward widths
 // minimise the staged samples per row.
 inline int reg_pick_nw(long long L, int K, bool hard_bwd, bool fwd = false) {
-  static int forced = -1;  // STLG_REG_NW=4..8: fixed tile width (A/B measurements)
-  if (forced < 0) {
-    const char* e = getenv("STLG_REG_NW");
-    forced = (e && e[0] >= '4' && e[0] <= '8') ? e[0] - '0' : 0;
-  }
-  if (forced && 512LL * forced >= 4LL * K) return forced;
   if (fwd && 2048LL >= 4LL * K) return 4;
   int best = -1;
   long long best_cost = 0;

@@ -5,15 +5,6 @@
 
 namespace stlg {
 
-bool reg_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STLG_REG");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 bool reg_applicable(int mode, const FGParams& p, bool bwd) {
   if (mode != M_HARD && mode != M_LSE && !(mode == M_SOFT && p.K >= 17)) return false;
   if (p.padmode || p.fill || p.K < 2 || p.L >= (1LL << 30) || p.B > 65535) return false;

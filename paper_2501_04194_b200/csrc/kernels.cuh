@@ -23,7 +23,6 @@ struct FGParams {
   int padmode;    // 1: windows read the padded child (smooth-interval hard path, no overrun rule)
   int fill;       // masked_fill compat: reduce sentinel-filled full columns (masking.py:195-202)
   float sent;     // SemanticsConfig.sentinel
-  int dbg_skip;   // measurement knob (STLG_PIPE_SKIP): 1 skip scans, 2 skip loads/stores
   ModeP mp;
 };
 
@@ -108,9 +107,6 @@ cudaError_t launch_until_bwd(int mode, UParams& p, cudaStream_t st);
 cudaError_t launch_smooth_fwd(int mode, SParams& p, cudaStream_t st);
 cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st);
 
-cudaError_t launch_fgt_fwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st);
-cudaError_t launch_fgt_bwd_pipe(int mode, int ek, FGParams& p, cudaStream_t st);
-bool pipe_enabled();
 
 cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs, long long es,
                                 float v, cudaStream_t st);
@@ -119,7 +115,6 @@ cudaError_t launch_fill_strided(float* p, long long B, long long T, long long rs
 void count_launch(int n = 1);
 
 // register-blocked exact timed F / G (hard, LSE): fg_reg.cu
-bool reg_enabled();
 bool reg_applicable(int mode, const FGParams& p, bool bwd);
 cudaError_t launch_reg_fwd(int mode, int ek, FGParams& p, cudaStream_t st);
 cudaError_t launch_reg_bwd(int mode, int ek, FGParams& p, cudaStream_t st);

@@ -645,7 +645,7 @@ template <int MODE>
 __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_constant__ UParams p) {
   __shared__ float Ls[UH_T * UH_S];
   __shared__ float Rs[UH_T * UH_S];
-  __shared__ Clamp cb[UH_T];
+  __shared__ Clamp cb[UH_T / 32];
   const long long row = blockIdx.x, L = p.L;
   const int tid = threadIdx.x;
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
@@ -665,16 +665,21 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
       Clamp ft{(l <= r) ? l : r, l};
       f = clamp_compose(ft, f);
     }
-    cb[tid] = f;
-    __syncthreads();
-    for (int off = 1; off < UH_T; off <<= 1) {  // suffix composition C_i = F_i o F_{i+1} o ...
-      Clamp x = cb[tid];
-      if (tid + off < UH_T) x = clamp_compose(x, cb[tid + off]);
-      __syncthreads();
-      cb[tid] = x;
-      __syncthreads();
+    // suffix composition over the later threads: warp shuffles, then the later warps
+    const int lane = tid & 31, warp = tid >> 5;
+    Clamp C = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Clamp n{__shfl_down_sync(0xffffffffu, C.lo, o), __shfl_down_sync(0xffffffffu, C.hi, o)};
+      if (lane + o < 32) C = clamp_compose(C, n);
     }
-    float v = (tid + 1 < UH_T) ? clamp_apply(cb[tid + 1], carry) : carry;
+    Clamp ex{__shfl_down_sync(0xffffffffu, C.lo, 1), __shfl_down_sync(0xffffffffu, C.hi, 1)};
+    if (lane == 31) ex = Clamp{-INFINITY, INFINITY};
+    if (lane == 0) cb[warp] = C;
+    __syncthreads();
+    float vw = carry;  // the carry pushed through the later warps of the chunk
+    for (int w = UH_T / 32 - 1; w > warp; --w) vw = clamp_apply(cb[w], vw);
+    float v = clamp_apply(ex, vw);
     for (int e = UH_E - 1; e >= 0; --e) {  // exact sequential walk with the reference tie rules
       if (c0 + tid * UH_E + e >= L) continue;
       float l = Ls[tid * UH_S + e], r = Rs[tid * UH_S + e];
@@ -698,18 +703,17 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
 // each child cotangent is final when its run ends (no atomics, fused VJPs).
 template <int MODE>
 __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_constant__ UParams p) {
-  __shared__ float sums[UH_T];
-  __shared__ int flags[UH_T];
-  __shared__ float carry_sh;
+  __shared__ double wsum[UH_T / 32];
+  __shared__ int wflag[UH_T / 32];
   const long long row = blockIdx.x, L = p.L;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* outr = p.out_in + row * L;
   const float* cot = p.cot + row * L;
-  float carry = 0.f;  // cotangent accumulated since the last terminator (earlier chunks)
+  double carry = 0.0;  // cotangent accumulated since the last terminator (earlier chunks)
   for (long long c0 = 0; c0 < L; c0 += UH_CH) {
     float g[UH_E];
     int term[UH_E];  // 0: pass to the next sample's source, 1: l_t, 2: r_t
-    float tail = 0.f;
+    double tail = 0.0;
     int anyterm = 0;
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
@@ -734,43 +738,54 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
       g[e] = cot[t];
       if (src) {
         anyterm = 1;
-        tail = 0.f;
+        tail = 0.0;
       } else {
-        tail += g[e];
+        tail += (double)g[e];
       }
     }
-    sums[tid] = tail;
-    flags[tid] = anyterm;
-    __syncthreads();
-    if (tid == 0) {  // exclusive segmented prefix over the 256 thread aggregates
-      float run = carry;
-      for (int i = 0; i < UH_T; ++i) {
-        float s = sums[i];
-        int f = flags[i];
-        sums[i] = run;
-        run = f ? s : run + s;
+    // exclusive segmented prefix (sum since the last terminator) over the earlier threads:
+    // (s, f) then (s', f')  ->  (f' ? s' : s + s', f | f'); warp shuffles, then the warps
+    double is = tail;
+    int iflag = anyterm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ps = __shfl_up_sync(0xffffffffu, is, o);
+      const int pf = __shfl_up_sync(0xffffffffu, iflag, o);
+      if (lane >= o) {
+        if (!iflag) is += ps;
+        iflag |= pf;
       }
-      carry_sh = run;
+    }
+    double xs = __shfl_up_sync(0xffffffffu, is, 1);
+    int xf = __shfl_up_sync(0xffffffffu, iflag, 1);
+    if (lane == 0) xs = 0.0, xf = 0;
+    if (lane == 31) {
+      wsum[warp] = is;
+      wflag[warp] = iflag;
     }
     __syncthreads();
-    float run = sums[tid];
+    double before = carry;  // carry, then the earlier warps, then the earlier lanes
+    for (int w = 0; w < warp; ++w) before = wflag[w] ? wsum[w] : before + wsum[w];
+    double run = xf ? xs : before + xs;
+    double nextc = carry;
+    for (int w = 0; w < UH_T / 32; ++w) nextc = wflag[w] ? wsum[w] : nextc + wsum[w];
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
       long long t = c0 + tid * UH_E + e;
       if (t >= L) break;
-      run += g[e];
+      run += (double)g[e];
       float gl = 0.f, gr = 0.f;
       if (term[e] == 1) {
-        gl = run;
-        run = 0.f;
+        gl = (float)run;
+        run = 0.0;
       } else if (term[e] == 2) {
-        gr = run;
-        run = 0.f;
+        gr = (float)run;
+        run = 0.0;
       }
       expr_vjp<MODE>(p.left, row, t, gl, p.mp);
       expr_vjp<MODE>(p.right, row, t, gr, p.mp);
     }
-    carry = carry_sh;
+    carry = nextc;
     __syncthreads();
   }
 }
@@ -1159,15 +1174,6 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
   }
 }
 
-static bool ul_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("STLG_UL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -1275,7 +1281,7 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((p.L + U_THREADS - 1) / U_THREADS), (unsigned)p.B);
-  if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled()) {
+  if (MODE == M_LSE && p.untimed && !p.fill) {
     k_until_unt_lse_fwd<<<grid, UL_T, 0, st>>>(p);
     count_launch();
     return cudaGetLastError();
@@ -1307,7 +1313,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if ((e = det_begin(p, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
   const size_t ul_smem = (size_t)U_CB_G * 2 * U_THREADS * 4 + (size_t)(ntx * 4 + 4) * sizeof(double);
-  if (MODE == M_LSE && p.untimed && !p.fill && ul_enabled() && p.scratch != nullptr && ul_smem <= kUSmemMax) {
+  if (MODE == M_LSE && p.untimed && !p.fill && p.scratch != nullptr && ul_smem <= kUSmemMax) {
     if ((e = set_smem_u(k_until_unt_lse_bwd, ul_smem)) != cudaSuccess) return e;
     const long long ntiles = (long long)ntx * p.B;
     int occ = 0;

@@ -230,6 +230,69 @@ __device__ __forceinline__ void expr_vjp(const DExpr& e, long long b, long long 
   }
 }
 
+// Register-resident forms for expressions of exactly N steps (N small): the step loop is
+// unrolled, so the SSA values live in registers and operands are picked by selects
+// instead of dynamically indexed (local-memory) arrays.
+template <int N>
+__device__ __forceinline__ float pick_n(const float (&v)[N], int idx, int k) {
+  float r = v[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    if (i < k) r = (idx == i) ? v[i] : r;
+  return r;
+}
+
+template <int MODE, int N>
+__device__ __forceinline__ float expr_eval_n(const DExpr& e, long long b, long long j, const ModeP& mp) {
+  float v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const DStep s = e.step[k];
+    if (s.op == ST_LEAF) {
+      v[k] = leaf_val(e, e.leaf[s.a], b, j);
+    } else {
+      float p1, p2;
+      v[k] = pair_red<MODE>(pick_n<N>(v, s.a, k), pick_n<N>(v, s.b, k), s.op == ST_MAX ? 1.f : -1.f, mp, p1, p2);
+    }
+  }
+  return v[N - 1];
+}
+
+template <int MODE, int N>
+__device__ __forceinline__ void expr_vjp_n(const DExpr& e, long long b, long long j, float g, const ModeP& mp) {
+  float v[N], w1[N], w2[N], adj[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const DStep s = e.step[k];
+    adj[k] = 0.f;
+    w1[k] = w2[k] = 0.f;
+    if (s.op == ST_LEAF) {
+      v[k] = leaf_val(e, e.leaf[s.a], b, j);
+    } else {
+      v[k] = pair_red<MODE>(pick_n<N>(v, s.a, k), pick_n<N>(v, s.b, k), s.op == ST_MAX ? 1.f : -1.f, mp,
+                            w1[k], w2[k]);
+    }
+  }
+  adj[N - 1] = g;
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) {
+    const DStep s = e.step[k];
+    const float a = adj[k];
+    if (s.op == ST_LEAF) {
+      const DLeaf& L = e.leaf[s.a];
+      if (a != 0.f || L.st1 || L.st2) leaf_vjp(e, L, b, j, a);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {  // scatter by selects (i < k: operands precede the step)
+        if (i < k) {
+          adj[i] += (s.a == i) ? a * w1[k] : 0.f;
+          adj[i] += (s.b == i) ? a * w2[k] : 0.f;
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // monoid states for window reductions (all in "max space": u = sg * v)
 // ---------------------------------------------------------------------------

@@ -37,7 +37,19 @@ namespace stlg {
 // grid (t tiles of 1024, rows): 4 samples per thread, 32-bit time index, no division
 constexpr int PW_T = 256, PW_E = 4, PW_N = PW_T * PW_E;
 
-template <int MODE>
+// NS > 0: expressions of exactly NS steps in registers (expr_eval_n); 0: the generic walk
+template <int MODE, int NS>
+__device__ __forceinline__ float pw_eval(const DExpr& e, long long row, int t, const ModeP& mp) {
+  if (NS > 0) return expr_eval_n<MODE, (NS > 0 ? NS : 1)>(e, row, t, mp);
+  return expr_eval<MODE>(e, row, t, mp);
+}
+template <int MODE, int NS>
+__device__ __forceinline__ void pw_vjp(const DExpr& e, long long row, int t, float g, const ModeP& mp) {
+  if (NS > 0) expr_vjp_n<MODE, (NS > 0 ? NS : 1)>(e, row, t, g, mp);
+  else expr_vjp<MODE>(e, row, t, g, mp);
+}
+
+template <int MODE, int NS>
 __global__ void __launch_bounds__(PW_T) k_pointwise_fwd(const __grid_constant__ FGParams p) {
   const int L = (int)p.L;
   for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
@@ -45,12 +57,12 @@ __global__ void __launch_bounds__(PW_T) k_pointwise_fwd(const __grid_constant__ 
 #pragma unroll
     for (int e = 0; e < PW_E; ++e) {
       const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
-      if (t < L) out[t] = expr_eval<MODE>(p.child, row, t, p.mp);
+      if (t < L) out[t] = pw_eval<MODE, NS>(p.child, row, t, p.mp);
     }
   }
 }
 
-template <int MODE>
+template <int MODE, int NS>
 __global__ void __launch_bounds__(PW_T) k_pointwise_vjp(const __grid_constant__ FGParams p,
                                                        const float* __restrict__ g) {
   const int L = (int)p.L;
@@ -59,10 +71,19 @@ __global__ void __launch_bounds__(PW_T) k_pointwise_vjp(const __grid_constant__ 
 #pragma unroll
     for (int e = 0; e < PW_E; ++e) {
       const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
-      if (t < L) expr_vjp<MODE>(p.child, row, t, gr[t], p.mp);
+      if (t < L) pw_vjp<MODE, NS>(p.child, row, t, gr[t], p.mp);
     }
   }
 }
+
+#define PW_DISPATCH(NSV, ...)                                    \
+  switch (NSV) {                                                 \
+    case 1: { constexpr int NS = 1; __VA_ARGS__; } break;        \
+    case 3: { constexpr int NS = 3; __VA_ARGS__; } break;        \
+    case 5: { constexpr int NS = 5; __VA_ARGS__; } break;        \
+    case 7: { constexpr int NS = 7; __VA_ARGS__; } break;        \
+    default: { constexpr int NS = 0; __VA_ARGS__; } break;       \
+  }
 
 static dim3 pw_grid(const FGParams& p) {
   return dim3((unsigned)((p.L + PW_N - 1) / PW_N), (unsigned)(p.B < 65535 ? p.B : 65535));
@@ -95,18 +116,20 @@ static int grid_for(long long n, int threads) {
 
 cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st) {
   const dim3 grid = pw_grid(p);
-  if (mode == M_HARD) k_pointwise_fwd<M_HARD><<<grid, PW_T, 0, st>>>(p);
-  else if (mode == M_LSE) k_pointwise_fwd<M_LSE><<<grid, PW_T, 0, st>>>(p);
-  else k_pointwise_fwd<M_SOFT><<<grid, PW_T, 0, st>>>(p);
+  PW_DISPATCH(p.child.n_step,
+              if (mode == M_HARD) k_pointwise_fwd<M_HARD, NS><<<grid, PW_T, 0, st>>>(p);
+              else if (mode == M_LSE) k_pointwise_fwd<M_LSE, NS><<<grid, PW_T, 0, st>>>(p);
+              else k_pointwise_fwd<M_SOFT, NS><<<grid, PW_T, 0, st>>>(p))
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cudaStream_t st) {
   const dim3 grid = pw_grid(p);
-  if (mode == M_HARD) k_pointwise_vjp<M_HARD><<<grid, PW_T, 0, st>>>(p, g);
-  else if (mode == M_LSE) k_pointwise_vjp<M_LSE><<<grid, PW_T, 0, st>>>(p, g);
-  else k_pointwise_vjp<M_SOFT><<<grid, PW_T, 0, st>>>(p, g);
+  PW_DISPATCH(p.child.n_step,
+              if (mode == M_HARD) k_pointwise_vjp<M_HARD, NS><<<grid, PW_T, 0, st>>>(p, g);
+              else if (mode == M_LSE) k_pointwise_vjp<M_LSE, NS><<<grid, PW_T, 0, st>>>(p, g);
+              else k_pointwise_vjp<M_SOFT, NS><<<grid, PW_T, 0, st>>>(p, g))
   count_launch();
   return cudaGetLastError();
 }

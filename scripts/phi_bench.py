@@ -1,68 +1,55 @@
-"""The reference's phi1..phi6 benchmark at GPU scale (reference
-bench.py:32-154, PAPER Table III).
+"""Table III of the paper on this box: the reference's phi1..phi6 benchmark
+(reference bench.py:32-154, recurrent.py:159-198).
 
-Formulas (restated from the reference's `bench_formulas`): box leaves
-`lo < c < lo + 1` with lo = -0.5 - 0.1 level over channels x, y ~ N(0, 1); windows
-[0, 5]:
-  phi1 Always(pair0)                 phi2 Eventually(Always(pair0))
-  phi3 Until(leaf0(x), leaf0(y))     phi4 four nested sequenced visits (depth 3)
-  phi5 visit then stabilise (depth 2) phi6 ten regions in any order (depth 0)
-Per (formula, T, B): the device forward in Hard mode and forward + robustness-mode
-gradient (d rho[:, 0] / d signals) in LogSumExp(10) — the reference's `run_bench`
-measurements (bench.py:87-100) — as medians of CUDA-event timings, plus the oracle port
-(numpy f64, the reference algorithm) on the host at the reference's own sizes.
+For each formula and signal length of the reference's own benchmark (batch 8,
+L in {32, ..., 512}), three engines run the same measurement as the reference's
+`run_bench` (bench.py:87-154): the robustness trace in Hard mode ("value") and the
+entry-0 gradient in LogSumExp(10) ("grad"):
+  * masking   — the reference's masking engine (stlmask from baseline/_ref, numpy, CPU);
+  * recurrent — the reference's recurrent engine (same package, CPU);
+  * b200      — this package's device engine (libstlg.so on cuda:0, CUDA-event timed,
+                inputs resident, one trace call + autograd per repetition).
+`relative` = masking / recurrent - 1 as in the paper's table (negative: masking faster),
+plus b200 / recurrent - 1.  At GPU scale (B=1024, T=10k; phi3 at T=4k since untimed LSE
+Until is O(T^2) per signal) only the device engine runs — the reference engines would take
+hours; their per-sample cost at L=512 is reported for scale.
 
-    python scripts/phi_bench.py [--quick]
+    python scripts/phi_bench.py [--quick] [--out profiles/r2_phi_bench.jsonl]
 """
 import argparse
 import json
 import os
 import statistics
 import sys
-import time
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 import numpy as np
 import torch
 
 import paper_2501_04194_b200 as P
-
-W = P.StepInterval(0, 5)
-
-
-def leaf(level, ch):
-    lo = -0.5 - 0.1 * level
-    return P.And(P.Pred(ch, ">", lo), P.Pred(ch, "<", lo + 1.0))
+from paper_2501_04194_b200.formula import from_json, to_json
 
 
-def pair(level):
-    return P.And(leaf(level, "x"), leaf(level, "y"))
+def reference():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "stlmask")):
+        path = "/root/reference/pkg/src"
+    sys.path.append(path)
+    import stlmask.bench as rb
+    return rb
 
 
-def formulas():
-    phi4 = P.Eventually(pair(0), W)
-    for lvl in (1, 2, 3):
-        phi4 = P.Eventually(P.And(pair(lvl), phi4), W)
-    phi5 = P.Eventually(P.And(pair(2), P.Eventually(P.Always(pair(0), W), W)), W)
-    phi6 = P.Eventually(pair(0), W)
-    for lvl in range(1, 10):
-        phi6 = P.And(P.Eventually(pair(lvl), W), phi6)
-    return {"phi1": P.Always(pair(0)), "phi2": P.Eventually(P.Always(pair(0))),
-            "phi3": P.Until(leaf(0, "x"), leaf(0, "y")), "phi4": phi4, "phi5": phi5, "phi6": phi6}
-
-
-def device_ms(f, B, T, mode, grad, reps):
-    g = torch.Generator(device="cuda").manual_seed(B * 7 + T)
+def device_ms(f, B, T, mode, grad, reps, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed + B * 7 + T)
     x = torch.randn(B, T, device="cuda", generator=g)
     y = torch.randn(B, T, device="cuda", generator=g)
     cfg = P.SemanticsConfig(mode=mode)
 
     def step():
-        xs = x.requires_grad_(grad)
-        ys = y.requires_grad_(grad)
+        xs = x.detach().requires_grad_(grad)
+        ys = y.detach().requires_grad_(grad)
         out = P.trace(f, {"x": xs, "y": ys}, cfg)
         if grad:
             torch.autograd.grad(out[:, 0].sum(), [xs, ys], allow_unused=True)
@@ -81,41 +68,51 @@ def device_ms(f, B, T, mode, grad, reps):
     return statistics.median(ts)
 
 
-def oracle_ms(f, B, T, mode, grad, reps=3):
-    import stl_oracle
-    rng = np.random.default_rng(0)
-    data = {"x": rng.normal(0, 1, (B, T)), "y": rng.normal(0, 1, (B, T))}
-    cfg = P.SemanticsConfig(mode=mode)
-    cot = np.zeros((B, T))
-    cot[:, 0] = 1.0
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        if grad:
-            stl_oracle.trace_and_grad(f, data, cfg, cot)
-        else:
-            stl_oracle.trace(f, data, cfg)
-        ts.append((time.perf_counter() - t0) * 1e3)
-    return statistics.median(ts)
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    fs = formulas()
-    shapes = [(8, 512, True), (1024, 10_000, False)] if not a.quick else [(8, 512, True)]
-    for name, f in fs.items():
-        for B, T, with_oracle in shapes:
-            if name == "phi3" and T > 4000 and not a.quick:
-                T = 4000  # untimed LSE Until is O(T^2) per signal
-            for mname, mode, grad in (("hard_fwd", P.Hard(), False), ("lse10_fwd_grad", P.LogSumExp(10.0), True)):
-                line = {"formula": name, "B": B, "T": T, "measure": mname,
-                        "device_ms": round(device_ms(f, B, T, mode, grad, 7), 4)}
-                if with_oracle:
-                    line["oracle_cpu_ms"] = round(oracle_ms(f, B, T, mode, grad), 2)
-                    line["speedup"] = round(line["oracle_cpu_ms"] / line["device_ms"], 1)
-                print(json.dumps(line), flush=True)
+    rb = reference()
+    sizes = (32, 128, 512) if a.quick else (32, 64, 128, 256, 512)
+    reps = 5 if a.quick else 11
+    # the reference's own measurement (CPU, both engines)
+    ref = rb.run_bench(sizes=sizes, reps=reps, batch=8, include_grad=True, seed=0)
+    lines = []
+    by = {(r["formula"], r["engine"], r["length"]): r for r in ref["results"]}
+    for name, rf in rb.BENCH_FORMULAS.items():
+        f = from_json(to_json(rf))  # the same AST in this package's classes
+        for L in sizes:
+            mask, rec = by[(name, "masking", L)], by[(name, "recurrent", L)]
+            dv = device_ms(f, 8, L, P.Hard(), False, reps) / 1e3
+            dg = device_ms(f, 8, L, P.LogSumExp(10.0), True, reps) / 1e3
+            line = {"formula": name, "batch": 8, "length": L,
+                    "masking_value_s": mask["value_median_s"], "recurrent_value_s": rec["value_median_s"],
+                    "b200_value_s": dv,
+                    "masking_grad_s": mask["grad_median_s"], "recurrent_grad_s": rec["grad_median_s"],
+                    "b200_grad_s": dg,
+                    "value_relative_masking_vs_recurrent": mask["value_median_s"] / rec["value_median_s"] - 1,
+                    "grad_relative_masking_vs_recurrent": mask["grad_median_s"] / rec["grad_median_s"] - 1,
+                    "value_relative_b200_vs_recurrent": dv / rec["value_median_s"] - 1,
+                    "grad_relative_b200_vs_recurrent": dg / rec["grad_median_s"] - 1}
+            lines.append(line)
+            print(json.dumps(line), flush=True)
+    # GPU scale: device engine only
+    for name, rf in rb.BENCH_FORMULAS.items():
+        f = from_json(to_json(rf))
+        B, T = 1024, (4000 if name == "phi3" else 10_000)
+        dv = device_ms(f, B, T, P.Hard(), False, 7)
+        dg = device_ms(f, B, T, P.LogSumExp(10.0), True, 5)
+        ref512 = by[(name, "masking", sizes[-1])]
+        line = {"formula": name, "batch": B, "length": T, "b200_value_ms": dv, "b200_grad_ms": dg,
+                "b200_value_timesteps_per_s": B * T / (dv / 1e3),
+                "reference_masking_grad_s_per_timestep_at_L%d" % sizes[-1]: ref512["grad_median_s"] / (8 * sizes[-1])}
+        lines.append(line)
+        print(json.dumps(line), flush=True)
+    if a.out:
+        with open(a.out, "w") as fh:
+            for ln in lines:
+                fh.write(json.dumps(ln) + "\n")
 
 
 if __name__ == "__main__":

@@ -34,175 +34,160 @@ constexpr int HT_T = 128;    // threads per CTA
 constexpr int HT_NT = 1024;  // outputs (forward) / owned elements (backward) per CTA
 constexpr int HT_R = 1 << 30;  // source flag: right child
 
+// Range state of the reference's Until over a range R = [s0, s1] of candidate ends s:
+//   m  = min l over R, mi its first arg-min,
+//   y  = max_{s in R} min(min l[s0 .. s], r_s), yi the gradient source of y.
+// Combining adjacent ranges A (earlier) and B (later):
+//   m = min(m_A, m_B) (a tie keeps A), y = max(y_A, min(m_A, y_B)) with the source
+//   yi_A if y_A >= min(m_A, y_B), else yi_B if y_B < m_A, else l[mi_A]
+// — the reference's tie rules, so the state of a range is unique and the combine is
+// associative (warp scans may use any bracketing).
+struct HS {
+  float m, y;
+  int mi, yi;
+};
+__device__ __forceinline__ HS hs_elem(float l, float r, int s) {
+  const bool cr = r < l;  // term tie keeps pm
+  return HS{l, cr ? r : l, s, cr ? (s | HT_R) : s};
+}
+__device__ __forceinline__ HS hs_comb(const HS& A, const HS& B) {
+  HS o;
+  const bool am = A.m <= B.m;
+  o.m = am ? A.m : B.m;
+  o.mi = am ? A.mi : B.mi;
+  const bool yb = B.y < A.m;
+  const float cand = yb ? B.y : A.m;
+  const int ci = yb ? B.yi : A.mi;
+  const bool ya = A.y >= cand;
+  o.y = ya ? A.y : cand;
+  o.yi = ya ? A.yi : ci;
+  return o;
+}
+__device__ __forceinline__ HS hs_shfl_up(const HS& v, int o) {
+  return HS{__shfl_up_sync(0xffffffffu, v.m, o), __shfl_up_sync(0xffffffffu, v.y, o),
+            __shfl_up_sync(0xffffffffu, v.mi, o), __shfl_up_sync(0xffffffffu, v.yi, o)};
+}
+__device__ __forceinline__ HS hs_shfl_down(const HS& v, int o) {
+  return HS{__shfl_down_sync(0xffffffffu, v.m, o), __shfl_down_sync(0xffffffffu, v.y, o),
+            __shfl_down_sync(0xffffffffu, v.mi, o), __shfl_down_sync(0xffffffffu, v.yi, o)};
+}
+
+// staged arrays: children, and per position the suffix state over [i, end of its
+// 32-block] and the prefix state over [start of its block, i] (struct-of-arrays)
 struct HTArr {
-  float *l, *r, *X, *Sm, *Y, *SA, *PA;
-  int *dX, *SI, *dY, *SAI, *PAI;
+  float *l, *r;
+  float *sm, *sy, *pm, *py;
+  int *smi, *syi, *pmi, *pyi;
+  __device__ __forceinline__ HS suf(int i) const { return HS{sm[i], sy[i], smi[i], syi[i]}; }
+  __device__ __forceinline__ HS pre(int i) const { return HS{pm[i], py[i], pmi[i], pyi[i]}; }
 };
 
-__device__ __forceinline__ HTArr ht_carve(float* base, int NS, bool has_a) {
+__device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
   HTArr A;
-  A.l = base;
-  A.r = A.l + NS;
-  A.X = A.r + NS;
-  A.Sm = A.X + NS;
-  A.Y = A.Sm + NS;
-  int* ib = reinterpret_cast<int*>(A.Y + NS);
-  A.dX = ib;
-  A.SI = A.dX + NS;
-  A.dY = A.SI + NS;
-  float* fb = reinterpret_cast<float*>(A.dY + NS);
-  A.SA = has_a ? fb : nullptr;
-  A.PA = has_a ? fb + NS : nullptr;
-  int* jb = reinterpret_cast<int*>(fb + 2 * NS);
-  A.SAI = has_a ? jb : nullptr;
-  A.PAI = has_a ? jb + NS : nullptr;
+  float* f = base;
+  A.l = f;
+  A.r = f + NS;
+  A.sm = f + 2 * NS;
+  A.sy = f + 3 * NS;
+  A.pm = f + 4 * NS;
+  A.py = f + 5 * NS;
+  int* q = reinterpret_cast<int*>(f + 6 * NS);
+  A.smi = q;
+  A.syi = q + NS;
+  A.pmi = q + 2 * NS;
+  A.pyi = q + 3 * NS;
   return A;
 }
 
-size_t ht_smem_bytes(int NS, bool has_a) { return (size_t)NS * 4 * (has_a ? 12 : 8); }
+size_t ht_smem_bytes(int NS) { return (size_t)NS * 4 * 10; }
 
-// stage the children over [base, base + NS) and run every block walk
+// stage the children over [base, base + NS) and scan every 32-block (one warp per block,
+// prefix and suffix states by shuffles)
 __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, const HTArr& A) {
-  const int L = (int)p.L, K = p.K, a = p.a;
-  const int hi = min(base + NS, L);  // staged positions [lo, hi)
-  const int lo = max(base, 0);
-  for (int i = threadIdx.x; i < NS; i += blockDim.x) {
-    const int pos = base + i;
-    if (pos >= lo && pos < hi) {
-      A.l[i] = expr_eval<M_HARD>(p.left, row, pos, p.mp);
-      A.r[i] = expr_eval<M_HARD>(p.right, row, pos, p.mp);
+  const int L = (int)p.L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (NS + 31) >> 5;
+  for (int bk = warp; bk < nb; bk += HT_T / 32) {
+    const int i = bk * 32 + lane, pos = base + i;
+    const bool live = i < NS && pos >= 0 && pos < L;
+    float l = 0.f, r = 0.f;
+    if (live) {
+      l = expr_eval<M_HARD>(p.left, row, pos, p.mp);
+      r = expr_eval<M_HARD>(p.right, row, pos, p.mp);
+    }
+    const HS e = hs_elem(l, r, pos);
+    HS pre = e, suf = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const HS a = hs_shfl_up(pre, o);
+      const HS b = hs_shfl_down(suf, o);
+      if (lane >= o) pre = hs_comb(a, pre);
+      if (lane + o < 32) suf = hs_comb(suf, b);
+    }
+    if (i < NS) {
+      A.l[i] = l;
+      A.r[i] = r;
+      A.pm[i] = pre.m;
+      A.py[i] = pre.y;
+      A.pmi[i] = pre.mi;
+      A.pyi[i] = pre.yi;
+      A.sm[i] = suf.m;
+      A.sy[i] = suf.y;
+      A.smi[i] = suf.mi;
+      A.syi[i] = suf.yi;
     }
   }
   __syncthreads();
-  if (lo >= hi) return;
-  // K blocks: backward X / Smin, forward Y
-  const int kb0 = lo / K, kb1 = (hi - 1) / K;
-  for (int kb = kb0 + (int)threadIdx.x; kb <= kb1; kb += blockDim.x) {
-    const int bs = max(kb * K, lo), be = min(kb * K + K - 1, hi - 1);
-    {  // backward walk
-      int i = be - base;
-      float Ll = A.l[i], Rr = A.r[i];
-      bool cR = Rr < Ll;
-      float X = cR ? Rr : Ll, Sm = Ll;
-      int dX = cR ? (be | HT_R) : be, SI = be;
-      A.X[i] = X;
-      A.dX[i] = dX;
-      A.Sm[i] = Sm;
-      A.SI[i] = SI;
-      for (int pos = be - 1; pos >= bs; --pos) {
-        i = pos - base;
-        Ll = A.l[i];
-        Rr = A.r[i];
-        cR = Rr < Ll;
-        const float c = cR ? Rr : Ll;
-        const float m2 = (Ll <= X) ? Ll : X;
-        if (c >= m2) {  // s = u is the first maximiser
-          X = c;
-          dX = cR ? (pos | HT_R) : pos;
-        } else if (!(X < Ll)) {  // clamped at l_u: theta = l_u, source l_u
-          X = Ll;
-          dX = pos;
-        }  // else X(u) = X(u + 1) with its source
-        if (Ll <= Sm) {  // first arg-min: a tie moves to the earlier position
-          Sm = Ll;
-          SI = pos;
-        }
-        A.X[i] = X;
-        A.dX[i] = dX;
-        A.Sm[i] = Sm;
-        A.SI[i] = SI;
+}
+
+// state of the staged range [i0, i1] (inclusive, relative indices)
+__device__ __forceinline__ HS ht_range(const HTArr& A, int i0, int i1, int base) {
+  const int b0 = i0 >> 5, b1 = i1 >> 5;
+  if (b0 == b1) {  // inside one block: element by element (at most 32 steps)
+    HS s = hs_elem(A.l[i0], A.r[i0], base + i0);
+    for (int i = i0 + 1; i <= i1; ++i) s = hs_comb(s, hs_elem(A.l[i], A.r[i], base + i));
+    return s;
+  }
+  HS s = A.suf(i0);
+  for (int bk = b0 + 1; bk < b1; ++bk) s = hs_comb(s, A.pre(bk * 32 + 31));
+  return hs_comb(s, A.pre(i1));
+}
+
+// min of l over [i0, i1] with its first arg-min (the a-prefix A_t of the window)
+__device__ __forceinline__ void ht_minrange(const HTArr& A, int i0, int i1, int base, float& mv, int& mi) {
+  const int b0 = i0 >> 5, b1 = i1 >> 5;
+  if (b0 == b1) {
+    mv = A.l[i0];
+    mi = base + i0;
+    for (int i = i0 + 1; i <= i1; ++i)
+      if (A.l[i] < mv) {
+        mv = A.l[i];
+        mi = base + i;
       }
-    }
-    {  // forward walk
-      int i = bs - base;
-      float Ll = A.l[i], Rr = A.r[i];
-      float M = Ll;
-      int MI = bs;
-      bool cR = Rr < M;
-      float Y = cR ? Rr : M;
-      int dY = cR ? (bs | HT_R) : MI;
-      A.Y[i] = Y;
-      A.dY[i] = dY;
-      for (int pos = bs + 1; pos <= be; ++pos) {
-        i = pos - base;
-        Ll = A.l[i];
-        Rr = A.r[i];
-        if (Ll < M) {  // running min keeps the earlier element on ties
-          M = Ll;
-          MI = pos;
-        }
-        cR = Rr < M;  // term tie keeps pm
-        const float cand = cR ? Rr : M;
-        if (!(Y >= cand)) {  // earlier maximiser wins ties
-          Y = cand;
-          dY = cR ? (pos | HT_R) : MI;
-        }
-        A.Y[i] = Y;
-        A.dY[i] = dY;
-      }
+    return;
+  }
+  mv = A.sm[i0];
+  mi = A.smi[i0];
+  for (int bk = b0 + 1; bk <= b1; ++bk) {
+    const int e = bk < b1 ? bk * 32 + 31 : i1;
+    if (A.pm[e] < mv) {
+      mv = A.pm[e];
+      mi = A.pmi[e];
     }
   }
-  if (a > 0) {  // a blocks: window min of l over [t, t + a - 1]
-    const int ab0 = lo / a, ab1 = (hi - 1) / a;
-    for (int ab = ab0 + (int)threadIdx.x; ab <= ab1; ab += blockDim.x) {
-      const int bs = max(ab * a, lo), be = min(ab * a + a - 1, hi - 1);
-      float S = INFINITY;
-      int SIx = be;
-      for (int pos = be; pos >= bs; --pos) {
-        const float Ll = A.l[pos - base];
-        if (Ll <= S) {
-          S = Ll;
-          SIx = pos;
-        }
-        A.SA[pos - base] = S;
-        A.SAI[pos - base] = SIx;
-      }
-      float Pm = INFINITY;
-      int PI = bs;
-      for (int pos = bs; pos <= be; ++pos) {
-        const float Ll = A.l[pos - base];
-        if (Ll < Pm) {
-          Pm = Ll;
-          PI = pos;
-        }
-        A.PA[pos - base] = Pm;
-        A.PAI[pos - base] = PI;
-      }
-    }
-  }
-  __syncthreads();
 }
 
 // source of out[t] (t + b <= L - 1): position | HT_R for the right child
 __device__ __forceinline__ int ht_source(const UParams& p, int base, int t, const HTArr& A) {
-  const int K = p.K, a = p.a;
-  const int u = t + a, v = t + p.b;
-  const int iu = u - base;
-  float V = A.X[iu];
-  int d = A.dX[iu];
-  if (u % K != 0) {  // the window spills into the next block
-    const float Smv = A.Sm[iu], Yv = A.Y[v - base];
-    const bool sm = Smv <= Yv;
-    const float z = sm ? Smv : Yv;
-    if (!(V >= z)) {
-      V = z;
-      d = sm ? A.SI[iu] : A.dY[v - base];
-    }
+  const int it = t - base, iu = it + p.a, iv = it + p.b;
+  const HS V = ht_range(A, iu, iv, base);
+  if (p.a > 0) {
+    float Av;
+    int Ai;
+    ht_minrange(A, it, iu - 1, base, Av, Ai);
+    if (Av <= V.y) return Ai;  // out = A_t: the first arg-min of l over [t, u - 1]
   }
-  if (a > 0) {
-    const int it = t - base;
-    float Av = A.SA[it];
-    int Ai = A.SAI[it];
-    if (t % a != 0) {
-      const float Pv = A.PA[it + a - 1];
-      if (Pv < Av) {
-        Av = Pv;
-        Ai = A.PAI[it + a - 1];
-      }
-    }
-    if (Av <= V) d = Ai;  // out = A_t: the first arg-min of l over [t, u - 1]
-  }
-  return d;
+  return V.yi;
 }
 
 __global__ void __launch_bounds__(HT_T) k_until_ht_fwd(const __grid_constant__ UParams p) {
@@ -211,7 +196,7 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_fwd(const __grid_constant__ U
   const int L = (int)p.L;
   const int t0 = blockIdx.x * HT_NT;
   const int NS = HT_NT + p.b;
-  const HTArr A = ht_carve(htsm, NS, p.a > 0);
+  const HTArr A = ht_carve(htsm, NS);
   ht_prepare(p, row, t0, NS, A);
   float* outr = p.out + row * L;
   const int tend = min(t0 + HT_NT, L);
@@ -241,7 +226,7 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd(const __grid_constant__ U
   const int t0 = blockIdx.x * HT_NT;
   const int base = t0 - p.b;
   const int NS = HT_NT + 2 * p.b;
-  const HTArr A = ht_carve(htsm, NS, p.a > 0);
+  const HTArr A = ht_carve(htsm, NS);
   for (int i = threadIdx.x; i < HT_NT; i += HT_T) accL[i] = accR[i] = 0ull;
   const float* cot = p.cot + row * L;
   const int tlo = max(base, 0), thi = min(t0 + HT_NT, L);  // outputs that can reach the range
@@ -304,11 +289,11 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd(const __grid_constant__ U
 // true when the O(T) kernels apply (hard, timed, no masked_fill, staging fits)
 bool until_ht_applicable(const UParams& p) {
   if (p.untimed || p.fill || p.K < 1 || p.L >= (1LL << 29)) return false;
-  return ht_smem_bytes(HT_NT + 2 * p.b, p.a > 0) <= 200 * 1024;
+  return ht_smem_bytes(HT_NT + 2 * p.b) <= 200 * 1024;
 }
 
 cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
-  const size_t smem = ht_smem_bytes(HT_NT + p.b, p.a > 0);
+  const size_t smem = ht_smem_bytes(HT_NT + p.b);
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((p.L + HT_NT - 1) / HT_NT), (unsigned)p.B);
@@ -319,7 +304,7 @@ cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
 
 // writes every element of p.gl / p.gr (the caller runs the child VJPs)
 cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st) {
-  const size_t smem = ht_smem_bytes(HT_NT + 2 * p.b, p.a > 0);
+  const size_t smem = ht_smem_bytes(HT_NT + 2 * p.b);
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((p.L + HT_NT - 1) / HT_NT), (unsigned)p.B);

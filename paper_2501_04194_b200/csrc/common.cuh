@@ -230,6 +230,43 @@ __device__ __forceinline__ void expr_vjp(const DExpr& e, long long b, long long 
   }
 }
 
+// A child expression evaluated with its leaf fields in registers: single-leaf affine /
+// trace children (the common Until operands) skip the generic walk's per-sample reads of
+// the expression descriptor; anything else falls back to expr_eval.  Same values, bit for
+// bit (leaf_val's formulas).
+struct ChildEval {
+  const DExpr* e;
+  long long row;
+  const float* p;
+  long long es;
+  float s_in, c, s_out;
+  int kind;  // 0 generic, 1 trace (LEAF_SRC), 2 affine (LEAF_AFFINE)
+  __device__ __forceinline__ ChildEval(const DExpr& ex, long long r) : e(&ex), row(r) {
+    kind = 0;
+    p = nullptr;
+    es = 0;
+    s_in = c = s_out = 0.f;
+    if (ex.n_step == 1) {
+      const DLeaf& L = ex.leaf[0];
+      if (L.kind == LEAF_SRC || L.kind == LEAF_AFFINE) {
+        const DSrc& sr = ex.src[L.src];
+        p = sr.p + r * sr.rs;
+        es = sr.es;
+        s_in = L.s_in;
+        c = L.c;
+        s_out = L.s_out;
+        kind = L.kind == LEAF_SRC ? 1 : 2;
+      }
+    }
+  }
+  template <int MODE>
+  __device__ __forceinline__ float value(long long j, const ModeP& mp) const {
+    if (kind == 1) return s_out * __ldg(p + j * es);
+    if (kind == 2) return s_out * __fadd_rn(s_in * __ldg(p + j * es), c);
+    return expr_eval<MODE>(*e, row, j, mp);
+  }
+};
+
 // Register-resident forms for expressions of exactly N steps (N small): the step loop is
 // unrolled, so the SSA values live in registers and operands are picked by selects
 // instead of dynamically indexed (local-memory) arrays.

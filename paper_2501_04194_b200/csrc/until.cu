@@ -42,11 +42,12 @@ constexpr int U_PERSIST_PER_SM = 6;  // resident CTAs per SM of the persistent b
 template <int MODE>
 __device__ __forceinline__ void stage_children(const UParams& p, long long row, long long lo, int n,
                                                float* Ls, float* Rs) {
+  const ChildEval cl(p.left, row), cr(p.right, row);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     long long j = lo + i;
     if (j < p.L) {
-      Ls[i] = expr_eval<MODE>(p.left, row, j, p.mp);
-      Rs[i] = expr_eval<MODE>(p.right, row, j, p.mp);
+      Ls[i] = cl.value<MODE>(j, p.mp);
+      Rs[i] = cr.value<MODE>(j, p.mp);
     } else if (p.pad_last) {  // padded rows (read by masked_fill windows only)
       Ls[i] = expr_eval<MODE>(p.left, row, p.L - 1, p.mp);
       Rs[i] = expr_eval<MODE>(p.right, row, p.L - 1, p.mp);
@@ -177,12 +178,15 @@ struct USrc {
   const float* Rs;
   const UParams* p;
   long long row, t0;
-  __device__ __forceinline__ float val(const DExpr& ex, long long j) const {
-    if (j < p->L) return expr_eval<MODE>(ex, row, j, p->mp);
-    return p->pad_last ? expr_eval<MODE>(ex, row, p->L - 1, p->mp) : p->pad_value;
+  ChildEval cl, cr;
+  __device__ __forceinline__ USrc(const float* ls, const float* rs, const UParams* pp, long long r, long long t)
+      : Ls(ls), Rs(rs), p(pp), row(r), t0(t), cl(pp->left, r), cr(pp->right, r) {}
+  __device__ __forceinline__ float val(const ChildEval& ce, long long j) const {
+    if (j < p->L) return ce.value<MODE>(j, p->mp);
+    return p->pad_last ? ce.value<MODE>(p->L - 1, p->mp) : p->pad_value;
   }
-  __device__ __forceinline__ float l(int e) const { return STAGED ? Ls[e] : val(p->left, t0 + e); }
-  __device__ __forceinline__ float r(int e) const { return STAGED ? Rs[e] : val(p->right, t0 + e); }
+  __device__ __forceinline__ float l(int e) const { return STAGED ? Ls[e] : val(cl, t0 + e); }
+  __device__ __forceinline__ float r(int e) const { return STAGED ? Rs[e] : val(cr, t0 + e); }
 };
 
 template <int MODE, bool STAGED>
@@ -192,7 +196,7 @@ __device__ __forceinline__ void until_fwd_tile(const UParams& p, long long row, 
   const int span = p.untimed ? (int)(L - t0) : U_THREADS + p.b;
   const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
   const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
-  USrc<MODE, STAGED> src{sm, sm + nst, &p, row, t0};
+  USrc<MODE, STAGED> src(sm, sm + nst, &p, row, t0);
   if (STAGED) {
     if (t0 < nvalid) stage_children<MODE>(p, row, t0, nst, sm, sm + nst);
     __syncthreads();
@@ -347,13 +351,13 @@ __device__ __forceinline__ void until_bwd_tile(const UParams& p, long long row, 
   const int nst = (int)((t0 + span <= L || p.fill) ? span : (L - t0));
   const long long rows = p.untimed ? L : L + p.b;  // column height (masked_fill)
   const int Kmax = p.untimed ? (int)(L - t0) : p.K;
-  USrc<MODE, STAGED> src{sm, sm + nst, &p, row, t0};
+  USrc<MODE, STAGED> src(sm, sm + nst, &p, row, t0);
   const int tid = threadIdx.x;
   const long long t = t0 + tid;
   const bool active = t < nvalid;
   const long long BL = p.B * L;
-  const DetRow gl = det_row(p.dacc, p.dacc + BL, p.dscale, row, L);
-  const DetRow gr = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L);
+  const DetRow gl = det_row(p.dacc, p.dacc + BL, p.dscale, row, L, MODE == M_SOFT);
+  const DetRow gr = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L, MODE == M_SOFT);
   const float* cot = p.cot + row * L;
   if (t0 < L) {
     // overrun outputs route to the pad sources (last padding): left if pl <= pr
@@ -648,13 +652,14 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
   __shared__ Clamp cb[UH_T / 32];
   const long long row = blockIdx.x, L = p.L;
   const int tid = threadIdx.x;
+  const ChildEval cl(p.left, row), cr(p.right, row);
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
   float carry = -INFINITY;
   for (long long c0 = ((L - 1) / UH_CH) * UH_CH; c0 >= 0; c0 -= UH_CH) {
     for (int k = tid; k < UH_CH; k += UH_T) {
       long long t = c0 + k;
-      Ls[uhpos(k)] = t < L ? expr_eval<MODE>(p.left, row, t, p.mp) : 0.f;
-      Rs[uhpos(k)] = t < L ? expr_eval<MODE>(p.right, row, t, p.mp) : 0.f;
+      Ls[uhpos(k)] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
+      Rs[uhpos(k)] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
     }
     __syncthreads();
     // this thread's function f_{t0} o f_{t0+1} o ... o f_{t0+E-1} (identity past the end)
@@ -709,6 +714,7 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* outr = p.out_in + row * L;
   const float* cot = p.cot + row * L;
+  const ChildEval cl(p.left, row), cr(p.right, row);
   double carry = 0.0;  // cotangent accumulated since the last terminator (earlier chunks)
   for (long long c0 = 0; c0 < L; c0 += UH_CH) {
     float g[UH_E];
@@ -721,8 +727,8 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
       term[e] = 0;
       g[e] = 0.f;
       if (t >= L) continue;
-      float l = expr_eval<MODE>(p.left, row, t, p.mp);
-      float r = expr_eval<MODE>(p.right, row, t, p.mp);
+      float l = cl.value<MODE>(t, p.mp);
+      float r = cr.value<MODE>(t, p.mp);
       bool a_is_l = l <= r;
       float A = a_is_l ? l : r;
       int src;
@@ -1108,8 +1114,8 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
     int gprev = 0;
     const int nstage = (int)((L - t0 + UL_T - 1) / UL_T);
     const long long BL = p.B * L;
-    const DetRow gl_row = det_row(p.dacc, p.dacc + BL, p.dscale, row, L);
-    const DetRow gr_row = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L);
+    const DetRow gl_row = det_row(p.dacc, p.dacc + BL, p.dscale, row, L, false);
+    const DetRow gr_row = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L, false);
     for (int s = nstage - 1; s >= 0; --s) {
       const long long k0 = t0 + (long long)s * UL_T;
       __syncthreads();
@@ -1230,7 +1236,7 @@ size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int
 // ---------------------------------------------------------------------------
 // reproducible accumulation (detacc.cuh)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_det_row_scale(const float* __restrict__ cot, long long L,
+__global__ void __launch_bounds__(256) k_det_row_scale(const float* __restrict__ cot, long long L, int span,
                                                        int* __restrict__ S) {
   __shared__ float red[8];
   const long long row = blockIdx.x;
@@ -1241,7 +1247,7 @@ __global__ void __launch_bounds__(256) k_det_row_scale(const float* __restrict__
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
-    S[row] = (m > 0.f && m < INFINITY) ? 28 - ilogbf(m) : 0;
+    S[row] = (m > 0.f && m < INFINITY) ? (span < 0 ? 28 : 61 - span) - ilogbf(m) : 0;
   }
 }
 
@@ -1250,24 +1256,42 @@ __global__ void k_det_finish(const unsigned long long* __restrict__ hi, const un
   const long long n = B * L;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int s = S[i / L];
-    out[i] = (float)((double)(long long)hi[i] * ldexp(1.0, -s) + (double)(long long)lo[i] * ldexp(1.0, -s - 40));
+    const double h = (double)(long long)hi[i] * ldexp(1.0, -s);
+    out[i] = (float)(lo != nullptr ? h + (double)(long long)lo[i] * ldexp(1.0, -s - 40) : h);
   }
 }
 
-static cudaError_t det_begin(const UParams& p, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(p.dacc, 0, sizeof(unsigned long long) * 4 * (size_t)(p.B * p.L), st);
+// softmax: two-word grid (weights outside [0, 1]); hard / LSE: one word, sized for the
+// largest number of outputs that reach one element (b + 1 timed, L untimed / masked_fill)
+static int det_span(int mode, const UParams& p) {
+  if (mode == M_SOFT) return -1;
+  const long long w = (p.untimed || p.fill) ? p.L + 1 : (long long)p.b + 2;
+  int bits = 0;
+  while ((1LL << bits) < w) ++bits;
+  return bits + 1;
+}
+
+static cudaError_t det_begin(int mode, const UParams& p, cudaStream_t st) {
+  const size_t n = (size_t)(p.B * p.L);
+  cudaError_t e = cudaMemsetAsync(p.dacc, 0, sizeof(unsigned long long) * n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.dacc + 2 * n, 0, sizeof(unsigned long long) * n, st);
+  if (e == cudaSuccess && mode == M_SOFT) {
+    e = cudaMemsetAsync(p.dacc + n, 0, sizeof(unsigned long long) * n, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.dacc + 3 * n, 0, sizeof(unsigned long long) * n, st);
+  }
   if (e != cudaSuccess) return e;
-  k_det_row_scale<<<(unsigned)p.B, 256, 0, st>>>(p.cot, p.L, p.dscale);
+  k_det_row_scale<<<(unsigned)p.B, 256, 0, st>>>(p.cot, p.L, det_span(mode, p), p.dscale);
   count_launch();
   return cudaGetLastError();
 }
 
-static cudaError_t det_end(const UParams& p, cudaStream_t st) {
+static cudaError_t det_end(int mode, const UParams& p, cudaStream_t st) {
   const long long n = p.B * p.L;
   const unsigned grid = (unsigned)min((n + 255) / 256, 148LL * 16);
-  k_det_finish<<<grid, 256, 0, st>>>(p.dacc, p.dacc + n, p.dscale, p.B, p.L, p.gl);
+  const bool two = mode == M_SOFT;
+  k_det_finish<<<grid, 256, 0, st>>>(p.dacc, two ? p.dacc + n : nullptr, p.dscale, p.B, p.L, p.gl);
   count_launch();
-  k_det_finish<<<grid, 256, 0, st>>>(p.dacc + 2 * n, p.dacc + 3 * n, p.dscale, p.B, p.L, p.gr);
+  k_det_finish<<<grid, 256, 0, st>>>(p.dacc + 2 * n, two ? p.dacc + 3 * n : nullptr, p.dscale, p.B, p.L, p.gr);
   count_launch();
   return cudaGetLastError();
 }
@@ -1310,7 +1334,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
     if ((e = launch_until_ht_bwd(p, st)) != cudaSuccess) return e;
   } else {
   if (p.dacc == nullptr || p.dscale == nullptr) return cudaErrorInvalidValue;
-  if ((e = det_begin(p, st)) != cudaSuccess) return e;
+  if ((e = det_begin(MODE, p, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
   const size_t ul_smem = (size_t)U_CB_G * 2 * U_THREADS * 4 + (size_t)(ntx * 4 + 4) * sizeof(double);
   if (MODE == M_LSE && p.untimed && !p.fill && p.scratch != nullptr && ul_smem <= kUSmemMax) {
@@ -1348,7 +1372,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   }
   count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = det_end(p, st)) != cudaSuccess) return e;
+  if ((e = det_end(MODE, p, st)) != cudaSuccess) return e;
   }
   // child VJPs from the accumulated cotangents (left first: first-writer order)
   FGParams q;

@@ -107,13 +107,14 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
   const int L = (int)p.L;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (NS + 31) >> 5;
+  const ChildEval cl(p.left, row), cr(p.right, row);
   for (int bk = warp; bk < nb; bk += HT_T / 32) {
     const int i = bk * 32 + lane, pos = base + i;
     const bool live = i < NS && pos >= 0 && pos < L;
     float l = 0.f, r = 0.f;
     if (live) {
-      l = expr_eval<M_HARD>(p.left, row, pos, p.mp);
-      r = expr_eval<M_HARD>(p.right, row, pos, p.mp);
+      l = cl.value<M_HARD>(pos, p.mp);
+      r = cr.value<M_HARD>(pos, p.mp);
     }
     const HS e = hs_elem(l, r, pos);
     HS pre = e, suf = e;

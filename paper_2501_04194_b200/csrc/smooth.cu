@@ -232,10 +232,11 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant__ SParams p) {
-  __shared__ float Gt[S_T + S_CH];
+  __shared__ __align__(16) float Gt[S_T + S_CH + 8];
   __shared__ float Mt[S_T + S_CH];
   __shared__ float Lt[(MODE == M_SOFT) ? S_T + S_CH : 1];
-  __shared__ float LW[S_CH];
+  __shared__ __align__(16) float LW[S_CH + 4];
+  __shared__ float Rc[6][S_T / 32];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
   const int j0 = blockIdx.x * S_T;
@@ -267,6 +268,118 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
     // dense cotangent over the staged range (e.g. the trace-mode ones seed):
     // no per-pair zero test, 4 issue slots + 2 loads per pair
     const int dense = __syncthreads_and(allnz);
+    if (MODE == M_LSE && K <= S_CH) {
+      // factorised, as the forward and the d/dw pass:
+      //   g_t 2^{tau2 (u_j - M_t) + lw_i} = A_t W_i 2^{tau2 (u_j - mmin) + lwmax + ge},
+      //   A_t = ldexp(g_t, -ge) 2^{tau2 (mmin - M_t)},  W_i = 2^{lw_i - lwmax}  (both <= 1),
+      // so a tile whose u and M values span <= 100 / tau2 needs one ex2 per staged element
+      // and one FMA per pair (the per-pair ex2 below made this kernel MUFU-bound).  A
+      // product that flushes to zero is < 2^-26 |g|max: below the tolerance.  The child sum
+      // is a convolution in the offset, i.e. a correlation against the reversed weights.
+      const int nq = S_T + kc - 1;
+      float umx = -INFINITY, umn = INFINITY, mmx = -INFINITY, mmn = INFINITY, gmx = 0.f, lwm = -INFINITY;
+      bool bad = false;
+      if (j <= jmax) {
+        umx = umn = uj;
+        bad = !(fabsf(uj) < INFINITY);
+      }
+      for (int q = threadIdx.x; q < nq; q += S_T) {
+        const float g = Gt[q];
+        if (g != 0.f) {
+          mmx = fmaxf(mmx, Mt[q]);
+          mmn = fminf(mmn, Mt[q]);
+          gmx = fmaxf(gmx, fabsf(g));
+          bad |= !(fabsf(Mt[q]) < INFINITY) || !(fabsf(g) < INFINITY);
+        }
+      }
+      for (int q = threadIdx.x; q < kc; q += S_T) lwm = fmaxf(lwm, LW[q]);
+      for (int o = 16; o > 0; o >>= 1) {
+        umx = fmaxf(umx, __shfl_xor_sync(0xffffffffu, umx, o));
+        umn = fminf(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+        mmx = fmaxf(mmx, __shfl_xor_sync(0xffffffffu, mmx, o));
+        mmn = fminf(mmn, __shfl_xor_sync(0xffffffffu, mmn, o));
+        gmx = fmaxf(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+        lwm = fmaxf(lwm, __shfl_xor_sync(0xffffffffu, lwm, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        Rc[0][threadIdx.x >> 5] = umx;
+        Rc[1][threadIdx.x >> 5] = umn;
+        Rc[2][threadIdx.x >> 5] = mmx;
+        Rc[3][threadIdx.x >> 5] = mmn;
+        Rc[4][threadIdx.x >> 5] = gmx;
+        Rc[5][threadIdx.x >> 5] = lwm;
+      }
+      bad = __syncthreads_or(bad);
+      umx = Rc[0][0], umn = Rc[1][0], mmx = Rc[2][0], mmn = Rc[3][0], gmx = Rc[4][0], lwm = Rc[5][0];
+      for (int w = 1; w < S_T / 32; ++w) {
+        umx = fmaxf(umx, Rc[0][w]);
+        umn = fminf(umn, Rc[1][w]);
+        mmx = fmaxf(mmx, Rc[2][w]);
+        mmn = fminf(mmn, Rc[3][w]);
+        gmx = fmaxf(gmx, Rc[4][w]);
+        lwm = fmaxf(lwm, Rc[5][w]);
+      }
+      if (gmx == 0.f) {  // no cotangent reaches this tile's children: acc stays 0
+        __syncthreads();
+        continue;  // K <= S_CH: the only chunk
+      }
+      const float span = tau2 * (fmaxf(umx, mmx) - fminf(umn, mmn));
+      if (!bad && span <= 100.f && gmx < INFINITY && lwm > -INFINITY) {
+        int ge;
+        frexpf(gmx, &ge);
+        __syncthreads();  // Rc read everywhere; Gt / LW are rewritten in place below
+        for (int q = threadIdx.x; q < S_T + kc + 7; q += S_T) {
+          float a = 0.f;
+          if (q < nq) {
+            const float g = Gt[q];
+            a = g != 0.f ? ldexpf(g, -ge) * ex2f(tau2 * (mmn - Mt[q])) : 0.f;
+          }
+          Gt[q] = a;
+        }
+        float wr[4];  // reversed weights (each thread rewrites the slots it read)
+        const int kc4 = (kc + 3) & ~3;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int q = threadIdx.x + r * S_T;
+          wr[r] = q < kc ? ex2f(LW[kc - 1 - q] - lwm) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int q = threadIdx.x + r * S_T;
+          if (q < kc4) LW[q] = wr[r];
+        }
+        __syncthreads();
+        {
+          const int o = threadIdx.x & (S_T / 4 - 1), g = threadIdx.x / (S_T / 4);
+          const int chunk = ((kc4 >> 2) + 3) & ~3;
+          const int kb = g * chunk, ke = min(kc4, kb + chunk);
+          const float4* A4 = reinterpret_cast<const float4*>(Gt);
+          const float4* W4 = reinterpret_cast<const float4*>(LW);
+          float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
+          for (int k = kb; k < ke; k += 4) {
+            const float4 w = W4[k >> 2];
+            const float4 a = A4[o + (k >> 2)], b = A4[o + (k >> 2) + 1];
+            r0 = fmaf(w.x, a.x, fmaf(w.y, a.y, fmaf(w.z, a.z, fmaf(w.w, a.w, r0))));
+            r1 = fmaf(w.x, a.y, fmaf(w.y, a.z, fmaf(w.z, a.w, fmaf(w.w, b.x, r1))));
+            r2 = fmaf(w.x, a.z, fmaf(w.y, a.w, fmaf(w.z, b.x, fmaf(w.w, b.y, r2))));
+            r3 = fmaf(w.x, a.w, fmaf(w.y, b.x, fmaf(w.z, b.y, fmaf(w.w, b.z, r3))));
+          }
+          __syncthreads();  // LW becomes the cross-group reduction buffer
+          LW[g * S_T + 4 * o] = r0;
+          LW[g * S_T + 4 * o + 1] = r1;
+          LW[g * S_T + 4 * o + 2] = r2;
+          LW[g * S_T + 4 * o + 3] = r3;
+          __syncthreads();
+        }
+        if (j <= jmax) {
+          const float sum = (LW[threadIdx.x] + LW[S_T + threadIdx.x]) + (LW[2 * S_T + threadIdx.x] + LW[3 * S_T + threadIdx.x]);
+          acc = ldexpf(sum * ex2f(fmaf(tau2, uj - mmn, lwm)), ge);
+        }
+        __syncthreads();
+        continue;  // K <= S_CH: the only chunk
+      }
+    }
     if (MODE == M_LSE && dense && fabsf(uj) < INFINITY) {  // (an infinite u_j takes the exact path)
       if (j <= jmax) {
         float a0 = 0.f, a1 = 0.f;

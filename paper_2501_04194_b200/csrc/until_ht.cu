@@ -83,7 +83,6 @@ struct HTArr {
 };
 
 __device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
-  NS = (NS + 31) & ~31;  // whole 32-blocks (the loads fill the padding)
   HTArr A;
   float* f = base;
   A.l = f;
@@ -100,7 +99,7 @@ __device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
   return A;
 }
 
-size_t ht_smem_bytes(int NS) { return (size_t)((NS + 31) & ~31) * 4 * 10; }
+size_t ht_smem_bytes(int NS) { return (size_t)NS * 4 * 10; }
 
 // stage the children over [base, base + NS) and scan every 32-block (one warp per block,
 // prefix and suffix states by shuffles)
@@ -109,18 +108,14 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (NS + 31) >> 5;
   const ChildEval cl(p.left, row), cr(p.right, row);
-  // loads first (all of a thread's samples in flight), then the scans from shared memory
-#pragma unroll 4
-  for (int i = threadIdx.x; i < nb * 32; i += HT_T) {
-    const int pos = base + i;
-    const bool live = i < NS && pos >= 0 && pos < L;
-    A.l[i] = live ? cl.value<M_HARD>(pos, p.mp) : 0.f;
-    A.r[i] = live ? cr.value<M_HARD>(pos, p.mp) : 0.f;
-  }
-  __syncthreads();
   for (int bk = warp; bk < nb; bk += HT_T / 32) {
     const int i = bk * 32 + lane, pos = base + i;
-    const float l = A.l[i], r = A.r[i];
+    const bool live = i < NS && pos >= 0 && pos < L;
+    float l = 0.f, r = 0.f;
+    if (live) {
+      l = cl.value<M_HARD>(pos, p.mp);
+      r = cr.value<M_HARD>(pos, p.mp);
+    }
     const HS e = hs_elem(l, r, pos);
     HS pre = e, suf = e;
 #pragma unroll
@@ -131,6 +126,8 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
       if (lane + o < 32) suf = hs_comb(suf, b);
     }
     if (i < NS) {
+      A.l[i] = l;
+      A.r[i] = r;
       A.pm[i] = pre.m;
       A.py[i] = pre.y;
       A.pmi[i] = pre.mi;

@@ -4,7 +4,8 @@ One JSON line per (config, mode): trace-mode step = full trace forward + ones-co
 VJP into every signal channel (and d(a, b, c) for C4), CUDA events around eager calls
 through the engine API (plan cached, workspace preallocated), median of `reps` after
 warm-up.  Inputs per SURVEY §8(d): C1 x ~ N(0,1); C2 2-D random walks; C3 x, y, z ~
-N(0,1); C4 smooth-interval bounds (0.3, 0.65, 9.0) over N(0,1) steps; C5 x, y ~ N(0,1).
+N(0,1); C4 smooth-interval bounds (0.3, 0.65, 9.0) over synth_step_dataset(seed=3)
+(apps.py:252-269); C5 x, y ~ N(0,1).
 
     python scripts/configs_bench.py [--quick]
 """
@@ -121,7 +122,7 @@ def main():
     si = P.SmoothInterval(0.3, 0.65, 9.0)
     f4 = P.Always(P.Pred("x", ">", 0.0), si)
     comp = compile_formula(f4, ["x"], P.SemanticsConfig(mode=P.LogSumExp(5.0)))
-    x4 = torch.cumsum(0.1 * randn(B, T), dim=1)
+    x4 = torch.tensor(np.asarray(P.synth_step_dataset(3, B, T), dtype=np.float32), device=dev)
     if want("C4"):
         fm, bm = timed(comp, {"x": x4}, B, T, smooth=(si.a, si.b, si.c), reps=3)
         emit("C4", "lse5", B, T, fm, bm, grads="x and (a, b, c)")

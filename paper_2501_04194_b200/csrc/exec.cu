@@ -622,9 +622,14 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
   if (!smooth_range(sp, T, &i_lo, &i_hi))
     return fail(STLG_E_EMPTY_WINDOW, "smooth interval produced an all-zero weight vector");
   float* tab = bf.tables + (size_t)e.table * 2 * (size_t)T;
-  cudaError_t ce = launch_smooth_table(sp.a, sp.b, sp.c, sp.eps, T, i_lo, i_hi, tab, st);
+  cudaError_t ce = cudaSuccess;
   int rc;
-  if ((rc = cuda_status(ce, "weight table"))) return rc;
+  // the forward builds the table in its workspace; the backward (same workspace and
+  // parameters) reads it
+  if (!backward) {
+    ce = launch_smooth_table(sp.a, sp.b, sp.c, sp.eps, T, i_lo, i_hi, tab, st);
+    if ((rc = cuda_status(ce, "weight table"))) return rc;
+  }
   const int mode = plan->cfg.mode;
   if (mode == STLG_MODE_HARD) {
     FGParams p;

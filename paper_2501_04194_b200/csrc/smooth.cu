@@ -656,20 +656,20 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
 
 // dw64[i] = sum over the partial rows in a fixed order (32 offsets x 8 partial strides
 // per CTA, then a fixed-shape tree): deterministic
-__global__ void __launch_bounds__(256) k_smooth_dw_reduce(const double* __restrict__ part, long long parts,
-                                                          long long L, int i_lo, int i_hi, double* dw64) {
-  __shared__ double s[8][33];
+__global__ void __launch_bounds__(1024) k_smooth_dw_reduce(const double* __restrict__ part, long long parts,
+                                                           long long L, int i_lo, int i_hi, double* dw64) {
+  __shared__ double s[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * 32 + lane;
   double acc = 0.0;
   if (i >= i_lo && i <= i_hi)
-    for (long long q = w; q < parts; q += 8) acc += part[q * L + i];
+    for (long long q = w; q < parts; q += 32) acc += part[q * L + i];
   s[w][lane] = acc;
   __syncthreads();
   if (w == 0 && i < L) {
     double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += s[k][lane];
+    for (int k = 0; k < 32; ++k) t += s[k][lane];
     dw64[i] = t;
   }
 }
@@ -759,7 +759,7 @@ cudaError_t launch_smooth_bwd(int mode, SParams& p, cudaStream_t st) {
     else k_smooth_bwd_w<M_SOFT><<<(unsigned)parts, S_T, 0, st>>>(p);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_smooth_dw_reduce<<<(unsigned)((p.L + 31) / 32), 256, 0, st>>>(p.dwpart, parts, p.L, p.i_lo, p.i_hi,
+    k_smooth_dw_reduce<<<(unsigned)((p.L + 31) / 32), 1024, 0, st>>>(p.dwpart, parts, p.L, p.i_lo, p.i_hi,
                                                                      p.dw64);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -794,18 +794,21 @@ __global__ void __launch_bounds__(1024) k_smooth_table(double a, double b, doubl
     lw2[i] = w > 0.0 ? (float)log2(w) : -INFINITY;
     s += w;
   }
-  part[tid] = s;
-  __syncthreads();
-  if (tid == 0) {  // exclusive suffix totals of the thread segments, in a fixed order
-    double acc = 0.0;
-    for (int k = 1023; k >= 0; --k) {
-      const double v = part[k];
-      part[k] = acc;
-      acc += v;
-    }
+  // exclusive suffix totals of the thread segments: warp shuffles, then the later warps
+  // (fixed shape, so the same table every call)
+  const int lane = tid & 31, warp = tid >> 5;
+  double inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double v = __shfl_down_sync(0xffffffffu, inc, o);
+    if (lane + o < 32) inc += v;
   }
+  if (lane == 0) part[warp] = inc;
   __syncthreads();
-  double suf = part[tid];
+  double later = 0.0;
+  for (int w = 31; w > warp; --w) later += part[w];
+  const double nxt = __shfl_down_sync(0xffffffffu, inc, 1);
+  double suf = later + (lane < 31 ? nxt : 0.0);
   for (long long m = m1 - 1; m >= m0; --m) {
     suf += wgt(m);
     lw2[L + m] = suf > 0.0 ? (float)log2(suf) : -INFINITY;

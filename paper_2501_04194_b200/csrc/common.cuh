@@ -239,12 +239,17 @@ struct ChildEval {
   long long row;
   const float* p;
   long long es;
+  float* gp;       // gradient destination row (or null)
+  long long ges;
+  int gst;         // 1: store (first writer), 0: accumulate
   float s_in, c, s_out;
   int kind;  // 0 generic, 1 trace (LEAF_SRC), 2 affine (LEAF_AFFINE)
   __device__ __forceinline__ ChildEval(const DExpr& ex, long long r) : e(&ex), row(r) {
     kind = 0;
     p = nullptr;
-    es = 0;
+    gp = nullptr;
+    es = ges = 0;
+    gst = 0;
     s_in = c = s_out = 0.f;
     if (ex.n_step == 1) {
       const DLeaf& L = ex.leaf[0];
@@ -252,12 +257,31 @@ struct ChildEval {
         const DSrc& sr = ex.src[L.src];
         p = sr.p + r * sr.rs;
         es = sr.es;
+        const DDst& d = ex.dst[L.src];
+        if (d.p) {
+          gp = d.p + r * d.rs;
+          ges = d.es;
+        }
+        gst = L.st1;
         s_in = L.s_in;
         c = L.c;
         s_out = L.s_out;
         kind = L.kind == LEAF_SRC ? 1 : 2;
       }
     }
+  }
+  // the child's VJP at j for cotangent g (leaf_vjp / expr_vjp, same arithmetic)
+  template <int MODE>
+  __device__ __forceinline__ void grad(long long j, float g, const ModeP& mp) const {
+    if (kind == 0) {
+      expr_vjp<MODE>(*e, row, j, g, mp);
+      return;
+    }
+    if (gp == nullptr) return;
+    const float v = kind == 1 ? g * s_out : g * s_out * s_in;
+    float* q = gp + j * ges;
+    if (gst) *q = v;
+    else *q += v;
   }
   template <int MODE>
   __device__ __forceinline__ float value(long long j, const ModeP& mp) const {

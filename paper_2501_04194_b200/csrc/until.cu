@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
 // each child cotangent is final when its run ends (no atomics, fused VJPs).
 template <int MODE>
 __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_constant__ UParams p) {
+  __shared__ float Ls[UH_T * UH_S], Rs[UH_T * UH_S], Os[UH_T * UH_S], Gs[UH_T * UH_S];
   __shared__ double wsum[UH_T / 32];
   __shared__ int wflag[UH_T / 32];
   const long long row = blockIdx.x, L = p.L;
@@ -717,36 +718,49 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
   const ChildEval cl(p.left, row), cr(p.right, row);
   double carry = 0.0;  // cotangent accumulated since the last terminator (earlier chunks)
   for (long long c0 = 0; c0 < L; c0 += UH_CH) {
+    // coalesced staging of l, r, out[t + 1] and the cotangent
+    for (int k = tid; k < UH_CH; k += UH_T) {
+      const long long t = c0 + k;
+      const int q = uhpos(k);
+      if (t < L) {
+        Ls[q] = cl.value<MODE>(t, p.mp);
+        Rs[q] = cr.value<MODE>(t, p.mp);
+        Os[q] = t + 1 < L ? outr[t + 1] : 0.f;
+        Gs[q] = cot[t];
+      }
+    }
+    __syncthreads();
     float g[UH_E];
     int term[UH_E];  // 0: pass to the next sample's source, 1: l_t, 2: r_t
     double tail = 0.0;
     int anyterm = 0;
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      long long t = c0 + tid * UH_E + e;
+      const long long t = c0 + tid * UH_E + e;
+      const int q = tid * UH_S + e;
       term[e] = 0;
       g[e] = 0.f;
-      if (t >= L) continue;
-      float l = cl.value<MODE>(t, p.mp);
-      float r = cr.value<MODE>(t, p.mp);
-      bool a_is_l = l <= r;
-      float A = a_is_l ? l : r;
-      int src;
-      if (t == L - 1) {
-        src = a_is_l ? 1 : 2;
-      } else {
-        float v = outr[t + 1];
-        bool b_is_l = l <= v;
-        float Bv = b_is_l ? l : v;
-        src = (A >= Bv) ? (a_is_l ? 1 : 2) : (b_is_l ? 1 : 0);
-      }
-      term[e] = src;
-      g[e] = cot[t];
-      if (src) {
-        anyterm = 1;
-        tail = 0.0;
-      } else {
-        tail += (double)g[e];
+      if (t < L) {
+        const float l = Ls[q], r = Rs[q];
+        const bool a_is_l = l <= r;
+        const float A = a_is_l ? l : r;
+        int src;
+        if (t == L - 1) {
+          src = a_is_l ? 1 : 2;
+        } else {
+          const float v = Os[q];
+          const bool b_is_l = l <= v;
+          const float Bv = b_is_l ? l : v;
+          src = (A >= Bv) ? (a_is_l ? 1 : 2) : (b_is_l ? 1 : 0);
+        }
+        term[e] = src;
+        g[e] = Gs[q];
+        if (src) {
+          anyterm = 1;
+          tail = 0.0;
+        } else {
+          tail += (double)g[e];
+        }
       }
     }
     // exclusive segmented prefix (sum since the last terminator) over the earlier threads:
@@ -775,10 +789,10 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
     double run = xf ? xs : before + xs;
     double nextc = carry;
     for (int w = 0; w < UH_T / 32; ++w) nextc = wflag[w] ? wsum[w] : nextc + wsum[w];
+    // the thread's gradients into its own staging slots (l -> Ls, r -> Rs)
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      long long t = c0 + tid * UH_E + e;
-      if (t >= L) break;
+      const int q = tid * UH_S + e;
       run += (double)g[e];
       float gl = 0.f, gr = 0.f;
       if (term[e] == 1) {
@@ -788,8 +802,17 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
         gr = (float)run;
         run = 0.0;
       }
-      expr_vjp<MODE>(p.left, row, t, gl, p.mp);
-      expr_vjp<MODE>(p.right, row, t, gr, p.mp);
+      Ls[q] = gl;
+      Rs[q] = gr;
+    }
+    __syncthreads();
+    // coalesced child VJPs (left first: first-writer order)
+    for (int k = tid; k < UH_CH; k += UH_T) {
+      const long long t = c0 + k;
+      if (t >= L) break;
+      const int q = uhpos(k);
+      cl.grad<MODE>(t, Ls[q], p.mp);
+      cr.grad<MODE>(t, Rs[q], p.mp);
     }
     carry = nextc;
     __syncthreads();

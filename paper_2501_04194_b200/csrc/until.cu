@@ -656,10 +656,20 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
   float carry = -INFINITY;
   for (long long c0 = ((L - 1) / UH_CH) * UH_CH; c0 >= 0; c0 -= UH_CH) {
-    for (int k = tid; k < UH_CH; k += UH_T) {
-      long long t = c0 + k;
-      Ls[uhpos(k)] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
-      Rs[uhpos(k)] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
+    {  // all of the thread's loads in flight before the first store (one CTA per row:
+       // nothing else hides the latency)
+      float lv[UH_E], rv[UH_E];
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        const long long t = c0 + tid + e * UH_T;
+        lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
+        rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        Ls[uhpos(tid + e * UH_T)] = lv[e];
+        Rs[uhpos(tid + e * UH_T)] = rv[e];
+      }
     }
     __syncthreads();
     // this thread's function f_{t0} o f_{t0+1} o ... o f_{t0+E-1} (identity past the end)
@@ -718,15 +728,24 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
   const ChildEval cl(p.left, row), cr(p.right, row);
   double carry = 0.0;  // cotangent accumulated since the last terminator (earlier chunks)
   for (long long c0 = 0; c0 < L; c0 += UH_CH) {
-    // coalesced staging of l, r, out[t + 1] and the cotangent
-    for (int k = tid; k < UH_CH; k += UH_T) {
-      const long long t = c0 + k;
-      const int q = uhpos(k);
-      if (t < L) {
-        Ls[q] = cl.value<MODE>(t, p.mp);
-        Rs[q] = cr.value<MODE>(t, p.mp);
-        Os[q] = t + 1 < L ? outr[t + 1] : 0.f;
-        Gs[q] = cot[t];
+    {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
+      float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        const long long t = c0 + tid + e * UH_T;
+        const bool in = t < L;
+        lv[e] = in ? cl.value<MODE>(t, p.mp) : 0.f;
+        rv[e] = in ? cr.value<MODE>(t, p.mp) : 0.f;
+        ov[e] = (t + 1 < L) ? outr[t + 1] : 0.f;
+        gv[e] = in ? cot[t] : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        const int q = uhpos(tid + e * UH_T);
+        Ls[q] = lv[e];
+        Rs[q] = rv[e];
+        Os[q] = ov[e];
+        Gs[q] = gv[e];
       }
     }
     __syncthreads();

@@ -289,6 +289,12 @@ struct ChildEval {
     if (kind == 2) return s_out * __fadd_rn(s_in * __ldg(p + j * es), c);
     return expr_eval<MODE>(*e, row, j, mp);
   }
+  // fast kinds only (kind != 0): the load and the leaf transform apart, so a caller can
+  // issue a batch of loads before the first use
+  __device__ __forceinline__ float raw(long long j) const { return __ldg(p + j * es); }
+  __device__ __forceinline__ float apply(float x) const {
+    return kind == 1 ? s_out * x : s_out * __fadd_rn(s_in * x, c);
+  }
 };
 
 // Register-resident forms for expressions of exactly N steps (N small): the step loop is

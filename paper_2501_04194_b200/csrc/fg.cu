@@ -76,6 +76,92 @@ __global__ void __launch_bounds__(PW_T) k_pointwise_vjp(const __grid_constant__ 
   }
 }
 
+// Binary root over two trace / affine leaves (And / Or of two sub-formulas — the usual
+// pointwise root): both leaves resolved into registers once per thread.
+struct PwLeaf {
+  const float* p;
+  long long es;
+  float* gp;
+  long long ges;
+  int gst, src;  // src: 1 trace (LEAF_SRC), 0 affine
+  float s_in, c, s_out;
+  __device__ __forceinline__ PwLeaf(const DExpr& e, const DLeaf& L, long long row) {
+    const DSrc& sr = e.src[L.src];
+    p = sr.p + row * sr.rs;
+    es = sr.es;
+    const DDst& d = e.dst[L.src];
+    gp = d.p ? d.p + row * d.rs : nullptr;
+    ges = d.es;
+    gst = L.st1;
+    src = L.kind == LEAF_SRC;
+    s_in = L.s_in;
+    c = L.c;
+    s_out = L.s_out;
+  }
+  __device__ __forceinline__ float value(long long j) const {
+    const float x = __ldg(p + j * es);
+    return src ? s_out * x : s_out * __fadd_rn(s_in * x, c);
+  }
+  __device__ __forceinline__ void grad(long long j, float g) const {
+    if (gp == nullptr || (g == 0.f && !gst)) return;
+    const float v = src ? g * s_out : g * s_out * s_in;
+    float* q = gp + j * ges;
+    if (gst) *q = v;
+    else *q += v;
+  }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(PW_T) k_pointwise2_fwd(const __grid_constant__ FGParams p) {
+  const int L = (int)p.L;
+  const DExpr& e = p.child;
+  const float sg = e.step[2].op == ST_MAX ? 1.f : -1.f;
+  for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
+    const PwLeaf a(e, e.leaf[e.step[0].a], row), b(e, e.leaf[e.step[1].a], row);
+    float* out = p.out + row * L;
+#pragma unroll
+    for (int k = 0; k < PW_E; ++k) {
+      const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
+      if (t < L) {
+        float w1, w2;
+        out[t] = pair_red<MODE>(a.value(t), b.value(t), sg, p.mp, w1, w2);
+      }
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(PW_T) k_pointwise2_vjp(const __grid_constant__ FGParams p,
+                                                        const float* __restrict__ g) {
+  const int L = (int)p.L;
+  const DExpr& e = p.child;
+  const float sg = e.step[2].op == ST_MAX ? 1.f : -1.f;
+  for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
+    const PwLeaf a(e, e.leaf[e.step[0].a], row), b(e, e.leaf[e.step[1].a], row);
+    const float* gr = g + row * L;
+#pragma unroll
+    for (int k = 0; k < PW_E; ++k) {
+      const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
+      if (t < L) {
+        float w1, w2;
+        pair_red<MODE>(a.value(t), b.value(t), sg, p.mp, w1, w2);
+        const float gv = gr[t];
+        b.grad(t, 0.f + gv * w2);  // expr_vjp order (the later step first) and its 0 + adj
+        a.grad(t, 0.f + gv * w1);
+      }
+    }
+  }
+}
+
+static bool pw_binary(const DExpr& e) {
+  if (e.n_step != 3 || e.step[0].op != ST_LEAF || e.step[1].op != ST_LEAF || e.step[2].op == ST_LEAF ||
+      e.step[2].a != 0 || e.step[2].b != 1)
+    return false;
+  const DLeaf &l0 = e.leaf[e.step[0].a], &l1 = e.leaf[e.step[1].a];
+  auto fast = [](const DLeaf& L) { return L.kind == LEAF_SRC || L.kind == LEAF_AFFINE; };
+  return fast(l0) && fast(l1);
+}
+
 #define PW_DISPATCH(NSV, ...)                                    \
   switch (NSV) {                                                 \
     case 1: { constexpr int NS = 1; __VA_ARGS__; } break;        \
@@ -116,6 +202,13 @@ static int grid_for(long long n, int threads) {
 
 cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st) {
   const dim3 grid = pw_grid(p);
+  if (pw_binary(p.child)) {
+    if (mode == M_HARD) k_pointwise2_fwd<M_HARD><<<grid, PW_T, 0, st>>>(p);
+    else if (mode == M_LSE) k_pointwise2_fwd<M_LSE><<<grid, PW_T, 0, st>>>(p);
+    else k_pointwise2_fwd<M_SOFT><<<grid, PW_T, 0, st>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
   PW_DISPATCH(p.child.n_step,
               if (mode == M_HARD) k_pointwise_fwd<M_HARD, NS><<<grid, PW_T, 0, st>>>(p);
               else if (mode == M_LSE) k_pointwise_fwd<M_LSE, NS><<<grid, PW_T, 0, st>>>(p);
@@ -126,6 +219,13 @@ cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st) {
 
 cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cudaStream_t st) {
   const dim3 grid = pw_grid(p);
+  if (pw_binary(p.child)) {
+    if (mode == M_HARD) k_pointwise2_vjp<M_HARD><<<grid, PW_T, 0, st>>>(p, g);
+    else if (mode == M_LSE) k_pointwise2_vjp<M_LSE><<<grid, PW_T, 0, st>>>(p, g);
+    else k_pointwise2_vjp<M_SOFT><<<grid, PW_T, 0, st>>>(p, g);
+    count_launch();
+    return cudaGetLastError();
+  }
   PW_DISPATCH(p.child.n_step,
               if (mode == M_HARD) k_pointwise_vjp<M_HARD, NS><<<grid, PW_T, 0, st>>>(p, g);
               else if (mode == M_LSE) k_pointwise_vjp<M_LSE, NS><<<grid, PW_T, 0, st>>>(p, g);

@@ -659,11 +659,27 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_consta
     {  // all of the thread's loads in flight before the first store (one CTA per row:
        // nothing else hides the latency)
       float lv[UH_E], rv[UH_E];
+      if (cl.kind != 0 && cr.kind != 0) {
 #pragma unroll
-      for (int e = 0; e < UH_E; ++e) {
-        const long long t = c0 + tid + e * UH_T;
-        lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
-        rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
+        for (int e = 0; e < UH_E; ++e) {
+          const long long t = c0 + tid + e * UH_T;
+          const long long tc = t < L ? t : L - 1;
+          lv[e] = cl.raw(tc);
+          rv[e] = cr.raw(tc);
+        }
+#pragma unroll
+        for (int e = 0; e < UH_E; ++e) {
+          const bool in = c0 + tid + e * UH_T < L;
+          lv[e] = in ? cl.apply(lv[e]) : 0.f;
+          rv[e] = in ? cr.apply(rv[e]) : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < UH_E; ++e) {
+          const long long t = c0 + tid + e * UH_T;
+          lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
+          rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
+        }
       }
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {
@@ -730,14 +746,32 @@ __global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_consta
   for (long long c0 = 0; c0 < L; c0 += UH_CH) {
     {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
       float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
+      const bool fast = cl.kind != 0 && cr.kind != 0;
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        const long long t = c0 + tid + e * UH_T;
+        const long long tc = t < L ? t : L - 1;
+        const long long to = t + 1 < L ? t + 1 : L - 1;
+        if (fast) {
+          lv[e] = cl.raw(tc);
+          rv[e] = cr.raw(tc);
+        }
+        ov[e] = outr[to];
+        gv[e] = cot[tc];
+      }
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {
         const long long t = c0 + tid + e * UH_T;
         const bool in = t < L;
-        lv[e] = in ? cl.value<MODE>(t, p.mp) : 0.f;
-        rv[e] = in ? cr.value<MODE>(t, p.mp) : 0.f;
-        ov[e] = (t + 1 < L) ? outr[t + 1] : 0.f;
-        gv[e] = in ? cot[t] : 0.f;
+        if (fast) {
+          lv[e] = in ? cl.apply(lv[e]) : 0.f;
+          rv[e] = in ? cr.apply(rv[e]) : 0.f;
+        } else {
+          lv[e] = in ? cl.value<MODE>(t, p.mp) : 0.f;
+          rv[e] = in ? cr.value<MODE>(t, p.mp) : 0.f;
+        }
+        ov[e] = (t + 1 < L) ? ov[e] : 0.f;
+        gv[e] = in ? gv[e] : 0.f;
       }
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {

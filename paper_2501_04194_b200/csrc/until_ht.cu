@@ -112,7 +112,14 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
     const int i = bk * 32 + lane, pos = base + i;
     const bool live = i < NS && pos >= 0 && pos < L;
     float l = 0.f, r = 0.f;
-    if (live) {
+    if (cl.kind != 0 && cr.kind != 0) {  // loads issued before the transforms
+      const int pc = live ? pos : 0;
+      const float xl = cl.raw(pc), xr = cr.raw(pc);
+      if (live) {
+        l = cl.apply(xl);
+        r = cr.apply(xr);
+      }
+    } else if (live) {
       l = cl.value<M_HARD>(pos, p.mp);
       r = cr.value<M_HARD>(pos, p.mp);
     }

@@ -81,9 +81,11 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
       // 2^-126, i.e. < 2^-30 of that term, below fp32 resolution of the sum.  Wider tiles
       // (or non-finite values) take the exact grouped path below.
       float umax = -INFINITY, umin = INFINITY, lwmax = -INFINITY;
+      bool nan_u = false;  // fmaxf / fminf drop NaN: flag it explicitly (exact path below)
       for (int q = threadIdx.x; q < S_T + kc - 1; q += S_T) {
         umax = fmaxf(umax, U[q]);
         umin = fminf(umin, U[q]);
+        nan_u |= U[q] != U[q];
       }
       for (int q = threadIdx.x; q < kc; q += S_T) lwmax = fmaxf(lwmax, LW[q]);
       for (int o = 16; o > 0; o >>= 1) {
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
         Red[1][threadIdx.x >> 5] = umin;
         Red[2][threadIdx.x >> 5] = lwmax;
       }
-      __syncthreads();
+      nan_u = __syncthreads_or(nan_u);
       umax = Red[0][0];
       umin = Red[1][0];
       lwmax = Red[2][0];
@@ -105,8 +107,8 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
         umin = fminf(umin, Red[1][w]);
         lwmax = fmaxf(lwmax, Red[2][w]);
       }
-      const float span = tau2 * (umax - umin);  // NaN / inf -> exact path
-      if (span <= 96.f && lwmax > -INFINITY) {
+      const float span = tau2 * (umax - umin);  // inf -> NaN span -> exact path
+      if (!nan_u && span <= 96.f && lwmax > -INFINITY) {
         __syncthreads();  // every thread has read Red
         // factors in place; zero tails so the 4-wide loads below read finite zeros
         for (int q = threadIdx.x; q < S_T + kc + 7; q += S_T)

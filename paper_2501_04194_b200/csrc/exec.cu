@@ -469,6 +469,8 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
         (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_TIMED) ||
         (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_UNTIMED && !cfg->masked_fill))
       e.aux_slot = plan->n_aux++;
+    // softmax smooth intervals: [L_hi | M_lo | L_lo] (double-float window LSE and mean)
+    if (cfg->mode == STLG_MODE_SOFTMAX && e.kind == E_FG_SMOOTH) plan->n_aux += 2;
     e.out_slot = (i == root) ? -1 : C.new_slot();
     C.slot_of[i] = e.out_slot;
     plan->entries.push_back(e);

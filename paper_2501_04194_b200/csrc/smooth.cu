@@ -222,8 +222,16 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
     if (MODE == M_LSE) {
       p.out[row * L + t] = sg * ((m + lg2f(s)) * p.mp.inv_tau2);  // log(sum w e^{tau u}) / tau
     } else {
-      p.out[row * L + t] = sg * (uc + (float)(D64 / S64));
-      p.aux[row * L + t] = (m + lg2f((float)S64)) * p.mp.inv_tau2;
+      // double-float window mean M and LSE L (max space) for the fp64 d/dw pass:
+      // aux = [L_hi | M_lo | L_lo] (three [B, L] planes)
+      const double M64 = (double)uc + D64 / S64;
+      const double L64 = ((double)m + log2(S64)) / (double)tau2;
+      const float Mh = (float)M64, Lh = (float)L64;
+      const long long BL = p.B * (long long)L;
+      p.out[row * L + t] = sg * Mh;
+      p.aux[row * L + t] = Lh;
+      p.aux[BL + row * L + t] = (float)(M64 - (double)Mh);
+      p.aux[2 * BL + row * L + t] = (float)(L64 - (double)Lh);
     }
   }
 }
@@ -471,6 +479,7 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
   __shared__ __align__(16) float Gt[S_T];
   __shared__ __align__(16) float Mt[S_T];
   __shared__ float Lt[S_T];
+  __shared__ double M64t[MODE == M_SOFT ? S_T : 1], L64t[MODE == M_SOFT ? S_T : 1];
   __shared__ float Rw[5][S_T / 32];
   __shared__ double red[S_CH];
   const int L = (int)p.L;
@@ -514,6 +523,11 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
         Gt[threadIdx.x] = g;
         Mt[threadIdx.x] = v ? sg * p.out_in[row * L + tt] : 0.f;
         Lt[threadIdx.x] = (MODE == M_SOFT && v) ? p.aux_in[row * L + tt] : 0.f;
+        if (MODE == M_SOFT) {  // double-float M and L written by the forward
+          const long long BL = p.B * (long long)L;
+          M64t[threadIdx.x] = v ? (double)Mt[threadIdx.x] + (double)p.aux_in[BL + row * L + tt] : 0.0;
+          L64t[threadIdx.x] = v ? (double)Lt[threadIdx.x] + (double)p.aux_in[2 * BL + row * L + tt] : 0.0;
+        }
         nz = (g != 0.f) | !v;
       }
       // dense cotangent row tile: no per-pair zero test, (G, M) read 4 at a time
@@ -622,12 +636,24 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
           acc[c] += (double)a + (double)a1;
           continue;
         }
+        if (MODE == M_SOFT) {
+          // softmax: sum_t g_t e^{tau (u - L_t)} (u - M_t) cancels terms of size
+          // tau |u - M| down to d(a, b, c): every term in fp64 with the double-float M, L
+          double a64 = 0.0;
+          for (int q = 0; q < nt; ++q) {
+            const float g = Gt[q];
+            if (g == 0.f) continue;
+            const double u = (double)U[q + k];
+            a64 += (double)g * exp2((double)tau2 * (u - L64t[q])) * (u - M64t[q]);
+          }
+          acc[c] += a64 * exp2((double)lw);  // w_i d out / d w_i convention (k_smooth_abc)
+          continue;
+        }
         for (int q = 0; q < nt; ++q) {
           float g = Gt[q];
           if (g == 0.f) continue;
           float u = U[q + k];
-          if (MODE == M_LSE) a = fmaf(g, ex2f(fmaf(tau2, u - Mt[q], lw)), a);
-          else a = fmaf(g * ex2f(fmaf(tau2, u - Lt[q], lw)), u - Mt[q], a);
+          a = fmaf(g, ex2f(fmaf(tau2, u - Mt[q], lw)), a);
         }
         acc[c] += (double)a;
       }

@@ -293,3 +293,48 @@ def test_smooth_interval_cotangent_density(cuda, mode, zero_frac, pad):
     # softmax d_b is ~1e2 out of summands up to ~3e4 (dw/db peaks at c L / 4 = 3375): its
     # d/dw terms run in fp64 against the forward's double-float M and L (csrc/smooth.cu)
     _check(type(mode).__name__, tr, g, ref_tr, ref_g, cot, dabc, np.array(ref_abc))
+
+
+def test_smooth_interval_graph_capture(cuda):
+    """smooth-interval forward + backward (weight table built on the device, no
+    host copies) capture into one CUDA graph and replay to the eager results."""
+    import ctypes
+    import torch
+    from paper_2501_04194_b200.engine import compile_formula
+    B, T = 64, 700
+    x = torch.tensor(np.asarray(P.synth_step_dataset(3, B, T), dtype=np.float32), device="cuda")
+    si = P.SmoothInterval(0.3, 0.65, 9.0)
+    comp = compile_formula(P.Always(P.Pred("x", ">", 0.0), si), ["x"], P.SemanticsConfig(mode=P.LogSumExp(5.0)))
+    params = comp.smooth_params()
+    fb, bb = comp.workspace_bytes(B, T)
+    fws = torch.empty(fb, dtype=torch.uint8, device="cuda")
+    bws = torch.empty(bb, dtype=torch.uint8, device="cuda")
+    ones = torch.ones(B, T, device="cuda")
+
+    def run(out, dx, dabc):
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        comp.forward([x], params, out, fws, st)
+        dabc.zero_()
+        comp.backward([x], params, out, ones, [dx], dabc, fws, bws, st)
+
+    eager = [torch.empty(B, T, device="cuda"), torch.empty(B, T, device="cuda"),
+             torch.zeros(3, dtype=torch.float64, device="cuda")]
+    run(*eager)
+    torch.cuda.synchronize()
+    cap = [torch.empty(B, T, device="cuda"), torch.empty(B, T, device="cuda"),
+           torch.zeros(3, dtype=torch.float64, device="cuda")]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run(*cap)  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    for t in cap:
+        t.zero_()
+    with torch.cuda.graph(g):
+        run(*cap)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, cap):
+        assert torch.equal(a, b)

@@ -469,6 +469,11 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
         (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_TIMED) ||
         (cfg->mode == STLG_MODE_LSE && e.kind == E_FG_UNTIMED && !cfg->masked_fill))
       e.aux_slot = plan->n_aux++;
+    // hard timed windows on the chunk-aligned kernels (17 <= K <= 1024): every window's first
+    // arg-max, so the backward routes cotangents without recomputing the windows
+    if (cfg->mode == STLG_MODE_HARD && e.kind == E_FG_TIMED && !cfg->masked_fill &&
+        e.b - e.a + 1 >= 17 && e.b - e.a + 1 <= 1024)
+      e.aux_slot = plan->n_aux++;
     // softmax smooth intervals: [L_hi | M_lo | L_lo] (double-float window LSE and mean)
     if (cfg->mode == STLG_MODE_SOFTMAX && e.kind == E_FG_SMOOTH) plan->n_aux += 2;
     e.out_slot = (i == root) ? -1 : C.new_slot();

@@ -175,7 +175,7 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   const float czero = p.canon ? 0.f : -0.f;
   float* outr = p.out + row * L;
-  float* auxr = ((RK == RK_LSE || RK == RK_SOFT) && p.aux != nullptr) ? p.aux + row * L : nullptr;
+  float* auxr = ((RK == RK_LSE || RK == RK_SOFT || RK == RK_HARDI) && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
   const int i0 = tid * RG_EPT;
@@ -213,9 +213,12 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
     RSt A0, A1;
     cav_middle<RK, NW>(d, tau2, T0, T1, A0, A1, T2);
     auto fin = [&](int, int i, RSt w, int sl) {
-      const float l2 = (RK == RK_HARD) ? 0.f : lg2f(w.s);
+      const float l2 = (RK == RK_HARD || RK == RK_HARDI) ? 0.f : lg2f(w.s);
       const bool live = full || t0 + i < nvalid;
-      if (RK == RK_SOFT) {  // value m + q / s; aux: the window LSE (max space) for the backward
+      if (RK == RK_HARDI) {  // value; aux: the first arg-max (global child index) for the backward
+        P0[sl] = __fadd_rn(live ? sg * w.m : padv, czero);
+        P1[sl] = live ? w.s : __int_as_float(-1);
+      } else if (RK == RK_SOFT) {  // value m + q / s; aux: the window LSE (max space) for the backward
         const float v = w.m + w.q / w.s;
         P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
         P1[sl] = live ? fmaf(l2, itau2, w.m) : 0.f;
@@ -235,7 +238,8 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
-    if (auxr != nullptr) {  // LSE: low word of the double-float trace; softmax: window LSE
+    if (auxr != nullptr) {  // LSE: low word of the double-float trace; softmax: window LSE;
+                            // hard: arg-max index
       const float* src1 = P1 + rpad(tid + K - 1);
       float* ap = auxr + t0 + tid;
 #pragma unroll
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   extern __shared__ float rsm[];
   __shared__ float T0[T], T1[RK == RK_HARD ? 1 : T], T2[rk3<RK>() ? T : 1];
   float* P0 = rsm;
-  float* P1 = rsm + C::NP;
+  float* P1 = rsm + C::NP;      // LSE / softmax / arg-max outputs
   float* P2 = rsm + 2 * C::NP;  // softmax only
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
@@ -271,13 +275,13 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   Ev<MODE, EK> ev(p.child, row, p.mp);
   const float padv = p.pad_last ? ev.value(L - 1, ev.load(L - 1)) : p.pad_value;
   float* outr = p.out + row * L;
-  float* auxr = ((RK == RK_LSE || RK == RK_SOFT) && p.aux != nullptr) ? p.aux + row * L : nullptr;
+  float* auxr = ((RK == RK_LSE || RK == RK_SOFT || RK == RK_HARDI) && p.aux != nullptr) ? p.aux + row * L : nullptr;
   const int tend = (t0 + J < L ? t0 + J : L) - t0;
   const int tid = threadIdx.x;
   if (t0 >= nvalid) {  // every output of the tile overruns
     for (int i = tid; i < tend; i += T) {
       outr[t0 + i] = __fadd_rn(padv, czero);
-      if (auxr) auxr[t0 + i] = 0.f;
+      if (auxr) auxr[t0 + i] = RK == RK_HARDI ? __int_as_float(-1) : 0.f;
     }
     return;
   }
@@ -313,7 +317,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   __syncthreads();
   RSt x[RG_EPT];
 #pragma unroll
-  for (int k = 0; k < RG_EPT; ++k) x[k] = RSt{P0[tid * (RG_EPT + 1) + k], 1.f};
+  for (int k = 0; k < RG_EPT; ++k)  // RK_HARDI: the global child index rides in s
+    x[k] = RSt{P0[tid * (RG_EPT + 1) + k], RK == RK_HARDI ? __int_as_float(s0 + tid * RG_EPT + k) : 1.f};
   cav_fwd_core<RK, NW>(p, row, t0, J, padv, x, P0, P1, T0, T1, P2, T2);
 }
 
@@ -616,7 +621,7 @@ __device__ __forceinline__ RunSeg run_shfl_up(RunSeg v, int o) {
                 __shfl_up_sync(0xffffffffu, v.whole, o)};
 }
 
-template <int EK, int NW>
+template <int EK, int NW, bool IDX>
 __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
@@ -643,6 +648,37 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
+  // IDX: the forward stored every window's first arg-max (global child index, aux): the
+  // keys come from it directly — no child loads, no scans (12 B per sample: g, index, d c)
+  int key[RG_EPT];
+  RSt x[RG_EPT];
+  float g[RG_EPT];
+  if constexpr (IDX) {
+    const int so = tid + (tid >> 4);
+    const int tb = first + tid - p.a;
+    const float* ix = p.aux_in + row * L;
+    const int thi = nvalid > 0 ? nvalid - 1 : 0;
+#pragma unroll
+    for (int h = 0; h < RG_EPT; h += CAV_LB) {
+      float gv[CAV_LB], iv[CAV_LB];
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int t = tb + (h + k) * T;
+        const int tc = t < 0 ? 0 : (t > thi ? thi : t);
+        gv[k] = ld_na(cot + tc);
+        iv[k] = ld_na(ix + tc);
+      }
+#pragma unroll
+      for (int k = 0; k < CAV_LB; ++k) {
+        const int t = tb + (h + k) * T;
+        const bool wv = tid + (h + k) * T < nwin && t >= 0 && t < nvalid;
+        // keys stay non-decreasing: 0 below the row start, NOKEY past the live windows
+        const int kk = wv ? __float_as_int(iv[k]) - first : (t < 0 ? 0 : NOKEY);
+        P0[so + (h + k) * SS] = __int_as_float(kk);
+        P1[so + (h + k) * SS] = wv ? gv[k] : 0.f;
+      }
+    }
+  } else {
   // phase 1: child values u (window start i <-> t = first + i - a)
   {
     const int so = tid + (tid >> 4);
@@ -686,6 +722,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
       }
     }
   }
+  }
   if (tid < 32) {  // overrun outputs route to c[L-1] ('last' padding)
     float ps = 0.f;
     if (p.pad_last && L - 1 >= j0 && L - 1 < j0 + Jo) {
@@ -699,23 +736,25 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
   __syncthreads();
   const float padsum = padsum_sh;
   const int kpad = (padsum != 0.f) ? L - 1 - first : -1;  // local index receiving the pad sum
-  RSt x[RG_EPT];
-  float g[RG_EPT];
   {
     const int q0 = tid * (RG_EPT + 1);
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) {
-      x[k] = RSt{P0[q0 + k], __int_as_float(tid * RG_EPT + k), 0.f};
+      if (IDX) key[k] = __float_as_int(P0[q0 + k]);
+      else x[k] = RSt{P0[q0 + k], __int_as_float(tid * RG_EPT + k), 0.f};
       g[k] = P1[q0 + k];
-      G[q0 + k] = (tid * RG_EPT + k == kpad) ? padsum : 0.f;
     }
   }
-  cav_scans<RK_HARDI>(x, 0.f, P0, P1, T0, T1);
-  __syncthreads();
-  RSt A0, A1;
-  cav_middle<RK_HARDI, NW>(d, 0.f, T0, T1, A0, A1);
-  int key[RG_EPT];
   {
+    const int q0 = tid * (RG_EPT + 1);
+#pragma unroll
+    for (int k = 0; k < RG_EPT; ++k) G[q0 + k] = (tid * RG_EPT + k == kpad) ? padsum : 0.f;
+  }
+  if constexpr (!IDX) {
+    cav_scans<RK_HARDI>(x, 0.f, P0, P1, T0, T1);
+    __syncthreads();
+    RSt A0, A1;
+    cav_middle<RK_HARDI, NW>(d, 0.f, T0, T1, A0, A1);
     auto fin = [&](int k, int, RSt w, int) { key[k] = __float_as_int(w.s); };
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) key[k] = NOKEY;
@@ -774,9 +813,11 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
 #pragma unroll
     for (int h = 0; h < RG_EPT; h += CAV_LB) {
       typename Ev<M_HARD, EK>::Raw r[CAV_LB];
+      // (affine / trace children need no value for their VJP: no reload)
+      constexpr bool need_raw = !(EK == EK_AFF || EK == EK_AFF1 || EK == EK_SRC);
 #pragma unroll
       for (int u = 0; u < CAV_LB; ++u)
-        if (tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
+        if (need_raw && tid + (h + u) * T < jn) r[u] = ev.load(jb + (h + u) * T);
 #pragma unroll
       for (int u = 0; u < CAV_LB; ++u)
         if (tid + (h + u) * T < jn) ev.template grad_t<ST>(jb + (h + u) * T, r[u], G[gb + (h + u) * SS]);

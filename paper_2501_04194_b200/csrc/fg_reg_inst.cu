@@ -23,7 +23,9 @@ cudaError_t fwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
   cudaError_t e;
   if (mode == M_HARD) {
     const size_t smem = (size_t)C::NP * 4;
-    if (cav) {
+    if (cav && p.aux != nullptr) {  // keep every window's first arg-max for the backward
+      REG_DISPATCH_EK(ek, e = reg_launch(k_cav_fwd<RK_HARDI, M_HARD, EK, NW>, grid, C::T, 2 * smem, p, st))
+    } else if (cav) {
       REG_DISPATCH_EK(ek, e = reg_launch(k_cav_fwd<RK_HARD, M_HARD, EK, NW>, grid, C::T, smem, p, st))
     } else {
       REG_DISPATCH_EK(ek, e = reg_launch(k_reg_fwd<RK_HARD, M_HARD, EK, NW>, grid, C::T, smem, p, st))
@@ -54,7 +56,11 @@ cudaError_t bwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
     const size_t smem = (size_t)3 * C::NP * 4;
     if (cav) {
-      REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW>, grid, C::T, smem, p, st))
+      if (p.aux_in != nullptr) {  // the forward's arg-max: no recomputation
+        REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW, true>, grid, C::T, smem, p, st))
+      } else {
+        REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW, false>, grid, C::T, smem, p, st))
+      }
     } else {
       REG_DISPATCH_EK(ek, e = reg_launch(k_reg_bwd_hard<EK, NW>, grid, C::T, smem, p, st))
     }

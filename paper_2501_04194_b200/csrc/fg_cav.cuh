@@ -750,6 +750,9 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) G[q0 + k] = (tid * RG_EPT + k == kpad) ? padsum : 0.f;
   }
+  // run totals land in other threads' G slots: every slot zeroed first (the scans' barrier
+  // does this on the recomputing path)
+  if constexpr (IDX) __syncthreads();
   if constexpr (!IDX) {
     cav_scans<RK_HARDI>(x, 0.f, P0, P1, T0, T1);
     __syncthreads();

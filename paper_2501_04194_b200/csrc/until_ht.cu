@@ -30,7 +30,7 @@
 
 namespace stlg {
 
-constexpr int HT_T = 128;    // threads per CTA
+constexpr int HT_T = 256;    // threads per CTA
 constexpr int HT_NT = 1024;  // outputs (forward) / owned elements (backward) per CTA
 constexpr int HT_R = 1 << 30;  // source flag: right child
 
@@ -41,7 +41,7 @@ constexpr int HT_R = 1 << 30;  // source flag: right child
 //   m = min(m_A, m_B) (a tie keeps A), y = max(y_A, min(m_A, y_B)) with the source
 //   yi_A if y_A >= min(m_A, y_B), else yi_B if y_B < m_A, else l[mi_A]
 // — the reference's tie rules, so the state of a range is unique and the combine is
-// associative (warp scans may use any bracketing).
+// associative.
 struct HS {
   float m, y;
   int mi, yi;
@@ -63,86 +63,113 @@ __device__ __forceinline__ HS hs_comb(const HS& A, const HS& B) {
   o.yi = ya ? A.yi : ci;
   return o;
 }
-__device__ __forceinline__ HS hs_shfl_up(const HS& v, int o) {
-  return HS{__shfl_up_sync(0xffffffffu, v.m, o), __shfl_up_sync(0xffffffffu, v.y, o),
-            __shfl_up_sync(0xffffffffu, v.mi, o), __shfl_up_sync(0xffffffffu, v.yi, o)};
+// staged arrays, padded one word per 32-block (ht_pad) so that a lane walking its own
+// block and a warp reading consecutive positions are both free of bank conflicts:
+//   lr[i]  = (l_i, r_i)
+//   suf[i] = state over [i, end of i's 32-block],  pre[i] = state over [start of the block, i]
+// (states packed as float4 {m, y, mi, yi}: one 128-bit shared load each)
+__device__ __forceinline__ int ht_pad(int i) { return i + (i >> 5); }
+__device__ __forceinline__ float4 hs_pack(const HS& s) {
+  return make_float4(s.m, s.y, __int_as_float(s.mi), __int_as_float(s.yi));
 }
-__device__ __forceinline__ HS hs_shfl_down(const HS& v, int o) {
-  return HS{__shfl_down_sync(0xffffffffu, v.m, o), __shfl_down_sync(0xffffffffu, v.y, o),
-            __shfl_down_sync(0xffffffffu, v.mi, o), __shfl_down_sync(0xffffffffu, v.yi, o)};
+__device__ __forceinline__ HS hs_unpack(const float4 v) {
+  return HS{v.x, v.y, __float_as_int(v.z), __float_as_int(v.w)};
 }
-
-// staged arrays: children, and per position the suffix state over [i, end of its
-// 32-block] and the prefix state over [start of its block, i] (struct-of-arrays)
 struct HTArr {
-  float *l, *r;
-  float *sm, *sy, *pm, *py;
-  int *smi, *syi, *pmi, *pyi;
-  __device__ __forceinline__ HS suf(int i) const { return HS{sm[i], sy[i], smi[i], syi[i]}; }
-  __device__ __forceinline__ HS pre(int i) const { return HS{pm[i], py[i], pmi[i], pyi[i]}; }
+  float2* lr;
+  float4 *sf, *pf;
+  __device__ __forceinline__ HS suf(int i) const { return hs_unpack(sf[ht_pad(i)]); }
+  __device__ __forceinline__ HS pre(int i) const { return hs_unpack(pf[ht_pad(i)]); }
+  __device__ __forceinline__ float2 at(int i) const { return lr[ht_pad(i)]; }
 };
 
+__host__ __device__ __forceinline__ int ht_padded(int NS) { return ((NS + 31) >> 5) * 33; }
+
 __device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
+  const int NP = ht_padded(NS);
   HTArr A;
-  float* f = base;
-  A.l = f;
-  A.r = f + NS;
-  A.sm = f + 2 * NS;
-  A.sy = f + 3 * NS;
-  A.pm = f + 4 * NS;
-  A.py = f + 5 * NS;
-  int* q = reinterpret_cast<int*>(f + 6 * NS);
-  A.smi = q;
-  A.syi = q + NS;
-  A.pmi = q + 2 * NS;
-  A.pyi = q + 3 * NS;
+  A.sf = reinterpret_cast<float4*>(base);
+  A.pf = A.sf + NP;
+  A.lr = reinterpret_cast<float2*>(A.pf + NP);
   return A;
 }
 
-size_t ht_smem_bytes(int NS) { return (size_t)NS * 4 * 10; }
+size_t ht_smem_bytes(int NS) { return (size_t)ht_padded(NS) * 40; }
 
-// stage the children over [base, base + NS) and scan every 32-block (one warp per block,
-// prefix and suffix states by shuffles)
+// stage the children over [base, base + NS) (coalesced), then walk every 32-block
+// serially: one lane per block for the prefix states and one for the suffix states
 __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, const HTArr& A) {
   const int L = (int)p.L;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nb = (NS + 31) >> 5;
   const ChildEval cl(p.left, row), cr(p.right, row);
-  for (int bk = warp; bk < nb; bk += HT_T / 32) {
-    const int i = bk * 32 + lane, pos = base + i;
-    const bool live = i < NS && pos >= 0 && pos < L;
-    float l = 0.f, r = 0.f;
-    if (cl.kind != 0 && cr.kind != 0) {  // loads issued before the transforms
-      const int pc = live ? pos : 0;
-      const float xl = cl.raw(pc), xr = cr.raw(pc);
-      if (live) {
-        l = cl.apply(xl);
-        r = cr.apply(xr);
-      }
-    } else if (live) {
-      l = cl.value<M_HARD>(pos, p.mp);
-      r = cr.value<M_HARD>(pos, p.mp);
-    }
-    const HS e = hs_elem(l, r, pos);
-    HS pre = e, suf = e;
+  constexpr int LB = 4;  // global loads in flight per thread before the transforms
+  for (int i0 = threadIdx.x; i0 < nb * 32; i0 += LB * HT_T) {
+    float xl[LB], xr[LB];
+    if (cl.kind != 0 && cr.kind != 0) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const HS a = hs_shfl_up(pre, o);
-      const HS b = hs_shfl_down(suf, o);
-      if (lane >= o) pre = hs_comb(a, pre);
-      if (lane + o < 32) suf = hs_comb(suf, b);
+      for (int k = 0; k < LB; ++k) {
+        const int pos = base + i0 + k * HT_T;
+        const int pc = pos >= 0 && pos < L ? pos : 0;
+        xl[k] = cl.raw(pc);
+        xr[k] = cr.raw(pc);
+      }
     }
-    if (i < NS) {
-      A.l[i] = l;
-      A.r[i] = r;
-      A.pm[i] = pre.m;
-      A.py[i] = pre.y;
-      A.pmi[i] = pre.mi;
-      A.pyi[i] = pre.yi;
-      A.sm[i] = suf.m;
-      A.sy[i] = suf.y;
-      A.smi[i] = suf.mi;
-      A.syi[i] = suf.yi;
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const int i = i0 + k * HT_T, pos = base + i;
+      if (i >= nb * 32) break;
+      const bool live = i < NS && pos >= 0 && pos < L;
+      float l = 0.f, r = 0.f;
+      if (live) {
+        if (cl.kind != 0 && cr.kind != 0) {
+          l = cl.apply(xl[k]);
+          r = cr.apply(xr[k]);
+        } else {
+          l = cl.value<M_HARD>(pos, p.mp);
+          r = cr.value<M_HARD>(pos, p.mp);
+        }
+      }
+      A.lr[ht_pad(i)] = make_float2(l, r);
+    }
+  }
+  __syncthreads();
+  const int nbw = (nb + 31) & ~31;  // suffix walkers start on a warp boundary (no divergence)
+  for (int w = threadIdx.x; w < nbw + nb; w += HT_T) {
+    const bool fwd = w < nbw;
+    if (fwd && w >= nb) continue;
+    const int bk = fwd ? w : w - nbw;
+    const float2* src = A.lr + bk * 33;
+    const int s0 = base + bk * 32;
+    if (fwd) {
+      float4* dst = A.pf + bk * 33;
+      HS s;
+#pragma unroll
+      for (int h = 0; h < 32; h += 8) {
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = src[h + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const HS e = hs_elem(v[k].x, v[k].y, s0 + h + k);
+          s = (h + k == 0) ? e : hs_comb(s, e);
+          dst[h + k] = hs_pack(s);
+        }
+      }
+    } else {
+      float4* dst = A.sf + bk * 33;
+      HS s;
+#pragma unroll
+      for (int h = 24; h >= 0; h -= 8) {
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = src[h + k];
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+          const HS e = hs_elem(v[k].x, v[k].y, s0 + h + k);
+          s = (h + k == 31) ? e : hs_comb(e, s);
+          dst[h + k] = hs_pack(s);
+        }
+      }
     }
   }
   __syncthreads();
@@ -152,8 +179,12 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
 __device__ __forceinline__ HS ht_range(const HTArr& A, int i0, int i1, int base) {
   const int b0 = i0 >> 5, b1 = i1 >> 5;
   if (b0 == b1) {  // inside one block: element by element (at most 32 steps)
-    HS s = hs_elem(A.l[i0], A.r[i0], base + i0);
-    for (int i = i0 + 1; i <= i1; ++i) s = hs_comb(s, hs_elem(A.l[i], A.r[i], base + i));
+    float2 v = A.at(i0);
+    HS s = hs_elem(v.x, v.y, base + i0);
+    for (int i = i0 + 1; i <= i1; ++i) {
+      v = A.at(i);
+      s = hs_comb(s, hs_elem(v.x, v.y, base + i));
+    }
     return s;
   }
   HS s = A.suf(i0);
@@ -165,22 +196,25 @@ __device__ __forceinline__ HS ht_range(const HTArr& A, int i0, int i1, int base)
 __device__ __forceinline__ void ht_minrange(const HTArr& A, int i0, int i1, int base, float& mv, int& mi) {
   const int b0 = i0 >> 5, b1 = i1 >> 5;
   if (b0 == b1) {
-    mv = A.l[i0];
+    mv = A.at(i0).x;
     mi = base + i0;
-    for (int i = i0 + 1; i <= i1; ++i)
-      if (A.l[i] < mv) {
-        mv = A.l[i];
+    for (int i = i0 + 1; i <= i1; ++i) {
+      const float l = A.at(i).x;
+      if (l < mv) {
+        mv = l;
         mi = base + i;
       }
+    }
     return;
   }
-  mv = A.sm[i0];
-  mi = A.smi[i0];
+  const HS s = A.suf(i0);
+  mv = s.m;
+  mi = s.mi;
   for (int bk = b0 + 1; bk <= b1; ++bk) {
-    const int e = bk < b1 ? bk * 32 + 31 : i1;
-    if (A.pm[e] < mv) {
-      mv = A.pm[e];
-      mi = A.pmi[e];
+    const HS e = A.pre(bk < b1 ? bk * 32 + 31 : i1);
+    if (e.m < mv) {
+      mv = e.m;
+      mi = e.mi;
     }
   }
 }
@@ -198,8 +232,8 @@ __device__ __forceinline__ int ht_source(const UParams& p, int base, int t, cons
   return V.yi;
 }
 
-__global__ void __launch_bounds__(HT_T) k_until_ht_fwd(const __grid_constant__ UParams p) {
-  extern __shared__ float htsm[];
+__global__ void __launch_bounds__(HT_T, 4) k_until_ht_fwd(const __grid_constant__ UParams p) {
+  extern __shared__ __align__(16) float htsm[];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
   const int t0 = blockIdx.x * HT_NT;
@@ -212,7 +246,8 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_fwd(const __grid_constant__ U
     float o;
     if (t + p.b <= L - 1) {
       const int d = ht_source(p, t0, t, A);
-      o = (d & HT_R) ? A.r[(d & (HT_R - 1)) - t0] : A.l[d - t0];
+      const float2 v = A.at((d & (HT_R - 1)) - t0);
+      o = (d & HT_R) ? v.y : v.x;
     } else {  // overrun: hard min of the pad values, a tie keeps the left (reference.py:189)
       float pl = p.pad_value, pr = p.pad_value;
       if (p.pad_last) {
@@ -225,8 +260,8 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_fwd(const __grid_constant__ U
   }
 }
 
-__global__ void __launch_bounds__(HT_T) k_until_ht_bwd(const __grid_constant__ UParams p) {
-  extern __shared__ float htsm[];
+__global__ void __launch_bounds__(HT_T, 3) k_until_ht_bwd(const __grid_constant__ UParams p) {
+  extern __shared__ __align__(16) float htsm[];
   __shared__ unsigned long long accL[HT_NT], accR[HT_NT];
   __shared__ float gred[HT_T / 32];
   const long long row = blockIdx.y;

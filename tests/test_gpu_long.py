@@ -229,7 +229,8 @@ def test_c5_untimed_until_T30k_hard(cuda):
 
 @pytest.mark.parametrize("pad", ["last", "const"])
 @pytest.mark.parametrize("a,K,L", [(0, 1, 50), (0, 2, 300), (1, 5, 300), (3, 64, 1500), (0, 101, 1500),
-                                   (17, 101, 2500), (2, 300, 5000), (40, 7, 900), (0, 1100, 2600)])
+                                   (17, 101, 2500), (2, 300, 5000), (40, 7, 900), (0, 1100, 2600),
+                                   (0, 65, 1400), (65, 65, 2100), (70, 129, 3000), (64, 200, 1900)])
 def test_hard_timed_until_sweep(cuda, a, K, L, pad):
     """O(T) hard timed Until (csrc/until_ht.cu) vs the oracle: tie-heavy inputs (integers
     and signed zeros), left- and right-sourced outputs, overrun tails, both paddings,

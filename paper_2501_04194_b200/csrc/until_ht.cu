@@ -31,7 +31,10 @@
 namespace stlg {
 
 constexpr int HT_T = 256;    // threads per CTA
-constexpr int HT_NT = 1024;  // outputs (forward) / owned elements (backward) per CTA
+// staged span NS = a multiple of 1024 positions (32 blocks: the walks fill whole warps),
+// the smallest leaving at least 512 outputs (forward) / owned elements (backward) per CTA
+// after the window halo (b forward, 2b backward): NT = NS - halo
+__host__ __device__ __forceinline__ int ht_ns(int halo) { return (halo + 512 + 1023) / 1024 * 1024; }
 constexpr int HT_R = 1 << 30;  // source flag: right child
 
 // Range state of the reference's Until over a range R = [s0, s1] of candidate ends s:
@@ -232,16 +235,16 @@ __device__ __forceinline__ int ht_source(const UParams& p, int base, int t, cons
   return V.yi;
 }
 
-__global__ void __launch_bounds__(HT_T, 4) k_until_ht_fwd(const __grid_constant__ UParams p) {
+__global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant__ UParams p) {
   extern __shared__ __align__(16) float htsm[];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
-  const int t0 = blockIdx.x * HT_NT;
-  const int NS = HT_NT + p.b;
+  const int NS = ht_ns(p.b), NT = NS - p.b;
+  const int t0 = blockIdx.x * NT;
   const HTArr A = ht_carve(htsm, NS);
   ht_prepare(p, row, t0, NS, A);
   float* outr = p.out + row * L;
-  const int tend = min(t0 + HT_NT, L);
+  const int tend = min(t0 + NT, L);
   for (int t = t0 + (int)threadIdx.x; t < tend; t += HT_T) {
     float o;
     if (t + p.b <= L - 1) {
@@ -260,19 +263,20 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_fwd(const __grid_constant_
   }
 }
 
-__global__ void __launch_bounds__(HT_T, 3) k_until_ht_bwd(const __grid_constant__ UParams p) {
+__global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant__ UParams p) {
   extern __shared__ __align__(16) float htsm[];
-  __shared__ unsigned long long accL[HT_NT], accR[HT_NT];
   __shared__ float gred[HT_T / 32];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
-  const int t0 = blockIdx.x * HT_NT;
+  const int NS = ht_ns(2 * p.b), NT = NS - 2 * p.b;
+  const int t0 = blockIdx.x * NT;
   const int base = t0 - p.b;
-  const int NS = HT_NT + 2 * p.b;
   const HTArr A = ht_carve(htsm, NS);
-  for (int i = threadIdx.x; i < HT_NT; i += HT_T) accL[i] = accR[i] = 0ull;
+  unsigned long long* accL = reinterpret_cast<unsigned long long*>(htsm + ht_padded(NS) * 10);
+  unsigned long long* accR = accL + NT;
+  for (int i = threadIdx.x; i < NT; i += HT_T) accL[i] = accR[i] = 0ull;
   const float* cot = p.cot + row * L;
-  const int tlo = max(base, 0), thi = min(t0 + HT_NT, L);  // outputs that can reach the range
+  const int tlo = max(base, 0), thi = min(t0 + NT, L);  // outputs that can reach the range
   // per-tile fixed-point scale: sum |g| over the tile's outputs < 2^62 / scale
   float gm = 0.f;  // (a NaN / inf cotangent makes gm inf: the ordered fallback below)
   for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(HT_T, 3) k_until_ht_bwd(const __grid_constant_
       const int d = (t + p.b <= L - 1) ? ht_source(p, base, t, A) : padsrc;
       if (d < 0) continue;
       const int j = (d & (HT_R - 1)) - t0;
-      if (j < 0 || j >= HT_NT) continue;
+      if (j < 0 || j >= NT) continue;
       const long long q = llrint((double)g * scale);
       atomicAdd((d & HT_R) ? &accR[j] : &accL[j], (unsigned long long)q);
     }
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(HT_T, 3) k_until_ht_bwd(const __grid_constant_
   float* gl = p.gl + row * L;
   float* gr = p.gr + row * L;
   const bool nonfinite = !(gm < INFINITY);  // inf / NaN cotangents: plain (ordered) sums
-  for (int j = t0 + (int)threadIdx.x; j < min(t0 + HT_NT, L); j += HT_T) {
+  for (int j = t0 + (int)threadIdx.x; j < min(t0 + NT, L); j += HT_T) {
     if (!nonfinite) {
       gl[j] = (float)((double)(long long)accL[j - t0] * inv);
       gr[j] = (float)((double)(long long)accR[j - t0] * inv);
@@ -332,14 +336,16 @@ __global__ void __launch_bounds__(HT_T, 3) k_until_ht_bwd(const __grid_constant_
 // true when the O(T) kernels apply (hard, timed, no masked_fill, staging fits)
 bool until_ht_applicable(const UParams& p) {
   if (p.untimed || p.fill || p.K < 1 || p.L >= (1LL << 29)) return false;
-  return ht_smem_bytes(HT_NT + 2 * p.b) <= 200 * 1024;
+  const int NS = ht_ns(2 * p.b);
+  return ht_smem_bytes(NS) + (size_t)(NS - 2 * p.b) * 16 <= 200 * 1024;
 }
 
 cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
-  const size_t smem = ht_smem_bytes(HT_NT + p.b);
+  const int NS = ht_ns(p.b), NT = NS - p.b;
+  const size_t smem = ht_smem_bytes(NS);
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((p.L + HT_NT - 1) / HT_NT), (unsigned)p.B);
+  dim3 grid((unsigned)((p.L + NT - 1) / NT), (unsigned)p.B);
   k_until_ht_fwd<<<grid, HT_T, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
@@ -347,10 +353,11 @@ cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
 
 // writes every element of p.gl / p.gr (the caller runs the child VJPs)
 cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st) {
-  const size_t smem = ht_smem_bytes(HT_NT + 2 * p.b);
+  const int NS = ht_ns(2 * p.b), NT = NS - 2 * p.b;
+  const size_t smem = ht_smem_bytes(NS) + (size_t)NT * 16;
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((p.L + HT_NT - 1) / HT_NT), (unsigned)p.B);
+  dim3 grid((unsigned)((p.L + NT - 1) / NT), (unsigned)p.B);
   k_until_ht_bwd<<<grid, HT_T, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();

@@ -100,21 +100,38 @@ __device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
 size_t ht_smem_bytes(int NS) { return (size_t)ht_padded(NS) * 40; }
 
 // stage the children over [base, base + NS) (coalesced), then walk every 32-block
-// serially: one lane per block for the prefix states and one for the suffix states
-__device__ void ht_prepare(const UParams& p, long long row, int base, int NS, const HTArr& A) {
+// serially: one lane per block for the prefix states and one for the suffix states.
+// Backward with NS <= 4 HT_T: the cotangents of the outputs at positions
+// i = threadIdx.x + k HT_T < NO ride in the same load batches into gk[k] (0 outside the
+// signal) and the per-warp max |g| lands in gred (a NaN / inf makes it inf).
+__device__ void ht_prepare(const UParams& p, long long row, int base, int NS, const HTArr& A,
+                           const float* cot = nullptr, int NO = 0, float* gk = nullptr, float* gred = nullptr) {
   const int L = (int)p.L;
   const int nb = (NS + 31) >> 5;
   const ChildEval cl(p.left, row), cr(p.right, row);
   constexpr int LB = 4;  // global loads in flight per thread before the transforms
+  float gm = 0.f;
   for (int i0 = threadIdx.x; i0 < nb * 32; i0 += LB * HT_T) {
-    float xl[LB], xr[LB];
-    if (cl.kind != 0 && cr.kind != 0) {
+    float xl[LB], xr[LB], xg[LB];
 #pragma unroll
-      for (int k = 0; k < LB; ++k) {
-        const int pos = base + i0 + k * HT_T;
-        const int pc = pos >= 0 && pos < L ? pos : 0;
+    for (int k = 0; k < LB; ++k) {
+      const int pos = base + i0 + k * HT_T;
+      const int pc = pos >= 0 && pos < L ? pos : 0;
+      if (cl.kind != 0 && cr.kind != 0) {
         xl[k] = cl.raw(pc);
         xr[k] = cr.raw(pc);
+      }
+      if (cot) xg[k] = cot[pc];
+    }
+    if (cot) {
+#pragma unroll
+      for (int k = 0; k < LB; ++k) {
+        const int i = i0 + k * HT_T, pos = base + i;
+        if (i >= NO) break;
+        const float g = pos >= 0 && pos < L ? xg[k] : 0.f;
+        const float ag = fabsf(g);
+        gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
+        gk[k] = g;
       }
     }
 #pragma unroll
@@ -134,6 +151,10 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
       }
       A.lr[ht_pad(i)] = make_float2(l, r);
     }
+  }
+  if (cot) {
+    for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if ((threadIdx.x & 31) == 0) gred[threadIdx.x >> 5] = gm;
   }
   __syncthreads();
   const int nbw = (nb + 31) & ~31;  // suffix walkers start on a warp boundary (no divergence)
@@ -278,15 +299,22 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
   const float* cot = p.cot + row * L;
   const int tlo = max(base, 0), thi = min(t0 + NT, L);  // outputs that can reach the range
   // per-tile fixed-point scale: sum |g| over the tile's outputs < 2^62 / scale
-  float gm = 0.f;  // (a NaN / inf cotangent makes gm inf: the ordered fallback below)
-  for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
-    const float ag = fabsf(cot[t]);
-    gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
+  // (a NaN / inf cotangent makes gm inf: the ordered fallback below)
+  const bool regs = NS <= 4 * HT_T;  // cotangents staged with the children, in registers
+  float gk[4] = {0.f, 0.f, 0.f, 0.f};
+  if (regs) {
+    ht_prepare(p, row, base, NS, A, cot, NT + p.b, gk, gred);  // (its barriers publish gred / acc)
+  } else {
+    float gm = 0.f;
+    for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
+      const float ag = fabsf(cot[t]);
+      gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
+    }
+    for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if ((threadIdx.x & 31) == 0) gred[threadIdx.x >> 5] = gm;
+    ht_prepare(p, row, base, NS, A);
   }
-  for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-  if ((threadIdx.x & 31) == 0) gred[threadIdx.x >> 5] = gm;
-  ht_prepare(p, row, base, NS, A);  // (contains the barriers that publish gred / acc)
-  gm = gred[0];
+  float gm = gred[0];
   for (int w = 1; w < HT_T / 32; ++w) gm = fmaxf(gm, gred[w]);
   int ge = 0;
   frexp((double)gm * (double)(thi - tlo + 1), &ge);  // sum |g| < 2^ge
@@ -298,15 +326,23 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
     padsrc = (pl <= pr) ? (L - 1) : ((L - 1) | HT_R);
   }
   if (gm > 0.f && gm < INFINITY) {
-    for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
-      const float g = cot[t];
-      if (g == 0.f) continue;
+    auto route = [&](int t, float g) {
+      if (g == 0.f) return;
       const int d = (t + p.b <= L - 1) ? ht_source(p, base, t, A) : padsrc;
-      if (d < 0) continue;
+      if (d < 0) return;
       const int j = (d & (HT_R - 1)) - t0;
-      if (j < 0 || j >= NT) continue;
+      if (j < 0 || j >= NT) return;
       const long long q = llrint((double)g * scale);
       atomicAdd((d & HT_R) ? &accR[j] : &accL[j], (unsigned long long)q);
+    };
+    if (regs) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = base + (int)threadIdx.x + k * HT_T;
+        if (t >= tlo && t < thi) route(t, gk[k]);
+      }
+    } else {
+      for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) route(t, cot[t]);
     }
   }
   __syncthreads();

@@ -277,6 +277,7 @@ struct Bufs {
   unsigned long long* dacc;  // [4][B, T] reproducible Until accumulators
   int* dscale;               // [B] their per-row grid exponents
   float* uslab;   // Until backward checkpoint slab (persistent kernel)
+  unsigned* lb;   // look-back slots of the multi-CTA untimed scans (forward: 1, backward: 2 rows)
   long long BT;
   float* slot(int s) const { return slots + (long long)s * BT; }
   float* gslot(int s) const { return gslots + (long long)s * BT; }
@@ -551,11 +552,11 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   long long BT = (long long)B * T;
   size_t sb, ab;
   fwd_layout(plan, BT, &sb, &ab);
-  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + 256;
+  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + align256(lb_slot_bytes(B, T)) + 256;
   if (bwd_bytes)
     *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
                  align256(sizeof(float) * 3 * (size_t)BT) + dw_bytes(plan, B, T) +
-                 det_bytes(plan, B, T) + until_slab_bytes(plan, T) + 1024;
+                 det_bytes(plan, B, T) + until_slab_bytes(plan, T) + align256(2 * lb_slot_bytes(B, T)) + 1024;
   return STLG_OK;
 }
 
@@ -572,6 +573,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.slots = (float*)base;
   bf.aux = (float*)(base + sb);
   bf.tables = (float*)(base + sb + ab);
+  bf.lb = (unsigned*)(base + sb + ab + tables_bytes(plan, T));
   bf.gslots = nullptr;
   bf.scratch = nullptr;
   bf.uslab = nullptr;
@@ -591,6 +593,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
       bf.dscale = (int*)(dp + align256(sizeof(unsigned long long) * 4 * (size_t)BT));
     }
     bf.uslab = (float*)(dp + det_bytes(plan, B, T) + 256);
+    bf.lb = (unsigned*)((uintptr_t)bf.uslab + until_slab_bytes(plan, T));
   }
   return STLG_OK;
 }
@@ -711,6 +714,7 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       if ((rc = resolve(plan, e.e1, channels, nullptr, bf, T, false, p.child))) return rc;
       p.out = out;
       p.aux = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
+      p.lb = bf.lb;
       if (e.kind == E_POINTWISE) ce = launch_pointwise_fwd(mode, p, st);
       else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_fwd(mode, p, st);
       else ce = launch_fg_untimed_fwd(mode, p, st);
@@ -720,6 +724,7 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       if ((rc = resolve(plan, e.e1, channels, nullptr, bf, T, false, p.left))) return rc;
       if ((rc = resolve(plan, e.e2, channels, nullptr, bf, T, false, p.right))) return rc;
       p.out = out;
+      p.lb = bf.lb;
       p.B = B;
       p.L = T;
       p.a = e.untimed ? 0 : e.a;
@@ -777,6 +782,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.aux_in = e.aux_slot >= 0 ? bf.auxp(e.aux_slot) : nullptr;
       p.cot = g;
       p.gbuf = bf.scratch;
+      p.lb = bf.lb;
       if (e.kind == E_POINTWISE) ce = launch_pointwise_vjp(mode, p, g, st);
       else if (e.kind == E_FG_TIMED) ce = launch_fg_timed_bwd(mode, p, st);
       else ce = launch_fg_untimed_bwd(mode, p, st);
@@ -802,6 +808,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.scratch = bf.uslab;
       p.dacc = bf.dacc;
       p.dscale = bf.dscale;
+      p.lb = bf.lb;
       p.mp = mode_params(plan->cfg);
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH

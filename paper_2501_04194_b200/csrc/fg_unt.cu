@@ -2,36 +2,55 @@
 // tape.py:475-535: out[t] = R_{j = t .. L-1} s[j], a reverse scan per row, no padding,
 // no `+ 0.0` canonicalisation).
 //
-// One CTA per row walks the row from its end in tiles of 16 T samples: coalesced
-// loads through the typed child evaluator, a transpose through shared memory, each
-// thread scans its 16-sample chunk in registers, a warp-shuffle suffix scan and one
-// cross-warp step give every thread the fold of the samples after its chunk (plus
-// the carry of the tiles already done), and the outputs leave through shared memory
-// with coalesced stores.  Three barriers per 4096 samples; two alternating buffers
-// let the next tile's loads overlap the previous tile's stores.
+// Per tile (one CTA walking a row's 4096-sample tiles, or one CTA per 1024-sample tile
+// for small batches — UN_SEQ / UN_LB below): coalesced loads through the typed child
+// evaluator, a transpose through shared memory, each thread scans its 16-sample chunk in registers, a
+// warp-shuffle scan and one cross-warp step give every thread the fold of the rest of
+// its tile; the carry of the tiles before it in scan order comes from registers
+// (sequential walk) or from the look-back slots (lookback.cuh: aggregates only, folded in
+// a fixed order, so the bits do not depend on scheduling); the outputs leave through
+// shared memory with coalesced stores.
 #include "fg_reg.cuh"
+#include "lookback.cuh"
 
 namespace stlg {
 
-constexpr int UN_NW = 8;
-using UNC = RC<UN_NW>;
+// Two shapes of the same kernels:
+//   LB = false, NW = 8: one CTA per row walks its 4096-sample tiles from the scan start with
+//                       the carry in registers (large batches: rows fill the GPU);
+//   LB = true,  NW = 2: one CTA per 1024-sample tile, carries from the look-back slots
+//                       (lookback.cuh) — small batches / long rows (BASELINE C5's batch 64).
+constexpr int UN_SEQ = 8, UN_LB = 2;
+static_assert(RC<UN_LB>::N == LB_MIN_TILE, "look-back slots are sized for 1024-sample tiles");
 
-template <int RK, int MODE, int EK>
-__global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ FGParams p) {
-  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
-  __shared__ float buf[2][NP];
-  __shared__ RSt WS[UN_NW];
-  const long long row = blockIdx.x;
+// scan bounds of this CTA: every tile of the row (sequential) or tile blockIdx.x (look-back)
+template <bool LB>
+__device__ __forceinline__ void unt_span(int ntiles, long long& row, int& s0, int& s1) {
+  row = LB ? blockIdx.y : blockIdx.x;
+  s0 = LB ? (int)blockIdx.x : 0;
+  s1 = LB ? (int)blockIdx.x + 1 : ntiles;
+}
+
+template <int RK, int MODE, int EK, int NW, bool LB>
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_fwd(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
+  __shared__ float P[NP];
+  __shared__ RSt WS[NW];
   const int L = (int)p.L;
+  const int ntiles = (L + N - 1) / N;
+  long long row;
+  int s0, s1;
+  unt_span<LB>(ntiles, row, s0, s1);
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ev<MODE, EK> ev(p.child, row, p.mp);
   float* outr = p.out + row * L;
   const RSt id = rident<RK>();
-  RSt carry = id;  // fold of every sample after the current tile
-  int b = 0;
-  for (int c0 = ((L - 1) / N) * N; c0 >= 0; c0 -= N, b ^= 1) {
-    float* P = buf[b];
+  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
+  RSt seq = id;  // sequential shape: fold of every sample after the current tile
+  for (int s = s0; s < s1; ++s) {
+    const int c0 = (ntiles - 1 - s) * N;  // scan order: from the row end
     const int nt = (L - c0 < N) ? L - c0 : N;  // live samples in this tile
     {
       float* dst = P + tid + (tid >> 4);
@@ -80,9 +99,23 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
     RSt ex{__shfl_down_sync(0xffffffffu, v.m, 1), RK == RK_HARDV ? 0.f : __shfl_down_sync(0xffffffffu, v.s, 1), 0.f};
     if (lane == 0) WS[warp] = v;
     __syncthreads();
+    RSt tile = WS[NW - 1];  // the tile's aggregate
+#pragma unroll
+    for (int w = NW - 2; w >= 0; --w) tile = rcomb<RK>(WS[w], tile, tau2);
+    RSt carry = seq;
+    if (LB) {
+      if (tid == 0 && s + 1 < ntiles) {  // publish (later tiles in scan order fold it)
+        const unsigned pw[2] = {__float_as_uint(tile.m), __float_as_uint(tile.s)};
+        lb_publish<2>(slots + (size_t)s * LB_WORDS, pw);
+      }
+      // agg_{s-1} (+) (... (+) (agg_0 (+) id)): the sequential walk's expression
+      carry = lb_carry<2>(slots, s, id, [&](RSt x, const unsigned* w) {
+        return rcomb<RK>(RSt{__uint_as_float(w[0]), __uint_as_float(w[1]), 0.f}, x, tau2);
+      });
+    }
     RSt cw = carry;
 #pragma unroll
-    for (int w = UN_NW - 1; w > 0; --w)
+    for (int w = NW - 1; w > 0; --w)
       if (w > warp) cw = rcomb<RK>(WS[w], cw, tau2);
     const RSt cin = lane < 31 ? rcomb<RK>(ex, cw, tau2) : cw;
     float lo[RK == RK_LSE ? RG_EPT : 1];
@@ -96,12 +129,7 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
       if (RK == RK_LSE) lo[k] = sg * fmaf(l2, itau2, o.m - val);
       P[q0 + k] = sg * val;  // own slots: read by the coalesced store after the barrier
     }
-    {
-      RSt tile = WS[UN_NW - 1];
-#pragma unroll
-      for (int w = UN_NW - 2; w >= 0; --w) tile = rcomb<RK>(WS[w], tile, tau2);
-      carry = rcomb<RK>(tile, carry, tau2);
-    }
+    if (!LB) seq = rcomb<RK>(tile, seq, tau2);
     __syncthreads();
     const float* src = P + tid + (tid >> 4);
     float* op = outr + c0 + tid;
@@ -118,21 +146,25 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_fwd(const __grid_constant__ F
       for (int k = 0; k < RG_EPT; ++k)
         if (tid + k * T < nt) ap[k * T] = src[k * SS];
     }
+    __syncthreads();
   }
 }
 
 // Untimed LSE backward (gather form, tape.py:475-535): child j receives
 //   2^{tau2 u_j} sum_{t <= j} g_t 2^{-tau2 M_t}
 // — an inclusive prefix scan over the outputs of the (e_t = -M_t, g_t) elements
-// (RK_GLSE), tiles walked from the row start with the carry of the tiles done, then
-// the fused child VJP over the tile.
-template <int EK>
-__global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant__ FGParams p) {
-  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
+// (RK_GLSE), scan order from the row start, then the fused child VJP over the tile.
+template <int EK, int NW, bool LB>
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_lse(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
   __shared__ float B0[NP], B1[NP];
-  __shared__ RSt WP[UN_NW];
-  const long long row = blockIdx.x;
+  __shared__ RSt WP[NW];
   const int L = (int)p.L;
+  const int ntiles = (L + N - 1) / N;
+  long long row;
+  int s0, s1;
+  unt_span<LB>(ntiles, row, s0, s1);
   const float tau2 = p.mp.tau2, sg = p.sg, nsg = -p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
@@ -140,9 +172,11 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
   const float* lor = p.aux_in != nullptr ? p.aux_in + row * L : nullptr;  // trace low word
   Ev<M_LSE, EK> ev(p.child, row, p.mp);
   const RSt id = rident<RK_GLSE>();
-  RSt carry = id;  // fold of every output before the current tile
   const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
-  for (int c0 = 0; c0 < L; c0 += N) {
+  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
+  RSt seq = id;  // sequential shape: fold of every output before the current tile
+  for (int s = s0; s < s1; ++s) {
+    const int c0 = s * N;  // scan order: from the row start
     const int nt = (L - c0 < N) ? L - c0 : N;
 #pragma unroll
     for (int h = 0; h < RG_EPT; h += 8) {
@@ -181,9 +215,23 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
     RSt ex{__shfl_up_sync(0xffffffffu, v.m, 1), __shfl_up_sync(0xffffffffu, v.s, 1), 0.f};
     if (lane == 31) WP[warp] = v;
     __syncthreads();
+    RSt tile = WP[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) tile = rcomb<RK_GLSE>(tile, WP[w], tau2);
+    RSt carry = seq;
+    if (LB) {
+      if (tid == 0 && s + 1 < ntiles) {
+        const unsigned pw[2] = {__float_as_uint(tile.m), __float_as_uint(tile.s)};
+        lb_publish<2>(slots + (size_t)s * LB_WORDS, pw);
+      }
+      // ((id (+) agg_0) (+) agg_1) ... (+) agg_{s-1}
+      carry = lb_carry<2>(slots, s, id, [&](RSt x, const unsigned* w) {
+        return rcomb<RK_GLSE>(x, RSt{__uint_as_float(w[0]), __uint_as_float(w[1]), 0.f}, tau2);
+      });
+    }
     RSt cw = carry;
 #pragma unroll
-    for (int w = 0; w < UN_NW - 1; ++w)
+    for (int w = 0; w < NW - 1; ++w)
       if (w < warp) cw = rcomb<RK_GLSE>(cw, WP[w], tau2);
     const RSt cin = lane > 0 ? rcomb<RK_GLSE>(cw, ex, tau2) : cw;
 #pragma unroll
@@ -192,12 +240,7 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_lse(const __grid_constant
       B0[q0 + k] = o.m;  // own slots
       B1[q0 + k] = o.s;
     }
-    {
-      RSt tile = WP[0];
-#pragma unroll
-      for (int w = 1; w < UN_NW; ++w) tile = rcomb<RK_GLSE>(tile, WP[w], tau2);
-      carry = rcomb<RK_GLSE>(carry, tile, tau2);
-    }
+    if (!LB) seq = rcomb<RK_GLSE>(seq, tile, tau2);
     __syncthreads();
     const int jb = c0 + tid;
 #pragma unroll
@@ -252,24 +295,33 @@ __device__ __forceinline__ HRun hrun_shfl_down(HRun v, int o) {
   return r;
 }
 
-template <int EK>
-__global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constant__ FGParams p) {
-  constexpr int T = UNC::T, N = UNC::N, SS = UNC::SS, NP = UNC::NP;
+template <int EK, int NW, bool LB>
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_hard(const __grid_constant__ FGParams p) {
+  using C = RC<NW>;
+  constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
   __shared__ float U[NP];  // child values (max space), then the arg-max keys
   __shared__ float G[NP];  // cotangents
-  __shared__ HRun WS[UN_NW];
-  __shared__ RSt WM[UN_NW];
-  const long long row = blockIdx.x;
+  __shared__ HRun WS[NW];
+  __shared__ RSt WM[NW];
   const int L = (int)p.L;
+  const int ntiles = (L + N - 1) / N;
+  long long row;
+  int s0, s1;
+  unt_span<LB>(ntiles, row, s0, s1);
   const float sg = p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
   const RSt idm = rident<RK_HARDI>();
-  RSt mcarry = idm;                 // (max, first arg-max) of every position after the tile
-  HRun rcarry{-1, -1, 0.0, 1};      // run state of every position after the tile
+  const HRun idr{-1, -1, 0.0, 1};
   const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
-  for (int c0 = ((L - 1) / N) * N; c0 >= 0; c0 -= N) {
+  // look-back: arg-max aggregates in slot row 0, run aggregates in slot row 1
+  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
+  unsigned* rslots = LB ? slots + (size_t)gridDim.y * ntiles * LB_WORDS : nullptr;
+  RSt mseq = idm;  // sequential shape: (max, first arg-max) of every position after the tile
+  HRun rseq = idr; //                   run state of every position after the tile
+  for (int s = s0; s < s1; ++s) {
+    const int c0 = (ntiles - 1 - s) * N;  // scan order: from the row end
     const int nt = (L - c0 < N) ? L - c0 : N;
     {
       const int jb = c0 + tid;
@@ -309,9 +361,22 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constan
     RSt ex{__shfl_down_sync(0xffffffffu, v.m, 1), __shfl_down_sync(0xffffffffu, v.s, 1), 0.f};
     if (lane == 0) WM[warp] = v;
     __syncthreads();
+    RSt mtile = WM[NW - 1];
+#pragma unroll
+    for (int w = NW - 2; w >= 0; --w) mtile = rcomb<RK_HARDI>(WM[w], mtile, 0.f);
+    RSt mcarry = mseq;
+    if (LB) {
+      if (tid == 0 && s + 1 < ntiles) {
+        const unsigned pw[2] = {__float_as_uint(mtile.m), __float_as_uint(mtile.s)};
+        lb_publish<2>(slots + (size_t)s * LB_WORDS, pw);
+      }
+      mcarry = lb_carry<2>(slots, s, idm, [&](RSt x, const unsigned* w) {
+        return rcomb<RK_HARDI>(RSt{__uint_as_float(w[0]), __uint_as_float(w[1]), 0.f}, x, 0.f);
+      });
+    }
     RSt cw = mcarry;
 #pragma unroll
-    for (int w = UN_NW - 1; w > 0; --w)
+    for (int w = NW - 1; w > 0; --w)
       if (w > warp) cw = rcomb<RK_HARDI>(WM[w], cw, 0.f);
     const RSt cin = lane < 31 ? rcomb<RK_HARDI>(ex, cw, 0.f) : cw;
     int key[RG_EPT];
@@ -321,14 +386,9 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constan
       key[k] = (i0 + k < nt) ? __float_as_int(rcomb<RK_HARDI>(S[k], cin, 0.f).s) : -1;
       gk[k] = G[q0 + k];
     }
-    {
-      RSt tile = WM[UN_NW - 1];
-#pragma unroll
-      for (int w = UN_NW - 2; w >= 0; --w) tile = rcomb<RK_HARDI>(WM[w], tile, 0.f);
-      mcarry = rcomb<RK_HARDI>(tile, mcarry, 0.f);
-    }
+    if (!LB) mseq = rcomb<RK_HARDI>(mtile, mseq, 0.f);
     // the thread's run state over its chunk, then the segmented scan over later threads
-    HRun mine{-1, -1, 0.0, 1};
+    HRun mine = idr;
 #pragma unroll
     for (int k = RG_EPT - 1; k >= 0; --k)
       if (key[k] >= 0) mine = hrun_comb(mine, HRun{key[k], key[k], (double)gk[k], 1});
@@ -339,20 +399,31 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constan
       if (lane + o < 32) rv = hrun_comb(w, rv);
     }
     HRun rex = hrun_shfl_down(rv, 1);
-    if (lane == 31) rex = HRun{-1, -1, 0.0, 1};
+    if (lane == 31) rex = idr;
     if (lane == 0) WS[warp] = rv;
-    __syncthreads();  // WS / WM visible; U / G reads done (keys go into U below)
+    __syncthreads();  // WS visible; U / G reads done (keys go into U below)
+    HRun rtile = WS[NW - 1];
+#pragma unroll
+    for (int w = NW - 2; w >= 0; --w) rtile = hrun_comb(rtile, WS[w]);
+    HRun rcarry = rseq;
+    if (LB) {
+      if (tid == 0 && s + 1 < ntiles) {
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(rtile.tail);
+        const unsigned pw[5] = {(unsigned)rtile.kf, (unsigned)rtile.kl, (unsigned)tb, (unsigned)(tb >> 32),
+                                (unsigned)rtile.whole};
+        lb_publish<5>(rslots + (size_t)s * LB_WORDS, pw);
+      }
+      rcarry = lb_carry<5>(rslots, s, idr, [&](HRun x, const unsigned* w) {
+        const unsigned long long tb = (unsigned long long)w[2] | ((unsigned long long)w[3] << 32);
+        return hrun_comb(x, HRun{(int)w[0], (int)w[1], __longlong_as_double((long long)tb), (int)w[4]});
+      });
+    }
     HRun rw = rcarry;  // later tiles, then the later warps of this tile, in descending t
 #pragma unroll
-    for (int w = UN_NW - 1; w > 0; --w)
+    for (int w = NW - 1; w > 0; --w)
       if (w > warp) rw = hrun_comb(rw, WS[w]);
     const HRun prev = hrun_comb(rw, rex);  // everything at larger t than the thread's chunk
-    {
-      HRun tile = WS[UN_NW - 1];
-#pragma unroll
-      for (int w = UN_NW - 2; w >= 0; --w) tile = hrun_comb(tile, WS[w]);
-      rcarry = hrun_comb(rcarry, tile);
-    }
+    if (!LB) rseq = hrun_comb(rseq, rtile);
     // walk the chunk downwards; a run that ends here (the next lower position has another
     // key) is complete: write its total at its target through the child VJP
     int pk = prev.kl;
@@ -413,15 +484,36 @@ __global__ void __launch_bounds__(UNC::T, 2) k_unt_bwd_hard(const __grid_constan
     __VA_ARGS__;                       \
   }
 
+// shape choice: the look-back kernels when the rows alone would leave the GPU short of
+// CTAs (fewer rows than ~2 per SM) and a row spans several 1024-sample tiles
+static bool unt_use_lb(const FGParams& p) {
+  return p.lb != nullptr && p.B < 2 * 148 && p.L >= 4 * LB_MIN_TILE;
+}
+static cudaError_t unt_lb_reset(const FGParams& p, int rows_of_slots, cudaStream_t st) {
+  const long long ntiles = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
+  return cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * ntiles * rows_of_slots), st);
+}
+
 // register-blocked untimed forward (hard / LSE without masked_fill); false: not handled
 bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   if (p.fill || (mode != M_HARD && mode != M_LSE) || p.L >= (1LL << 30)) return false;
   const int ek = expr_kind(p.child);
-  dim3 grid((unsigned)p.B);
-  if (mode == M_HARD) {
-    UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_HARDV, M_HARD, EK><<<grid, UNC::T, 0, st>>>(p)))
+  if (unt_use_lb(p)) {
+    using C = RC<UN_LB>;
+    const dim3 grid((unsigned)((p.L + C::N - 1) / C::N), (unsigned)p.B);
+    if ((err = unt_lb_reset(p, 1, st)) != cudaSuccess) return true;
+    if (mode == M_HARD) {
+      UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_HARDV, M_HARD, EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))
+    } else {
+      UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_LSE, M_LSE, EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))
+    }
   } else {
-    UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_LSE, M_LSE, EK><<<grid, UNC::T, 0, st>>>(p)))
+    using C = RC<UN_SEQ>;
+    if (mode == M_HARD) {
+      UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_HARDV, M_HARD, EK, UN_SEQ, false><<<(unsigned)p.B, C::T, 0, st>>>(p)))
+    } else {
+      UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_LSE, M_LSE, EK, UN_SEQ, false><<<(unsigned)p.B, C::T, 0, st>>>(p)))
+    }
   }
   count_launch();
   err = cudaGetLastError();
@@ -432,10 +524,22 @@ bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
 bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   if (p.fill || (mode != M_LSE && mode != M_HARD) || p.L >= (1LL << 30)) return false;
   const int ek = expr_kind(p.child);
-  if (mode == M_HARD) {
-    UNT_DISPATCH_EK(ek, (k_unt_bwd_hard<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
+  if (unt_use_lb(p)) {
+    using C = RC<UN_LB>;
+    const dim3 grid((unsigned)((p.L + C::N - 1) / C::N), (unsigned)p.B);
+    if ((err = unt_lb_reset(p, mode == M_HARD ? 2 : 1, st)) != cudaSuccess) return true;
+    if (mode == M_HARD) {
+      UNT_DISPATCH_EK(ek, (k_unt_bwd_hard<EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))
+    } else {
+      UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))
+    }
   } else {
-    UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK><<<(unsigned)p.B, UNC::T, 0, st>>>(p)))
+    using C = RC<UN_SEQ>;
+    if (mode == M_HARD) {
+      UNT_DISPATCH_EK(ek, (k_unt_bwd_hard<EK, UN_SEQ, false><<<(unsigned)p.B, C::T, 0, st>>>(p)))
+    } else {
+      UNT_DISPATCH_EK(ek, (k_unt_bwd_lse<EK, UN_SEQ, false><<<(unsigned)p.B, C::T, 0, st>>>(p)))
+    }
   }
   count_launch();
   err = cudaGetLastError();

@@ -23,6 +23,7 @@ struct FGParams {
   int padmode;    // 1: windows read the padded child (smooth-interval hard path, no overrun rule)
   int fill;       // masked_fill compat: reduce sentinel-filled full columns (masking.py:195-202)
   float sent;     // SemanticsConfig.sentinel
+  unsigned* lb;   // untimed scans: look-back slots [B][tiles][LB_WORDS] (lookback.cuh)
   ModeP mp;
 };
 
@@ -45,6 +46,7 @@ struct UParams {
   float* scratch;  // backward: per-thread checkpoint slab of the persistent kernel (or null)
   unsigned long long* dacc;  // backward: reproducible accumulators [4][B, L] (detacc.cuh)
   int* dscale;               // backward: per-row grid exponents [B]
+  unsigned* lb;              // untimed hard: look-back slots [B][tiles][LB_WORDS] (lookback.cuh)
   ModeP mp;
 };
 
@@ -99,6 +101,11 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_fwd(int mode, FGParams& p, cudaStream_t st);
 cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st);
 size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K);
+// look-back slots of the multi-CTA untimed scans (lookback.cuh): tiles of >= 1024 samples
+constexpr int LB_MIN_TILE = 1024;
+inline size_t lb_slot_bytes(long long B, long long L) {
+  return (size_t)B * (size_t)((L + LB_MIN_TILE - 1) / LB_MIN_TILE) * 32;
+}
 cudaError_t launch_mining_grid(int mode, const float* x, long long n, int L, long long rs, const double* a,
                                const double* b, long long npairs, double c, double eps, float tau,
                                double gamma, double* loss, double* dloss, cudaStream_t st);

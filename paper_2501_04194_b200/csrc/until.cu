@@ -21,12 +21,14 @@
 //     element t0 + a + k + i, which is owned by lane (i + k) mod 32, so a
 //     shuffle replaces the atomic and each element is flushed once per warp.
 //   * untimed hard: the O(T) clamp recurrence out[t] = max(min(l_t, r_t),
-//     min(l_t, out[t+1])) as a chunked block scan of clamp functions; the
-//     backward finds each output's gradient source locally (terminator test
-//     with the stored out[t+1]) and sums cotangents over runs — no atomics,
-//     the child VJPs are fused.
+//     min(l_t, out[t+1])) as a block scan of clamp functions, one CTA per
+//     1024-sample chunk with look-back carries (lookback.cuh); the backward
+//     finds each output's gradient source locally (terminator test with the
+//     stored out[t+1]) and sums cotangents over runs — no atomics, the child
+//     VJPs are fused.
 #include "detacc.cuh"
 #include "kernels.cuh"
+#include "lookback.cuh"
 
 namespace stlg {
 
@@ -642,233 +644,278 @@ __device__ __forceinline__ Clamp clamp_compose(Clamp g, Clamp f) {
   return Clamp{clamp_apply(g, f.lo), clamp_apply(g, f.hi)};
 }
 
-constexpr int UH_T = 256, UH_E = 8, UH_CH = UH_T * UH_E, UH_S = UH_E + 1;
+// Two shapes (as fg_unt.cu): LB = false, one CTA of 256 threads per row walking its
+// 2048-sample chunks with the carry in registers (large batches); LB = true, one CTA of
+// 128 threads per 1024-sample chunk (grid: chunks x rows, blockIdx.x = scan index) that
+// publishes its aggregate (forward: the composed clamp; backward: the segmented run sum)
+// and folds the aggregates of the chunks before it in scan order (lookback.cuh).
+constexpr int UH_E = 8, UH_S = UH_E + 1, UH_SEQ = 256, UH_LB = 128;
+static_assert(UH_LB * UH_E == LB_MIN_TILE, "look-back slots are sized for 1024-sample tiles");
 __device__ __forceinline__ int uhpos(int k) { return (k >> 3) * UH_S + (k & 7); }
 
-template <int MODE>
-__global__ void __launch_bounds__(UH_T) k_until_unt_hard_fwd(const __grid_constant__ UParams p) {
+template <int MODE, bool LB>
+__global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_fwd(const __grid_constant__ UParams p) {
+  constexpr int UH_T = LB ? UH_LB : UH_SEQ, UH_CH = UH_T * UH_E;
   __shared__ float Ls[UH_T * UH_S];
   __shared__ float Rs[UH_T * UH_S];
   __shared__ Clamp cb[UH_T / 32];
-  const long long row = blockIdx.x, L = p.L;
+  const long long row = LB ? blockIdx.y : blockIdx.x, L = p.L;
+  const int nch = (int)((L + UH_CH - 1) / UH_CH);
   const int tid = threadIdx.x;
   const ChildEval cl(p.left, row), cr(p.right, row);
+  unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
-  float carry = -INFINITY;
-  for (long long c0 = ((L - 1) / UH_CH) * UH_CH; c0 >= 0; c0 -= UH_CH) {
-    {  // all of the thread's loads in flight before the first store (one CTA per row:
-       // nothing else hides the latency)
-      float lv[UH_E], rv[UH_E];
-      if (cl.kind != 0 && cr.kind != 0) {
+  float seq = -INFINITY;  // sequential shape: the value entering the current chunk
+  for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
+  const long long c0 = (long long)(nch - 1 - s) * UH_CH;  // scan order: from the row end
+  {  // all of the thread's loads in flight before the first store
+    float lv[UH_E], rv[UH_E];
+    if (cl.kind != 0 && cr.kind != 0) {
 #pragma unroll
-        for (int e = 0; e < UH_E; ++e) {
-          const long long t = c0 + tid + e * UH_T;
-          const long long tc = t < L ? t : L - 1;
-          lv[e] = cl.raw(tc);
-          rv[e] = cr.raw(tc);
-        }
-#pragma unroll
-        for (int e = 0; e < UH_E; ++e) {
-          const bool in = c0 + tid + e * UH_T < L;
-          lv[e] = in ? cl.apply(lv[e]) : 0.f;
-          rv[e] = in ? cr.apply(rv[e]) : 0.f;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < UH_E; ++e) {
-          const long long t = c0 + tid + e * UH_T;
-          lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
-          rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
-        }
+      for (int e = 0; e < UH_E; ++e) {
+        const long long t = c0 + tid + e * UH_T;
+        const long long tc = t < L ? t : L - 1;
+        lv[e] = cl.raw(tc);
+        rv[e] = cr.raw(tc);
       }
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {
-        Ls[uhpos(tid + e * UH_T)] = lv[e];
-        Rs[uhpos(tid + e * UH_T)] = rv[e];
+        const bool in = c0 + tid + e * UH_T < L;
+        lv[e] = in ? cl.apply(lv[e]) : 0.f;
+        rv[e] = in ? cr.apply(rv[e]) : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < UH_E; ++e) {
+        const long long t = c0 + tid + e * UH_T;
+        lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
+        rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
       }
     }
-    __syncthreads();
-    // this thread's function f_{t0} o f_{t0+1} o ... o f_{t0+E-1} (identity past the end)
-    Clamp f{-INFINITY, INFINITY};
-    for (int e = UH_E - 1; e >= 0; --e) {
-      if (c0 + tid * UH_E + e >= L) continue;
-      float l = Ls[tid * UH_S + e], r = Rs[tid * UH_S + e];
-      Clamp ft{(l <= r) ? l : r, l};
-      f = clamp_compose(ft, f);
-    }
-    // suffix composition over the later threads: warp shuffles, then the later warps
-    const int lane = tid & 31, warp = tid >> 5;
-    Clamp C = f;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Clamp n{__shfl_down_sync(0xffffffffu, C.lo, o), __shfl_down_sync(0xffffffffu, C.hi, o)};
-      if (lane + o < 32) C = clamp_compose(C, n);
+    for (int e = 0; e < UH_E; ++e) {
+      Ls[uhpos(tid + e * UH_T)] = lv[e];
+      Rs[uhpos(tid + e * UH_T)] = rv[e];
     }
-    Clamp ex{__shfl_down_sync(0xffffffffu, C.lo, 1), __shfl_down_sync(0xffffffffu, C.hi, 1)};
-    if (lane == 31) ex = Clamp{-INFINITY, INFINITY};
-    if (lane == 0) cb[warp] = C;
-    __syncthreads();
-    float vw = carry;  // the carry pushed through the later warps of the chunk
-    for (int w = UH_T / 32 - 1; w > warp; --w) vw = clamp_apply(cb[w], vw);
-    float v = clamp_apply(ex, vw);
-    for (int e = UH_E - 1; e >= 0; --e) {  // exact sequential walk with the reference tie rules
-      if (c0 + tid * UH_E + e >= L) continue;
-      float l = Ls[tid * UH_S + e], r = Rs[tid * UH_S + e];
-      float A = (l <= r) ? l : r;
-      float Bv = (l <= v) ? l : v;
-      v = (A >= Bv) ? A : Bv;
-      Ls[tid * UH_S + e] = v;
+  }
+  __syncthreads();
+  // this thread's function f_{t0} o f_{t0+1} o ... o f_{t0+E-1} (identity past the end)
+  Clamp f{-INFINITY, INFINITY};
+  for (int e = UH_E - 1; e >= 0; --e) {
+    if (c0 + tid * UH_E + e >= L) continue;
+    float l = Ls[tid * UH_S + e], r = Rs[tid * UH_S + e];
+    Clamp ft{(l <= r) ? l : r, l};
+    f = clamp_compose(ft, f);
+  }
+  // suffix composition over the later threads: warp shuffles, then the later warps
+  const int lane = tid & 31, warp = tid >> 5;
+  Clamp C = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Clamp n{__shfl_down_sync(0xffffffffu, C.lo, o), __shfl_down_sync(0xffffffffu, C.hi, o)};
+    if (lane + o < 32) C = clamp_compose(C, n);
+  }
+  Clamp ex{__shfl_down_sync(0xffffffffu, C.lo, 1), __shfl_down_sync(0xffffffffu, C.hi, 1)};
+  if (lane == 31) ex = Clamp{-INFINITY, INFINITY};
+  if (lane == 0) cb[warp] = C;
+  __syncthreads();
+  float carry = seq;
+  if (LB) {
+    if (tid == 0 && s + 1 < nch) {  // the chunk's function cb[0] o cb[1] o ... (later last)
+      Clamp F = cb[UH_T / 32 - 1];
+      for (int w = UH_T / 32 - 2; w >= 0; --w) F = clamp_compose(cb[w], F);
+      const unsigned pw[2] = {__float_as_uint(F.lo), __float_as_uint(F.hi)};
+      lb_publish<2>(slots + (size_t)s * LB_WORDS, pw);
     }
-    __syncthreads();
-    carry = Ls[0];
-    for (int k = tid; k < UH_CH; k += UH_T) {
-      long long t = c0 + k;
-      if (t < L) p.out[row * L + t] = Ls[uhpos(k)];
-    }
-    __syncthreads();
+    // the value entering the chunk: the later chunks' functions applied in scan order
+    carry = lb_carry<2>(slots, s, -INFINITY, [](float x, const unsigned* w) {
+      return clamp_apply(Clamp{__uint_as_float(w[0]), __uint_as_float(w[1])}, x);
+    });
+  }
+  float vw = carry;  // the carry pushed through the later warps of the chunk
+  for (int w = UH_T / 32 - 1; w > warp; --w) vw = clamp_apply(cb[w], vw);
+  float v = clamp_apply(ex, vw);
+  for (int e = UH_E - 1; e >= 0; --e) {  // exact sequential walk with the reference tie rules
+    if (c0 + tid * UH_E + e >= L) continue;
+    float l = Ls[tid * UH_S + e], r = Rs[tid * UH_S + e];
+    float A = (l <= r) ? l : r;
+    float Bv = (l <= v) ? l : v;
+    v = (A >= Bv) ? A : Bv;
+    Ls[tid * UH_S + e] = v;
+  }
+  __syncthreads();
+  if (!LB) seq = Ls[0];
+  for (int k = tid; k < UH_CH; k += UH_T) {
+    long long t = c0 + k;
+    if (t < L) p.out[row * L + t] = Ls[uhpos(k)];
+  }
+  __syncthreads();
   }
 }
 
 // backward: terminator test per t with the stored out[t+1]; runs of equal
 // source end at their terminator, whose own index is the source index, so
 // each child cotangent is final when its run ends (no atomics, fused VJPs).
-template <int MODE>
-__global__ void __launch_bounds__(UH_T) k_until_unt_hard_bwd(const __grid_constant__ UParams p) {
+// Chunk carry: the cotangent accumulated since the last terminator in the chunks
+// before (scan order from the row start).
+template <int MODE, bool LB>
+__global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(const __grid_constant__ UParams p) {
+  constexpr int UH_T = LB ? UH_LB : UH_SEQ, UH_CH = UH_T * UH_E;
   __shared__ float Ls[UH_T * UH_S], Rs[UH_T * UH_S], Os[UH_T * UH_S], Gs[UH_T * UH_S];
   __shared__ double wsum[UH_T / 32];
   __shared__ int wflag[UH_T / 32];
-  const long long row = blockIdx.x, L = p.L;
+  const long long row = LB ? blockIdx.y : blockIdx.x, L = p.L;
+  const int nch = (int)((L + UH_CH - 1) / UH_CH);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* outr = p.out_in + row * L;
   const float* cot = p.cot + row * L;
   const ChildEval cl(p.left, row), cr(p.right, row);
-  double carry = 0.0;  // cotangent accumulated since the last terminator (earlier chunks)
-  for (long long c0 = 0; c0 < L; c0 += UH_CH) {
-    {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
-      float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
-      const bool fast = cl.kind != 0 && cr.kind != 0;
-#pragma unroll
-      for (int e = 0; e < UH_E; ++e) {
-        const long long t = c0 + tid + e * UH_T;
-        const long long tc = t < L ? t : L - 1;
-        const long long to = t + 1 < L ? t + 1 : L - 1;
-        if (fast) {
-          lv[e] = cl.raw(tc);
-          rv[e] = cr.raw(tc);
-        }
-        ov[e] = outr[to];
-        gv[e] = cot[tc];
-      }
-#pragma unroll
-      for (int e = 0; e < UH_E; ++e) {
-        const long long t = c0 + tid + e * UH_T;
-        const bool in = t < L;
-        if (fast) {
-          lv[e] = in ? cl.apply(lv[e]) : 0.f;
-          rv[e] = in ? cr.apply(rv[e]) : 0.f;
-        } else {
-          lv[e] = in ? cl.value<MODE>(t, p.mp) : 0.f;
-          rv[e] = in ? cr.value<MODE>(t, p.mp) : 0.f;
-        }
-        ov[e] = (t + 1 < L) ? ov[e] : 0.f;
-        gv[e] = in ? gv[e] : 0.f;
-      }
-#pragma unroll
-      for (int e = 0; e < UH_E; ++e) {
-        const int q = uhpos(tid + e * UH_T);
-        Ls[q] = lv[e];
-        Rs[q] = rv[e];
-        Os[q] = ov[e];
-        Gs[q] = gv[e];
-      }
-    }
-    __syncthreads();
-    float g[UH_E];
-    int term[UH_E];  // 0: pass to the next sample's source, 1: l_t, 2: r_t
-    double tail = 0.0;
-    int anyterm = 0;
+  unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
+  double seq = 0.0;  // sequential shape: cotangent accumulated since the last terminator
+  for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
+  const long long c0 = (long long)s * UH_CH;
+  {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
+    float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
+    const bool fast = cl.kind != 0 && cr.kind != 0;
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      const long long t = c0 + tid * UH_E + e;
-      const int q = tid * UH_S + e;
-      term[e] = 0;
-      g[e] = 0.f;
-      if (t < L) {
-        const float l = Ls[q], r = Rs[q];
-        const bool a_is_l = l <= r;
-        const float A = a_is_l ? l : r;
-        int src;
-        if (t == L - 1) {
-          src = a_is_l ? 1 : 2;
-        } else {
-          const float v = Os[q];
-          const bool b_is_l = l <= v;
-          const float Bv = b_is_l ? l : v;
-          src = (A >= Bv) ? (a_is_l ? 1 : 2) : (b_is_l ? 1 : 0);
-        }
-        term[e] = src;
-        g[e] = Gs[q];
-        if (src) {
-          anyterm = 1;
-          tail = 0.0;
-        } else {
-          tail += (double)g[e];
-        }
+      const long long t = c0 + tid + e * UH_T;
+      const long long tc = t < L ? t : L - 1;
+      const long long to = t + 1 < L ? t + 1 : L - 1;
+      if (fast) {
+        lv[e] = cl.raw(tc);
+        rv[e] = cr.raw(tc);
       }
+      ov[e] = outr[to];
+      gv[e] = cot[tc];
     }
-    // exclusive segmented prefix (sum since the last terminator) over the earlier threads:
-    // (s, f) then (s', f')  ->  (f' ? s' : s + s', f | f'); warp shuffles, then the warps
-    double is = tail;
-    int iflag = anyterm;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double ps = __shfl_up_sync(0xffffffffu, is, o);
-      const int pf = __shfl_up_sync(0xffffffffu, iflag, o);
-      if (lane >= o) {
-        if (!iflag) is += ps;
-        iflag |= pf;
-      }
-    }
-    double xs = __shfl_up_sync(0xffffffffu, is, 1);
-    int xf = __shfl_up_sync(0xffffffffu, iflag, 1);
-    if (lane == 0) xs = 0.0, xf = 0;
-    if (lane == 31) {
-      wsum[warp] = is;
-      wflag[warp] = iflag;
-    }
-    __syncthreads();
-    double before = carry;  // carry, then the earlier warps, then the earlier lanes
-    for (int w = 0; w < warp; ++w) before = wflag[w] ? wsum[w] : before + wsum[w];
-    double run = xf ? xs : before + xs;
-    double nextc = carry;
-    for (int w = 0; w < UH_T / 32; ++w) nextc = wflag[w] ? wsum[w] : nextc + wsum[w];
-    // the thread's gradients into its own staging slots (l -> Ls, r -> Rs)
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      const int q = tid * UH_S + e;
-      run += (double)g[e];
-      float gl = 0.f, gr = 0.f;
-      if (term[e] == 1) {
-        gl = (float)run;
-        run = 0.0;
-      } else if (term[e] == 2) {
-        gr = (float)run;
-        run = 0.0;
+      const long long t = c0 + tid + e * UH_T;
+      const bool in = t < L;
+      if (fast) {
+        lv[e] = in ? cl.apply(lv[e]) : 0.f;
+        rv[e] = in ? cr.apply(rv[e]) : 0.f;
+      } else {
+        lv[e] = in ? cl.value<MODE>(t, p.mp) : 0.f;
+        rv[e] = in ? cr.value<MODE>(t, p.mp) : 0.f;
       }
-      Ls[q] = gl;
-      Rs[q] = gr;
+      ov[e] = (t + 1 < L) ? ov[e] : 0.f;
+      gv[e] = in ? gv[e] : 0.f;
     }
-    __syncthreads();
-    // coalesced child VJPs (left first: first-writer order)
-    for (int k = tid; k < UH_CH; k += UH_T) {
-      const long long t = c0 + k;
-      if (t >= L) break;
-      const int q = uhpos(k);
-      cl.grad<MODE>(t, Ls[q], p.mp);
-      cr.grad<MODE>(t, Rs[q], p.mp);
+#pragma unroll
+    for (int e = 0; e < UH_E; ++e) {
+      const int q = uhpos(tid + e * UH_T);
+      Ls[q] = lv[e];
+      Rs[q] = rv[e];
+      Os[q] = ov[e];
+      Gs[q] = gv[e];
     }
-    carry = nextc;
-    __syncthreads();
+  }
+  __syncthreads();
+  float g[UH_E];
+  int term[UH_E];  // 0: pass to the next sample's source, 1: l_t, 2: r_t
+  double tail = 0.0;
+  int anyterm = 0;
+#pragma unroll
+  for (int e = 0; e < UH_E; ++e) {
+    const long long t = c0 + tid * UH_E + e;
+    const int q = tid * UH_S + e;
+    term[e] = 0;
+    g[e] = 0.f;
+    if (t < L) {
+      const float l = Ls[q], r = Rs[q];
+      const bool a_is_l = l <= r;
+      const float A = a_is_l ? l : r;
+      int src;
+      if (t == L - 1) {
+        src = a_is_l ? 1 : 2;
+      } else {
+        const float v = Os[q];
+        const bool b_is_l = l <= v;
+        const float Bv = b_is_l ? l : v;
+        src = (A >= Bv) ? (a_is_l ? 1 : 2) : (b_is_l ? 1 : 0);
+      }
+      term[e] = src;
+      g[e] = Gs[q];
+      if (src) {
+        anyterm = 1;
+        tail = 0.0;
+      } else {
+        tail += (double)g[e];
+      }
+    }
+  }
+  // exclusive segmented prefix (sum since the last terminator) over the earlier threads:
+  // (s, f) then (s', f')  ->  (f' ? s' : s + s', f | f'); warp shuffles, then the warps
+  double is = tail;
+  int iflag = anyterm;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ps = __shfl_up_sync(0xffffffffu, is, o);
+    const int pf = __shfl_up_sync(0xffffffffu, iflag, o);
+    if (lane >= o) {
+      if (!iflag) is += ps;
+      iflag |= pf;
+    }
+  }
+  double xs = __shfl_up_sync(0xffffffffu, is, 1);
+  int xf = __shfl_up_sync(0xffffffffu, iflag, 1);
+  if (lane == 0) xs = 0.0, xf = 0;
+  if (lane == 31) {
+    wsum[warp] = is;
+    wflag[warp] = iflag;
+  }
+  __syncthreads();
+  double carry = seq;
+  if (LB) {
+    if (tid == 0 && s + 1 < nch) {  // the chunk's (sum since its last terminator, any terminator)
+      double cs = 0.0;
+      int cf = 0;
+      for (int w = 0; w < UH_T / 32; ++w) {
+        cs = wflag[w] ? wsum[w] : cs + wsum[w];
+        cf |= wflag[w];
+      }
+      const unsigned long long b = (unsigned long long)__double_as_longlong(cs);
+      const unsigned pw[3] = {(unsigned)b, (unsigned)(b >> 32), (unsigned)cf};
+      lb_publish<3>(slots + (size_t)s * LB_WORDS, pw);
+    }
+    carry = lb_carry<3>(slots, s, 0.0, [](double x, const unsigned* w) {
+      const double cs = __longlong_as_double((long long)((unsigned long long)w[0] | ((unsigned long long)w[1] << 32)));
+      return w[2] ? cs : x + cs;
+    });
+  } else {
+    for (int w = 0; w < UH_T / 32; ++w) seq = wflag[w] ? wsum[w] : seq + wsum[w];
+  }
+  double before = carry;  // carry, then the earlier warps, then the earlier lanes
+  for (int w = 0; w < warp; ++w) before = wflag[w] ? wsum[w] : before + wsum[w];
+  double run = xf ? xs : before + xs;
+  // the thread's gradients into its own staging slots (l -> Ls, r -> Rs)
+#pragma unroll
+  for (int e = 0; e < UH_E; ++e) {
+    const int q = tid * UH_S + e;
+    run += (double)g[e];
+    float gl = 0.f, gr = 0.f;
+    if (term[e] == 1) {
+      gl = (float)run;
+      run = 0.0;
+    } else if (term[e] == 2) {
+      gr = (float)run;
+      run = 0.0;
+    }
+    Ls[q] = gl;
+    Rs[q] = gr;
+  }
+  __syncthreads();
+  // coalesced child VJPs (left first: first-writer order)
+  for (int k = tid; k < UH_CH; k += UH_T) {
+    const long long t = c0 + k;
+    if (t >= L) break;
+    const int q = uhpos(k);
+    cl.grad<MODE>(t, Ls[q], p.mp);
+    cr.grad<MODE>(t, Rs[q], p.mp);
+  }
+  __syncthreads();
   }
 }
 
@@ -1372,11 +1419,21 @@ static cudaError_t det_end(int mode, const UParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// untimed hard Until: the look-back shape when the rows alone leave the GPU short of CTAs
+static bool uh_use_lb(const UParams& p) { return p.lb != nullptr && p.B < 2 * 148 && p.L >= 4 * LB_MIN_TILE; }
+
 template <int MODE>
 static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
   if (MODE == M_HARD && until_ht_applicable(p)) return launch_until_ht_fwd(p, st);  // O(T), until_ht.cu
   if (p.untimed && MODE == M_HARD && !p.fill) {
-    k_until_unt_hard_fwd<MODE><<<(unsigned)p.B, UH_T, 0, st>>>(p);
+    if (uh_use_lb(p)) {
+      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
+      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);
+      if (e != cudaSuccess) return e;
+      k_until_unt_hard_fwd<MODE, true><<<dim3((unsigned)nch, (unsigned)p.B), UH_LB, 0, st>>>(p);
+    } else {
+      k_until_unt_hard_fwd<MODE, false><<<(unsigned)p.B, UH_SEQ, 0, st>>>(p);
+    }
     count_launch();
     return cudaGetLastError();
   }
@@ -1401,7 +1458,14 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
 template <int MODE>
 static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if (p.untimed && MODE == M_HARD && !p.fill) {
-    k_until_unt_hard_bwd<MODE><<<(unsigned)p.B, UH_T, 0, st>>>(p);
+    if (uh_use_lb(p)) {
+      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
+      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);
+      if (e != cudaSuccess) return e;
+      k_until_unt_hard_bwd<MODE, true><<<dim3((unsigned)nch, (unsigned)p.B), UH_LB, 0, st>>>(p);
+    } else {
+      k_until_unt_hard_bwd<MODE, false><<<(unsigned)p.B, UH_SEQ, 0, st>>>(p);
+    }
     count_launch();
     return cudaGetLastError();
   }

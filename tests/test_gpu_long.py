@@ -251,3 +251,42 @@ def test_hard_timed_until_sweep(cuda, a, K, L, pad):
     _, ref_g2, _ = stl_oracle.trace_and_grad(f, arrays, cfg, cot.astype(np.float64))
     for k in ("x", "y"):
         assert rel_err(g2[k], ref_g2[k]) <= 1e-6, k
+
+
+@pytest.mark.parametrize("case", ["F_hard", "G_lse", "U_hard"])
+def test_untimed_sequential_shape_large_batch(cuda, case):
+    """Untimed scans at >= 296 rows take the one-CTA-per-row shape (fg_unt.cu / until.cu,
+    LB = false) with its register carry across 4096- / 2048-sample tiles; rows checked
+    against the oracle (the look-back shape is covered by the small-batch tests above)."""
+    rng = np.random.default_rng(300 + len(case))
+    B, T = 300, 9000
+    x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    y = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+    cot = np.asarray(rng.uniform(0.5, 1.5, (B, T)), dtype=np.float32)
+    if case == "F_hard":
+        f, cfg, data = P.Eventually(P.Pred("x", ">", 0.0)), P.SemanticsConfig(), {"x": np.round(2 * x)}
+    elif case == "G_lse":
+        f, cfg, data = P.Always(P.Pred("x", ">", 0.0)), P.SemanticsConfig(mode=P.LogSumExp(10.0)), {"x": x}
+    else:
+        f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", ">", 0.0))
+        cfg, data = P.SemanticsConfig(), {"x": np.round(2 * x), "y": np.round(2 * y)}
+    tr, g = _run(f, data, cfg, cot)
+    for r in (0, 151, 299):
+        c64 = cot[r:r + 1].astype(np.float64)
+        if case == "G_lse":
+            ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, {"x": x[r:r + 1].astype(np.float64)}, cfg, c64)
+            assert rel_err(tr[r:r + 1], ref_tr) <= TOL
+            assert rel_err(g["x"][r:r + 1], ref_g["x"]) <= TOL
+        elif case == "F_hard":
+            xr = data["x"][r:r + 1].astype(np.float64)
+            ref, _ = stl_oracle.suffix_hard(xr, np.ones((1, T)), "max")
+            _, rg = stl_oracle.suffix_hard(xr, c64, "max")
+            assert_hard_equal(tr[r:r + 1], ref.astype(np.float32))
+            assert rel_err(g["x"][r:r + 1], rg) <= 1e-6
+        else:
+            xr, yr = data["x"][r:r + 1].astype(np.float64), data["y"][r:r + 1].astype(np.float64)
+            ref, _, _ = stl_oracle.until_untimed_hard(xr, yr, np.ones((1, T)))
+            _, dl, dr = stl_oracle.until_untimed_hard(xr, yr, c64)
+            assert_hard_equal(tr[r:r + 1], ref.astype(np.float32))
+            assert rel_err(g["x"][r:r + 1], dl) <= 1e-6
+            assert rel_err(g["y"][r:r + 1], dr) <= 1e-6

@@ -215,9 +215,10 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
     auto fin = [&](int, int i, RSt w, int sl) {
       const float l2 = (RK == RK_HARD || RK == RK_HARDI) ? 0.f : lg2f(w.s);
       const bool live = full || t0 + i < nvalid;
-      if (RK == RK_HARDI) {  // value; aux: the first arg-max (global child index) for the backward
+      if (RK == RK_HARDI) {  // value; aux: the first arg-max for the backward, as its offset
+                             // in the window (K <= 1024: 16 bits; 0xffff: no live window)
         P0[sl] = __fadd_rn(live ? sg * w.m : padv, czero);
-        P1[sl] = live ? w.s : __int_as_float(-1);
+        P1[sl] = __int_as_float(live ? __float_as_int(w.s) - (t0 + p.a + i) : 0xffff);
       } else if (RK == RK_SOFT) {  // value m + q / s; aux: the window LSE (max space) for the backward
         const float v = w.m + w.q / w.s;
         P0[sl] = __fadd_rn(live ? sg * v : padv, czero);
@@ -239,12 +240,19 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
     if (auxr != nullptr) {  // LSE: low word of the double-float trace; softmax: window LSE;
-                            // hard: arg-max index
+                            // hard: arg-max offset (uint16 plane in the row's aux words)
       const float* src1 = P1 + rpad(tid + K - 1);
-      float* ap = auxr + t0 + tid;
+      if (RK == RK_HARDI) {
+        unsigned short* ap = reinterpret_cast<unsigned short*>(auxr) + t0 + tid;
 #pragma unroll
-      for (int k = 0; k < RG_EPT; ++k)
-        if (tid + k * T < tend) ap[k * T] = src1[k * SS];
+        for (int k = 0; k < RG_EPT; ++k)
+          if (tid + k * T < tend) ap[k * T] = (unsigned short)__float_as_int(src1[k * SS]);
+      } else {
+        float* ap = auxr + t0 + tid;
+#pragma unroll
+        for (int k = 0; k < RG_EPT; ++k)
+          if (tid + k * T < tend) ap[k * T] = src1[k * SS];
+      }
     }
   }
 }
@@ -281,7 +289,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
   if (t0 >= nvalid) {  // every output of the tile overruns
     for (int i = tid; i < tend; i += T) {
       outr[t0 + i] = __fadd_rn(padv, czero);
-      if (auxr) auxr[t0 + i] = RK == RK_HARDI ? __int_as_float(-1) : 0.f;
+      if (auxr && RK == RK_HARDI) reinterpret_cast<unsigned short*>(auxr)[t0 + i] = 0xffff;
+      else if (auxr) auxr[t0 + i] = 0.f;
     }
     return;
   }
@@ -648,32 +657,35 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
-  // IDX: the forward stored every window's first arg-max (global child index, aux): the
-  // keys come from it directly — no child loads, no scans (12 B per sample: g, index, d c)
+  // IDX: the forward stored every window's first arg-max (its offset in the window, a
+  // uint16 plane in the aux words): the keys come from it directly — no child loads, no
+  // scans (10 B per sample: g, offset, d c)
   int key[RG_EPT];
   RSt x[RG_EPT];
   float g[RG_EPT];
   if constexpr (IDX) {
     const int so = tid + (tid >> 4);
     const int tb = first + tid - p.a;
-    const float* ix = p.aux_in + row * L;
+    const unsigned short* ix = reinterpret_cast<const unsigned short*>(p.aux_in + row * L);
     const int thi = nvalid > 0 ? nvalid - 1 : 0;
 #pragma unroll
     for (int h = 0; h < RG_EPT; h += CAV_LB) {
-      float gv[CAV_LB], iv[CAV_LB];
+      float gv[CAV_LB];
+      int iv[CAV_LB];
 #pragma unroll
       for (int k = 0; k < CAV_LB; ++k) {
         const int t = tb + (h + k) * T;
         const int tc = t < 0 ? 0 : (t > thi ? thi : t);
         gv[k] = ld_na(cot + tc);
-        iv[k] = ld_na(ix + tc);
+        iv[k] = __ldg(ix + tc);
       }
 #pragma unroll
       for (int k = 0; k < CAV_LB; ++k) {
         const int t = tb + (h + k) * T;
         const bool wv = tid + (h + k) * T < nwin && t >= 0 && t < nvalid;
-        // keys stay non-decreasing: 0 below the row start, NOKEY past the live windows
-        const int kk = wv ? __float_as_int(iv[k]) - first : (t < 0 ? 0 : NOKEY);
+        // key = window-local arg-max (offset + window index); keys stay non-decreasing:
+        // 0 below the row start, NOKEY past the live windows
+        const int kk = wv ? iv[k] + tid + (h + k) * T : (t < 0 ? 0 : NOKEY);
         P0[so + (h + k) * SS] = __int_as_float(kk);
         P1[so + (h + k) * SS] = wv ? gv[k] : 0.f;
       }

@@ -576,7 +576,11 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_sm(const __grid_constant
 // Inputs cover NB+1 blocks from s0 = j0 - K + 1 (the start of the window of
 // output t = j0 - b); outputs t = s - a for starts s in blocks 0..NB-1.
 //   U [(NB+1)Kp] child, PV/PI prefix (value, tile-local index),
-//   GT [NB*Kp] cotangent by start, G [J] accumulated child cotangent
+//   GT [NB*Kp] cotangent by start, G [2][J] accumulated child cotangent: thread qb's
+//   windows reach blocks qb and qb+1 only, so even and odd threads each own their
+//   targets in one of the two copies (plain adds in program order, summed in a fixed
+//   order at the end: reproducible, no atomics); padded targets ('last') are summed per
+//   thread and folded in thread order
 template <int EK>
 __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_constant__ FGParams p) {
   extern __shared__ __align__(16) float sm[];
@@ -597,6 +601,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
   int* PI = reinterpret_cast<int*>(sm + 2 * nsi);
   float* GT = sm + 3 * nsi;
   float* G = GT + NB * Kp;
+  float* G2 = G + J;
+  __shared__ float PADG[256];
   const float sg = p.sg;
   const float* cot = p.cot + row * L;
   Ev<M_HARD, EK> ev(p.child, row, p.mp);
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
       }
     }
   }
-  for (int i = threadIdx.x; i < J; i += FG_THREADS) G[i] = 0.f;
+  for (int i = threadIdx.x; i < 2 * J; i += FG_THREADS) G[i] = 0.f;
   // all-pad windows route to c[L-1]; in fill mode only if the pad beats the sentinel
   const bool own_last = p.pad_last && (L - 1 >= j0) && (L - 1 < j0 + J) &&
                         !(p.fill && ufill <= -p.sent);
@@ -660,6 +666,8 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
   if (threadIdx.x < NB) {
     const int qb = threadIdx.x;
     const int b0 = qb * Kp, nb = b0 + Kp - 1;
+    float* Gw = (qb & 1) ? G2 : G;
+    float padg = 0.f;
     float av = U[b0 + K - 1];
     int ai = qb * K + K - 1;
 #pragma unroll 4
@@ -680,10 +688,20 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
         if (!fill_merge<M_HARD>(rv, lse0, (float)(L + p.b - K), p.sent, s0 + qb * K + i > 0, 0.f, 0.f))
           g = 0.f;
       }
-      int jj = s0 + ri;
-      if (jj >= L) jj = p.pad_last ? L - 1 : -1;  // padded samples route to c[L-1] ('last')
-      if (g != 0.f && jj >= j0 && jj < j0 + J) atomicAdd(&G[jj - j0], g);
+      const int jj = s0 + ri;
+      if (jj >= L) {  // padded samples route to c[L-1] ('last')
+        if (p.pad_last) padg += g;
+      } else if (g != 0.f && jj >= j0 && jj < j0 + J) {
+        Gw[jj - j0] += g;
+      }
     }
+    PADG[qb] = padg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && p.pad_last && L - 1 >= j0 && L - 1 < j0 + J) {
+    float s = 0.f;
+    for (int q = 0; q < NB; ++q) s += PADG[q];
+    G[L - 1 - j0] += s;
   }
   __syncthreads();
   const int jn = (j0 + J < L ? j0 + J : L) - j0;
@@ -699,7 +717,7 @@ __global__ void __launch_bounds__(FG_THREADS) k_fgt_bwd_hard(const __grid_consta
       int i = i0 + u * FG_THREADS;
       if (i >= jn) continue;
       int j = j0 + i;
-      float g = G[i];
+      float g = G[i] + G2[i];
       if (own_last && j == L - 1) g += padsum;
       ev.grad(j, r[u], g);
     }
@@ -802,6 +820,68 @@ __global__ void __launch_bounds__(256) k_fg_timed_bwd_direct(const __grid_consta
       }
     }
   }
+}
+
+// backward for windows of K < 4 samples in gather form: thread j sums the contributions
+// of the (at most 3) outputs whose window holds j, recomputing each window — every
+// element written once, no atomics, so the sum order is fixed.  Element L-1 also
+// collects the padded samples of 'last' padding and the overrun outputs.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_fg_timed_bwd_gather(const __grid_constant__ FGParams p) {
+  const long long row = blockIdx.y, L = p.L;
+  const long long nvalid = p.padmode ? L : L - p.b;
+  const float tau2 = p.mp.tau2;
+  const float padv = p.pad_last ? expr_eval<MODE>(p.child, row, L - 1, p.mp) : p.pad_value;
+  auto uval = [&](long long idx) {
+    return p.sg * (idx < L ? expr_eval<MODE>(p.child, row, idx, p.mp) : padv);
+  };
+  const float* cot = p.cot + row * L;
+  float* gb = p.gbuf + row * L;
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= L) return;
+  const bool last = j == L - 1;
+  // outputs whose window reaches j (or, for L-1 with 'last' padding, any padded sample)
+  long long t_lo = j - p.b, t_hi = last ? L - 1 : j - p.a;
+  if (t_lo < 0) t_lo = 0;
+  float acc = 0.f;
+  for (long long t = t_lo; t <= t_hi; ++t) {
+    const float g = cot[t];
+    if (g == 0.f) continue;
+    if (t >= nvalid) {  // overrun output: the whole cotangent to the pad source
+      if (last && p.pad_last) acc += g;
+      continue;
+    }
+    if (MODE == M_HARD) {
+      float m = -INFINITY;
+      long long am = 0;
+      for (int k = 0; k < p.K; ++k) {
+        const float x = uval(t + p.a + k);
+        if (x > m) {
+          m = x;
+          am = t + p.a + k;
+        }
+      }
+      if (am >= L) am = p.pad_last ? L - 1 : -1;
+      if (p.fill) {
+        float lse0 = 0.f;
+        if (!fill_merge<M_HARD>(m, lse0, (float)(L + p.b - p.K), p.sent, t + p.a > 0, 0.f, 0.f)) am = -1;
+      }
+      if (am == j) acc += g;
+    } else {
+      const float M = p.sg * p.out_in[row * L + t];
+      const float Lt = (MODE == M_SOFT) ? p.aux_in[row * L + t] : M;
+      for (int k = 0; k < p.K; ++k) {
+        long long idx = t + p.a + k;
+        if (idx >= L) idx = p.pad_last ? L - 1 : -1;
+        if (idx != j) continue;
+        const float x = uval(t + p.a + k);
+        float w = ex2f(tau2 * (x - Lt));
+        if (MODE == M_SOFT) w *= fmaf(p.mp.tau, x - M, 1.f);
+        acc += g * w;
+      }
+    }
+  }
+  gb[j] = acc;
 }
 
 // ===========================================================================
@@ -924,11 +1004,17 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
   if (mode == M_SOFT && sx_applicable(p)) return launch_sx_bwd(p, st);
   if (reg_applicable(mode, p, true)) return launch_reg_bwd(mode, expr_kind(p.child), p, st);
   if (use_direct(p.K, mode)) {
-    if ((e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
     dim3 grid((unsigned)((p.L + 255) / 256), (unsigned)p.B);
-    if (mode == M_HARD) k_fg_timed_bwd_direct<M_HARD><<<grid, 256, 0, st>>>(p);
-    else if (mode == M_LSE) k_fg_timed_bwd_direct<M_LSE><<<grid, 256, 0, st>>>(p);
-    else k_fg_timed_bwd_direct<M_SOFT><<<grid, 256, 0, st>>>(p);
+    if (p.K < 4) {  // gather form: reproducible (K > ~3000 windows keep the scatter below)
+      if (mode == M_HARD) k_fg_timed_bwd_gather<M_HARD><<<grid, 256, 0, st>>>(p);
+      else if (mode == M_LSE) k_fg_timed_bwd_gather<M_LSE><<<grid, 256, 0, st>>>(p);
+      else k_fg_timed_bwd_gather<M_SOFT><<<grid, 256, 0, st>>>(p);
+    } else {
+      if ((e = cudaMemsetAsync(p.gbuf, 0, sizeof(float) * p.B * p.L, st)) != cudaSuccess) return e;
+      if (mode == M_HARD) k_fg_timed_bwd_direct<M_HARD><<<grid, 256, 0, st>>>(p);
+      else if (mode == M_LSE) k_fg_timed_bwd_direct<M_LSE><<<grid, 256, 0, st>>>(p);
+      else k_fg_timed_bwd_direct<M_SOFT><<<grid, 256, 0, st>>>(p);
+    }
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return launch_pointwise_vjp(mode, p, p.gbuf, st);
@@ -936,11 +1022,11 @@ cudaError_t launch_fg_timed_bwd(int mode, FGParams& p, cudaStream_t st) {
   p.Kp = odd_stride(p.K);
   const int ek = expr_kind(p.child);
   if (mode == M_HARD) {
-    // U, PV, PI over NB+1 blocks + GT over NB blocks + J accumulators
-    int nb = pick_nb(p.K, 5);
+    // U, PV, PI over NB+1 blocks + GT over NB blocks + 2 x J accumulators
+    int nb = pick_nb(p.K, 6);
     if (nb > 254) nb = 254;
     p.NB = nb;
-    size_t smem = (size_t)3 * (nb + 1) * p.Kp * 4 + (size_t)nb * p.Kp * 4 + (size_t)(nb - 1) * p.K * 4;
+    size_t smem = (size_t)3 * (nb + 1) * p.Kp * 4 + (size_t)nb * p.Kp * 4 + (size_t)2 * (nb - 1) * p.K * 4;
     long long J = (long long)(nb - 1) * p.K;
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
     DISPATCH_EK(ek, e = (bwd_hard_v2<EK>(p, smem, grid, st)))

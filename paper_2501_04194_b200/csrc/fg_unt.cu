@@ -383,8 +383,14 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_hard(const __
     float gk[RG_EPT];
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k) {
-      key[k] = (i0 + k < nt) ? __float_as_int(rcomb<RK_HARDI>(S[k], cin, 0.f).s) : -1;
+      const RSt o = rcomb<RK_HARDI>(S[k], cin, 0.f);
+      key[k] = (i0 + k < nt) ? __float_as_int(o.s) : -1;
       gk[k] = G[q0 + k];
+      if (p.fill) {  // masked_fill: the t sentinel rows of the column win ties (no gradient)
+        float M = o.m, l0 = 0.f;
+        const int t = c0 + i0 + k;
+        if (!fill_merge<M_HARD>(M, l0, (float)t, p.sent, t > 0, 0.f, 0.f)) gk[k] = 0.f;
+      }
     }
     if (!LB) mseq = rcomb<RK_HARDI>(mtile, mseq, 0.f);
     // the thread's run state over its chunk, then the segmented scan over later threads
@@ -522,7 +528,8 @@ bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
 
 // register-blocked untimed backward, LSE and hard (no masked_fill); false: not handled
 bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
-  if (p.fill || (mode != M_LSE && mode != M_HARD) || p.L >= (1LL << 30)) return false;
+  // masked_fill: hard only (a sentinel winning the column just zeroes that output's cotangent)
+  if ((p.fill && mode != M_HARD) || (mode != M_LSE && mode != M_HARD) || p.L >= (1LL << 30)) return false;
   const int ek = expr_kind(p.child);
   if (unt_use_lb(p)) {
     using C = RC<UN_LB>;

@@ -78,3 +78,44 @@ def test_lookback_shape_bitwise_reproducible(cuda, name, f, mode):
     for other in runs[1:]:
         for a, b in zip(runs[0], other):
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), name
+
+
+MORE = [
+    ("F_timed_hard_K9", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(2, 10)), P.SemanticsConfig()),
+    ("G_timed_hard_K3", P.Always(P.Pred("x", ">", 0.0), P.StepInterval(0, 2)), P.SemanticsConfig()),
+    ("F_smooth_lse_last", P.Eventually(P.Pred("x", ">", 0.0), SI),
+     P.SemanticsConfig(mode=P.LogSumExp(5.0), padding=P.PaddingPolicy.last_value())),
+    ("F_timed_hard_fill", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(1, 30)),
+     P.SemanticsConfig(masked_fill=True, sentinel=4.0)),
+    ("G_untimed_hard_fill", P.Always(P.Pred("x", ">", 0.0)), P.SemanticsConfig(masked_fill=True, sentinel=4.0)),
+    ("F_timed_lse_fill", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(1, 30)),
+     P.SemanticsConfig(mode=P.LogSumExp(3.0), masked_fill=True, sentinel=4.0)),
+    ("F_timed_hard_fill_K2", P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 1)),
+     P.SemanticsConfig(masked_fill=True, sentinel=4.0, padding=P.PaddingPolicy.last_value())),
+    ("G_timed_lse_fill_K3", P.Always(P.Pred("x", ">", 0.0), P.StepInterval(1, 3)),
+     P.SemanticsConfig(mode=P.LogSumExp(3.0), masked_fill=True, sentinel=4.0)),
+]
+
+
+@pytest.mark.parametrize("name,f,cfg", MORE, ids=[c[0] for c in MORE])
+def test_more_paths_bitwise_reproducible(cuda, name, f, cfg):
+    """Short windows (register-blocked K <= 16 kernels), 'last' padding of a smooth
+    interval, and masked_fill: same bits on every run under a random cotangent."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(11)
+    B, T = 64, 1500
+    x = torch.round(torch.randn(B, T, device="cuda", generator=g) * 2)
+    cot = torch.randn(B, T, device="cuda", generator=g)
+    runs = []
+    for _ in range(3):
+        xs = x.clone().requires_grad_(True)
+        smooth = "smooth" in name
+        abc = tuple(torch.tensor(v, dtype=torch.float64, device="cuda", requires_grad=True)
+                    for v in (SI.a, SI.b, SI.c)) if smooth else None
+        out = P.trace(f, {"x": xs}, cfg, smooth_binding=abc)
+        leaves = [xs] + (list(abc) if abc else [])
+        grads = torch.autograd.grad(out, leaves, cot)
+        runs.append([np.atleast_1d(t.detach().cpu().numpy()) for t in (out, *grads)])
+    for other in runs[1:]:
+        for a, b in zip(runs[0], other):
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), name

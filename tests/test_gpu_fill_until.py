@@ -137,3 +137,30 @@ def test_untimed_lse_until_wide_range_rows(cuda):
     assert rel_err(tr, ref_tr) <= 1e-5
     for k in ("x", "y"):
         assert rel_err(g[k], ref_g[k]) <= 1e-5, k
+
+
+@pytest.mark.parametrize("mode", ["hard", "lse", "soft"])
+@pytest.mark.parametrize("iv", [(0, 0), (0, 1), (1, 3), (4, 5)], ids=["a0b0", "a0b1", "a1b3", "a4b5"])
+@pytest.mark.parametrize("pad", ["last", "const"])
+@pytest.mark.parametrize("fill", [False, True], ids=["plain", "fill"])
+def test_short_window_gather_backward_vs_oracle(cuda, mode, iv, pad, fill):
+    """Windows of K < 4 samples that miss the register-blocked kernels (masked_fill) run
+    the gather-form backward (fg.cu k_fg_timed_bwd_gather): tie-heavy values, a random
+    cotangent, both paddings, L-1 collecting the padded samples."""
+    P = cuda
+    orc = _oracle()
+    rng = np.random.default_rng(zlib.crc32(repr((mode, iv, pad, fill)).encode()))
+    L = 77
+    x = np.round(rng.normal(0, 1.5, (3, L)) * 2) / 2
+    m = {"hard": P.Hard(), "lse": P.LogSumExp(2.0), "soft": P.SoftMax(2.0)}[mode]
+    padding = P.PaddingPolicy.last_value() if pad == "last" else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(mode=m, padding=padding, masked_fill=fill, sentinel=4.0)
+    f = P.Eventually(P.Pred("x", ">", 0.25), P.StepInterval(*iv))
+    cot = rng.normal(0, 1, (3, L))
+    tr, g, _ = run_device(f, {"x": x}, cfg, cot=cot)
+    ref_tr, ref_g, _ = orc.trace_and_grad(f, {"x": x}, cfg, cot)
+    if mode == "hard":
+        assert_hard_equal(tr, np.asarray(ref_tr, dtype=np.float32))
+    else:
+        assert rel_err(tr, ref_tr) <= 1e-5
+    assert rel_err(g["x"], ref_g["x"]) <= 1e-5

@@ -965,12 +965,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// tile frame F = max over [t0, L) of -tau2 l and -tau2 r; false: take the per-pair path
-__device__ __forceinline__ bool ul_frame(const UParams& p, long long row, long long t0, float& F, float* red) {
+// tile frame F = max over [t0, kend) of -tau2 l and -tau2 r (kend = L untimed, the last
+// window end of the tile timed); false: take the per-pair path
+__device__ __forceinline__ bool ul_frame(const UParams& p, long long row, long long t0, long long kend, float& F,
+                                         float* red) {
   const float tau2 = p.mp.tau2;
   float hi = -INFINITY, lo = INFINITY;
   bool ok = true;
-  for (long long k = t0 + threadIdx.x; k < p.L; k += UL_T) {
+  for (long long k = t0 + threadIdx.x; k < kend; k += UL_T) {
     const float u = -tau2 * expr_eval<M_LSE>(p.left, row, k, p.mp);
     const float v = -tau2 * expr_eval<M_LSE>(p.right, row, k, p.mp);
     ok = ok && isfinite(u) && isfinite(v);
@@ -1052,19 +1054,49 @@ __device__ __forceinline__ double ul_chunk_fwd(const UlStage& S, int c, int n, d
   return (double)(s0 + s1) * pow2d(g);
 }
 
-__global__ void __launch_bounds__(UL_T) k_until_unt_lse_fwd(const __grid_constant__ UParams p) {
+// the same sum over the chunk columns [jlo, jhi) only (timed windows cut chunks)
+__device__ __forceinline__ double ul_chunk_fwd_rng(const UlStage& S, int c, int jlo, int jhi, double base) {
+  const double den = base + S.bmin[c];
+  const int g = -ilogb_d(den);
+  const float scale = pow2f(S.fmin[c] + g);
+  const float bb = (float)(base * pow2d(g));
+  const float* bk = S.bk + c * UL_C;
+  float s0 = 0.f;
+  for (int j = jlo; j < jhi; ++j) s0 += rcp_approx(fmaf(bk[j], scale, bb));
+  return (double)s0 * pow2d(g);
+}
+
+// overrun output (t + b > L-1, timed): the hard min of the pad values in every mode
+// (masking.py:180-192); its gradient source: left if pl <= pr
+__device__ __forceinline__ void ul_pads(const UParams& p, long long row, float& pl, float& pr) {
+  pl = p.pad_value;
+  pr = p.pad_value;
+  if (p.pad_last) {
+    pl = expr_eval<M_LSE>(p.left, row, p.L - 1, p.mp);
+    pr = expr_eval<M_LSE>(p.right, row, p.L - 1, p.mp);
+  }
+}
+
+// Reciprocal form, untimed (every column k >= t) or timed (columns [t + a, t + b]; the pm
+// sum still starts at t, so base accumulates every column from t on).
+template <bool TIMED>
+__global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constant__ UParams p) {
   __shared__ UlStage S;
   __shared__ float red[8];
   const long long row = blockIdx.y, t0 = (long long)blockIdx.x * UL_T;
+  const long long L = p.L;
+  const long long kend = TIMED ? min(L, t0 + UL_T - 1 + p.b + 1) : L;  // columns the tile reads
   float F;
-  if (!ul_frame(p, row, t0, F, red)) {
+  if (!ul_frame(p, row, t0, kend, F, red)) {
     until_fwd_tile<M_LSE, false>(p, row, t0, nullptr);
     return;
   }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const long long L = p.L, t = t0 + tid;
+  const long long t = t0 + tid;
+  const bool live = !TIMED || t + p.b <= L - 1;
+  const long long u = TIMED ? t + p.a : t, v = TIMED ? (live ? t + p.b : -1) : L - 1;  // columns
   double A = 0.0, base = 0.0;
-  for (long long k0 = t0; k0 < L; k0 += UL_T) {
+  for (long long k0 = t0; k0 < kend; k0 += UL_T) {
     __syncthreads();
     ul_stage<false>(p, row, k0, F, S);
     __syncthreads();
@@ -1072,22 +1104,38 @@ __global__ void __launch_bounds__(UL_T) k_until_unt_lse_fwd(const __grid_constan
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       const long long c0 = k0 + c * UL_C;
-      if (c0 >= L) break;
+      if (c0 >= kend) break;
       const int n = (int)min((long long)UL_C, L - c0);
       if (diag && c == w) {  // the thread's own chunk, exactly
         double s = 0.0;
         for (int j = lane; j < n; ++j) {
           s += S.ex[c * UL_C + j];
-          A += 1.0 / (s + S.E[c * UL_C + j]);
+          const long long col = c0 + j;
+          if (!TIMED || (col >= u && col <= v)) A += 1.0 / (s + S.E[c * UL_C + j]);
         }
         base = s;
       } else if (!diag || c > w) {
-        A += ul_chunk_fwd(S, c, n, base);
+        if (!TIMED) {
+          A += ul_chunk_fwd(S, c, n, base);
+        } else if (c0 <= v && c0 + n > u) {
+          const int jlo = (int)max(0LL, u - c0), jhi = (int)min((long long)n, v - c0 + 1);
+          A += (jlo == 0 && jhi == n) ? ul_chunk_fwd(S, c, n, base) : ul_chunk_fwd_rng(S, c, jlo, jhi, base);
+        }
         base += S.qtot[c];
       }
     }
   }
-  if (t < L) p.out[row * L + t] = (float)((log2(A) - (double)F) / (double)p.mp.tau2);
+  if (t < L) {
+    float o;
+    if (live) {
+      o = (float)((log2(A) - (double)F) / (double)p.mp.tau2);
+    } else {
+      float pl, pr;
+      ul_pads(p, row, pl, pr);
+      o = (pl <= pr) ? pl : pr;
+    }
+    p.out[row * L + t] = p.canon ? __fadd_rn(o, 0.f) : o;
+  }
 }
 
 // 32 values per lane -> lane i holds the warp's sum of value i
@@ -1194,7 +1242,7 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
     const float gt = t < L ? p.cot[row * L + t] : 0.f;
     if (!__syncthreads_or(gt != 0.f)) continue;
     float F;
-    if (!ul_frame(p, row, t0, F, red)) {
+    if (!ul_frame(p, row, t0, L, F, red)) {
       until_bwd_tile<M_LSE, false, U_CB_G>(p, row, t0, nullptr, scr);
       __syncthreads();
       continue;
@@ -1341,6 +1389,12 @@ static int until_sm_count() {
   return n;
 }
 
+// timed LSE Until forward in reciprocal form: windows long enough that one rcp per pair
+// beats the incremental per-pair ex2 / lg2.  (A timed reciprocal backward measured slower
+// than the per-output one — 40.1 vs 33.9 ms at C5 U[0,100]: the own-chunk exact fp64 pass
+// and the window-masked chunk columns dominate at K = 101 — so the backward stays there.)
+static bool ul_timed(const UParams& p) { return !p.untimed && !p.fill && p.K >= 16 && p.L < (1LL << 30); }
+
 size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K) {
   UParams p;
   memset(&p, 0, sizeof(p));
@@ -1438,8 +1492,9 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((p.L + U_THREADS - 1) / U_THREADS), (unsigned)p.B);
-  if (MODE == M_LSE && p.untimed && !p.fill) {
-    k_until_unt_lse_fwd<<<grid, UL_T, 0, st>>>(p);
+  if (MODE == M_LSE && !p.fill && (p.untimed || ul_timed(p))) {
+    if (p.untimed) k_until_rcp_lse_fwd<false><<<grid, UL_T, 0, st>>>(p);
+    else k_until_rcp_lse_fwd<true><<<grid, UL_T, 0, st>>>(p);
     count_launch();
     return cudaGetLastError();
   }

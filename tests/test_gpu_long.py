@@ -290,3 +290,26 @@ def test_untimed_sequential_shape_large_batch(cuda, case):
             assert_hard_equal(tr[r:r + 1], ref.astype(np.float32))
             assert rel_err(g["x"][r:r + 1], dl) <= 1e-6
             assert rel_err(g["y"][r:r + 1], dr) <= 1e-6
+
+
+@pytest.mark.parametrize("pad", ["last", "const"])
+@pytest.mark.parametrize("a,K,L", [(0, 16, 300), (0, 101, 1500), (3, 20, 700), (17, 101, 2500),
+                                   (2, 300, 1100), (70, 129, 3000), (0, 600, 700), (5, 40, 30)])
+def test_lse_timed_until_reciprocal_sweep(cuda, a, K, L, pad):
+    """Timed LSE Until forward in reciprocal form (until.cu k_until_rcp_lse_fwd<true>,
+    K >= 16): one rcp per (t, s) pair over the window [t + a, t + b], the pm sum from t;
+    overrun outputs, both paddings, a-prefixes, windows longer than the 128-output tile
+    and than the row; values and gradients vs the oracle at 1e-5 under a random cotangent."""
+    rng = np.random.default_rng(a * 7919 + K * 31 + L + (pad == "last"))
+    x = np.asarray(rng.normal(0, 1, (2, L)), dtype=np.float32)
+    y = np.asarray(rng.normal(0, 1, (2, L)), dtype=np.float32)
+    f = P.Until(P.Pred("x", ">", 0.0), P.Pred("y", "<", 0.5), P.StepInterval(a, a + K - 1))
+    padding = P.PaddingPolicy.last_value() if pad == "last" else P.PaddingPolicy.constant(-0.75)
+    cfg = P.SemanticsConfig(mode=P.LogSumExp(3.0), padding=padding)
+    cot = np.asarray(rng.normal(0, 1, (2, L)), dtype=np.float32)
+    tr, g = _run(f, {"x": x, "y": y}, cfg, cot)
+    arrays = {"x": x.astype(np.float64), "y": y.astype(np.float64)}
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, arrays, cfg, cot.astype(np.float64))
+    assert rel_err(tr, ref_tr) <= TOL
+    for k in ("x", "y"):
+        assert rel_err(g[k], ref_g[k]) <= TOL, k

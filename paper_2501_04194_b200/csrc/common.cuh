@@ -360,6 +360,92 @@ __device__ __forceinline__ void expr_vjp_n(const DExpr& e, long long b, long lon
   }
 }
 
+// Row-hoisted N-step expressions for the pointwise kernels: every leaf step's source /
+// gradient row base and its transform are resolved once per row (expressions whose
+// leaves are constants, traces or affine predicates over unit-stride planes — the host
+// checks, pw_unit), so a sample costs one load per leaf instead of the descriptor walk and
+// 64-bit address arithmetic of leaf_val (the transforms stay in the parameter bank).
+template <int N>
+struct RowLeaves {
+  const float* src[N];  // leaf steps: row base of the source (null: constant / not a leaf)
+  float* dst[N];        // leaf steps: row base of the gradient destination (or null)
+  __device__ __forceinline__ RowLeaves(const DExpr& e, long long row, bool want_dst) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      src[k] = nullptr;
+      dst[k] = nullptr;
+      const DStep sp = e.step[k];
+      if (sp.op != ST_LEAF) continue;
+      const DLeaf& L = e.leaf[sp.a];
+      if (L.kind == LEAF_CONST) continue;
+      src[k] = e.src[L.src].p + row * e.src[L.src].rs;
+      if (want_dst && e.dst[L.src].p) dst[k] = e.dst[L.src].p + row * e.dst[L.src].rs;
+    }
+  }
+  __device__ __forceinline__ float value(const DLeaf& L, int k, int j) const {
+    if (L.kind == LEAF_CONST) return L.c;
+    const float x = __ldg(src[k] + j);
+    return L.kind == LEAF_SRC ? L.s_out * x : L.s_out * __fadd_rn(L.s_in * x, L.c);
+  }
+  __device__ __forceinline__ void grad(const DLeaf& L, int k, int j, float g) const {
+    if (dst[k] == nullptr) return;
+    const float v = L.kind == LEAF_SRC ? g * L.s_out : g * L.s_out * L.s_in;
+    if (L.st1) dst[k][j] = v;
+    else dst[k][j] += v;
+  }
+};
+
+template <int MODE, int N>
+__device__ __forceinline__ float expr_eval_rn(const DExpr& e, const RowLeaves<N>& R, int j, const ModeP& mp) {
+  float v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const DStep s = e.step[k];
+    if (s.op == ST_LEAF) {
+      v[k] = R.value(e.leaf[s.a], k, j);
+    } else {
+      float p1, p2;
+      v[k] = pair_red<MODE>(pick_n<N>(v, s.a, k), pick_n<N>(v, s.b, k), s.op == ST_MAX ? 1.f : -1.f, mp, p1, p2);
+    }
+  }
+  return v[N - 1];
+}
+
+template <int MODE, int N>
+__device__ __forceinline__ void expr_vjp_rn(const DExpr& e, const RowLeaves<N>& R, int j, float g, const ModeP& mp) {
+  float v[N], w1[N], w2[N], adj[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const DStep s = e.step[k];
+    adj[k] = 0.f;
+    w1[k] = w2[k] = 0.f;
+    if (s.op == ST_LEAF) {
+      v[k] = R.value(e.leaf[s.a], k, j);
+    } else {
+      v[k] = pair_red<MODE>(pick_n<N>(v, s.a, k), pick_n<N>(v, s.b, k), s.op == ST_MAX ? 1.f : -1.f, mp,
+                            w1[k], w2[k]);
+    }
+  }
+  adj[N - 1] = g;
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) {
+    const DStep s = e.step[k];
+    const float a = adj[k];
+    if (s.op == ST_LEAF) {
+      const DLeaf& L = e.leaf[s.a];
+      if (a != 0.f || L.st1) R.grad(L, k, j, a);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (i < k) {
+          adj[i] += (s.a == i) ? a * w1[k] : 0.f;
+          adj[i] += (s.b == i) ? a * w2[k] : 0.f;
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // monoid states for window reductions (all in "max space": u = sg * v)
 // ---------------------------------------------------------------------------

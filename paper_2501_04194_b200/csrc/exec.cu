@@ -88,6 +88,10 @@ namespace {
 // --------------------------------------------------------------------------
 // compiler
 // --------------------------------------------------------------------------
+// an And / Or operand heavier than this many leaves becomes its own pointwise entry
+// (2 measured slower on the paper's phi formulas than 7: more passes over memory)
+constexpr int PW_MAX_W = 7;
+
 struct Compiler {
   const stlg_node* nodes;
   int n;
@@ -108,6 +112,12 @@ struct Compiler {
     else w = 1;
     weight_[i] = w;
     return w;
+  }
+
+  // an elementwise sub-formula with at least one And / Or (through any Nots)
+  bool compound(int i) {
+    while (nodes[i].op == STLG_NOT && slot_of[i] < 0) i = nodes[i].left;
+    return slot_of[i] < 0 && (nodes[i].op == STLG_AND || nodes[i].op == STLG_OR);
   }
 
   // Materialise an elementwise sub-formula into its own slot (pointwise entry).
@@ -162,8 +172,8 @@ struct Compiler {
         bool is_min = (nd.op == STLG_AND) == (sign > 0);
         int ka, kb;
         int l = nd.left, r = nd.right;
-        if (is_elementwise(nodes[l].op) && slot_of[l] < 0 && weight(l) > 7) materialise(l);
-        if (is_elementwise(nodes[r].op) && slot_of[r] < 0 && weight(r) > 7) materialise(r);
+        if (is_elementwise(nodes[l].op) && slot_of[l] < 0 && weight(l) > PW_MAX_W) materialise(l);
+        if (is_elementwise(nodes[r].op) && slot_of[r] < 0 && weight(r) > PW_MAX_W) materialise(r);
         ka = build(l, sign, ex);
         kb = build(r, sign, ex);
         DStep s{(unsigned char)(is_min ? ST_MIN : ST_MAX), (unsigned char)ka, (unsigned char)kb, 0};
@@ -456,6 +466,12 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     } else {
       e.kind = e.untimed ? E_FG_UNTIMED : E_FG_TIMED;
     }
+    // a compound child (an And / Or of predicates) runs as its own register-resident
+    // pointwise entry: the window / Until kernels then read a materialised trace through
+    // their single-leaf fast paths instead of interpreting the expression per staged
+    // sample (the generic interpreter's step array lives in local memory)
+    if (C.compound(nd.left)) C.materialise(nd.left);
+    if (nd.op == STLG_UNTIL && C.compound(nd.right)) C.materialise(nd.right);
     C.build(nd.left, 1.f, e.e1);
     if (nd.op == STLG_UNTIL) C.build(nd.right, 1.f, e.e2);
     if (!C.fits(e.e1) || (nd.op == STLG_UNTIL && !C.fits(e.e2))) {

@@ -49,31 +49,63 @@ __device__ __forceinline__ void pw_vjp(const DExpr& e, long long row, int t, flo
   else expr_vjp<MODE>(e, row, t, g, mp);
 }
 
-template <int MODE, int NS>
+// UNIT: every leaf is a constant, trace or affine predicate over unit-stride planes
+// (pw_unit): the leaves are resolved once per row (RowLeaves)
+template <int MODE, int NS, bool UNIT>
 __global__ void __launch_bounds__(PW_T) k_pointwise_fwd(const __grid_constant__ FGParams p) {
   const int L = (int)p.L;
   for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
     float* out = p.out + row * L;
+    if constexpr (UNIT && NS > 0) {
+      const RowLeaves<NS> R(p.child, row, false);
 #pragma unroll
-    for (int e = 0; e < PW_E; ++e) {
-      const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
-      if (t < L) out[t] = pw_eval<MODE, NS>(p.child, row, t, p.mp);
+      for (int e = 0; e < PW_E; ++e) {
+        const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+        if (t < L) out[t] = expr_eval_rn<MODE, NS>(p.child, R, t, p.mp);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < PW_E; ++e) {
+        const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+        if (t < L) out[t] = pw_eval<MODE, NS>(p.child, row, t, p.mp);
+      }
     }
   }
 }
 
-template <int MODE, int NS>
+template <int MODE, int NS, bool UNIT>
 __global__ void __launch_bounds__(PW_T) k_pointwise_vjp(const __grid_constant__ FGParams p,
                                                        const float* __restrict__ g) {
   const int L = (int)p.L;
   for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
     const float* gr = g + row * L;
+    if constexpr (UNIT && NS > 0) {
+      const RowLeaves<NS> R(p.child, row, true);
 #pragma unroll
-    for (int e = 0; e < PW_E; ++e) {
-      const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
-      if (t < L) pw_vjp<MODE, NS>(p.child, row, t, gr[t], p.mp);
+      for (int e = 0; e < PW_E; ++e) {
+        const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+        if (t < L) expr_vjp_rn<MODE, NS>(p.child, R, t, gr[t], p.mp);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < PW_E; ++e) {
+        const int t = blockIdx.x * PW_N + e * PW_T + threadIdx.x;
+        if (t < L) pw_vjp<MODE, NS>(p.child, row, t, gr[t], p.mp);
+      }
     }
   }
+}
+
+// host: every leaf a constant / trace / affine predicate with unit element strides
+static bool pw_unit(const DExpr& e) {
+  for (int i = 0; i < e.n_leaf; ++i) {
+    const DLeaf& L = e.leaf[i];
+    if (L.kind == LEAF_CONST) continue;
+    if (L.kind != LEAF_SRC && L.kind != LEAF_AFFINE) return false;
+    if (e.src[L.src].es != 1) return false;
+    if (e.dst[L.src].p != nullptr && e.dst[L.src].es != 1) return false;
+  }
+  return true;
 }
 
 // Binary root over two trace / affine leaves (And / Or of two sub-formulas — the usual
@@ -209,10 +241,17 @@ cudaError_t launch_pointwise_fwd(int mode, const FGParams& p, cudaStream_t st) {
     count_launch();
     return cudaGetLastError();
   }
-  PW_DISPATCH(p.child.n_step,
-              if (mode == M_HARD) k_pointwise_fwd<M_HARD, NS><<<grid, PW_T, 0, st>>>(p);
-              else if (mode == M_LSE) k_pointwise_fwd<M_LSE, NS><<<grid, PW_T, 0, st>>>(p);
-              else k_pointwise_fwd<M_SOFT, NS><<<grid, PW_T, 0, st>>>(p))
+  if (pw_unit(p.child)) {
+    PW_DISPATCH(p.child.n_step,
+                if (mode == M_HARD) k_pointwise_fwd<M_HARD, NS, true><<<grid, PW_T, 0, st>>>(p);
+                else if (mode == M_LSE) k_pointwise_fwd<M_LSE, NS, true><<<grid, PW_T, 0, st>>>(p);
+                else k_pointwise_fwd<M_SOFT, NS, true><<<grid, PW_T, 0, st>>>(p))
+  } else {
+    PW_DISPATCH(p.child.n_step,
+                if (mode == M_HARD) k_pointwise_fwd<M_HARD, NS, false><<<grid, PW_T, 0, st>>>(p);
+                else if (mode == M_LSE) k_pointwise_fwd<M_LSE, NS, false><<<grid, PW_T, 0, st>>>(p);
+                else k_pointwise_fwd<M_SOFT, NS, false><<<grid, PW_T, 0, st>>>(p))
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -226,10 +265,17 @@ cudaError_t launch_pointwise_vjp(int mode, const FGParams& p, const float* g, cu
     count_launch();
     return cudaGetLastError();
   }
-  PW_DISPATCH(p.child.n_step,
-              if (mode == M_HARD) k_pointwise_vjp<M_HARD, NS><<<grid, PW_T, 0, st>>>(p, g);
-              else if (mode == M_LSE) k_pointwise_vjp<M_LSE, NS><<<grid, PW_T, 0, st>>>(p, g);
-              else k_pointwise_vjp<M_SOFT, NS><<<grid, PW_T, 0, st>>>(p, g))
+  if (pw_unit(p.child)) {
+    PW_DISPATCH(p.child.n_step,
+                if (mode == M_HARD) k_pointwise_vjp<M_HARD, NS, true><<<grid, PW_T, 0, st>>>(p, g);
+                else if (mode == M_LSE) k_pointwise_vjp<M_LSE, NS, true><<<grid, PW_T, 0, st>>>(p, g);
+                else k_pointwise_vjp<M_SOFT, NS, true><<<grid, PW_T, 0, st>>>(p, g))
+  } else {
+    PW_DISPATCH(p.child.n_step,
+                if (mode == M_HARD) k_pointwise_vjp<M_HARD, NS, false><<<grid, PW_T, 0, st>>>(p, g);
+                else if (mode == M_LSE) k_pointwise_vjp<M_LSE, NS, false><<<grid, PW_T, 0, st>>>(p, g);
+                else k_pointwise_vjp<M_SOFT, NS, false><<<grid, PW_T, 0, st>>>(p, g))
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -256,6 +256,17 @@ __device__ __forceinline__ int ht_source(const UParams& p, int base, int t, cons
   return V.yi;
 }
 
+// 64-bit integer add into shared memory from two native 32-bit atomics (a 64-bit shared
+// atomicAdd compiles to a CAS spin loop): the low word's carry-out is exact per add, so
+// the pair holds the exact sum mod 2^64 for any order of arrival
+__device__ __forceinline__ void ht_add64(unsigned long long* a, unsigned long long v) {
+  unsigned* w = reinterpret_cast<unsigned*>(a);  // little endian: w[0] low, w[1] high
+  const unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
+  const unsigned old = atomicAdd(w, lo);
+  const unsigned carry = (old + lo < old) ? 1u : 0u;
+  if (hi + carry != 0u) atomicAdd(w + 1, hi + carry);
+}
+
 __global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant__ UParams p) {
   extern __shared__ __align__(16) float htsm[];
   const long long row = blockIdx.y;
@@ -333,7 +344,7 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
       const int j = (d & (HT_R - 1)) - t0;
       if (j < 0 || j >= NT) return;
       const long long q = llrint((double)g * scale);
-      atomicAdd((d & HT_R) ? &accR[j] : &accL[j], (unsigned long long)q);
+      ht_add64((d & HT_R) ? &accR[j] : &accL[j], (unsigned long long)q);
     };
     if (regs) {
 #pragma unroll

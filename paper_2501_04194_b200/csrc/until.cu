@@ -284,35 +284,50 @@ __global__ void __launch_bounds__(U_THREADS) k_until_fwd_g(const __grid_constant
 // ---------------------------------------------------------------------------
 struct Systolic {
   float acc;
-  long long cur;  // element currently accumulated by this lane (-1 none)
+  long long cur;   // element currently accumulated by this lane (-1 none)
+  float pacc;      // the previous element's finished total, not yet written
+  long long pcur;  // (-1 none)
   __device__ __forceinline__ void reset() {
     acc = 0.f;
     cur = -1;
+    pacc = 0.f;
+    pcur = -1;
   }
-  // called by all 32 lanes with the same k (warp-uniform); dst = row base pointer
+  // called by all 32 lanes with the same k (warp-uniform); dst = row base pointer.  A
+  // lane's element changes once per 32 consecutive k (at k = lane + 1 mod 32 descending,
+  // k = lane ascending): the finished total waits in (pcur, pacc) and every lane writes
+  // at once when k = 0 mod 32 — uniform, instead of one diverged lane per step
   __device__ __forceinline__ void step(float val, long long base, int k, const DetRow& dst, long long L) {
     const int lane = threadIdx.x & 31;
     int src = (lane - k) & 31;
     float got = __shfl_sync(0xffffffffu, val, src);
     long long j = base + k + ((lane - k) & 31);
     if (j != cur) {
-      put(dst, L);
+      pcur = cur;
+      pacc = acc;
       cur = j;
       acc = 0.f;
     }
     acc += got;
+    if ((k & 31) == 0) put_pending(dst, L);
   }
   // padded positions (masked_fill windows past the end) feed element L - 1 under
   // 'last' padding (pad_last is set by the caller) and nothing under a constant pad
   int pad_last = 0;
-  __device__ __forceinline__ void put(const DetRow& dst, long long L) {
-    if (cur >= 0 && acc != 0.f) {
-      if (cur < L) dst.add(cur, acc);
-      else if (pad_last) dst.add(L - 1, acc);
+  __device__ __forceinline__ void put1(long long e, float v, const DetRow& dst, long long L) const {
+    if (e >= 0 && v != 0.f) {
+      if (e < L) dst.add(e, v);
+      else if (pad_last) dst.add(L - 1, v);
     }
   }
+  __device__ __forceinline__ void put_pending(const DetRow& dst, long long L) {
+    put1(pcur, pacc, dst, L);
+    pcur = -1;
+    pacc = 0.f;
+  }
   __device__ __forceinline__ void flush(const DetRow& dst, long long L) {
-    put(dst, L);
+    put_pending(dst, L);
+    put1(cur, acc, dst, L);
     reset();
   }
 };

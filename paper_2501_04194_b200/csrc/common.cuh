@@ -165,7 +165,7 @@ __device__ __forceinline__ float pair_red(float l, float r, float sg, const Mode
   float e1 = ex2f(mp.tau2 * (u1 - m));
   float e2 = ex2f(mp.tau2 * (u2 - m));
   float s = e1 + e2;
-  float inv = 1.f / s;
+  float inv = __frcp_rn(s);  // s in [1, 2]: the correctly rounded reciprocal, = 1.f / s
   if (MODE == M_LSE) {
     p1 = e1 * inv;
     p2 = e2 * inv;

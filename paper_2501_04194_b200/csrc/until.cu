@@ -1153,6 +1153,129 @@ __global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constan
   }
 }
 
+// Timed LSE Until backward in reciprocal form, one thread per output t (the per-output
+// kernels' structure, the reciprocal form's arithmetic): with ex_j = e^{-tau l_j},
+// E_s = e^{-tau r_s} staged in fp64 under the tile frame and D_s = sum_{j=t..s} ex_j + E_s,
+//   A = sum_{s in [u, v]} 1 / D_s,   d out / d r_s = E_s D_s^-2 / A,
+//   d out / d l_j = ex_j sum_{s >= max(j, u)} D_s^-2 / A,
+// pass 1 accumulates S and A ascending with a checkpoint of S every UR_CB columns, pass 2
+// walks the blocks descending (q = 1/D recomputed from the checkpoint into QB), and the
+// contributions scatter warp-systolically into the reproducible int64 accumulators.
+// Tiles whose values span more than UL_RANGE log2 units run the per-pair tile function
+// (global-slab checkpoints; the grid is persistent for that slab).
+constexpr int UR_CB = 32;
+__host__ __device__ __forceinline__ int ur_span(int b) { return U_THREADS + b; }
+static size_t ur_smem(const UParams& p) {
+  const size_t qb = (size_t)UR_CB * U_THREADS * 8;  // also the fallback's block buffer
+  const size_t st = (size_t)2 * ur_span(p.b) * 8;
+  const size_t ck = (size_t)((p.K + UR_CB - 1) / UR_CB) * U_THREADS * 8;
+  return qb + st + ck;
+}
+
+__global__ void __launch_bounds__(U_THREADS) k_until_rcp_lse_bwd_timed(const __grid_constant__ UParams p, int ntx,
+                                                                      long long ntiles) {
+  extern __shared__ __align__(16) float dsm[];
+  __shared__ float red[8];
+  const long long L = p.L;
+  const int K = p.K, tid = threadIdx.x, span = ur_span(p.b);
+  double* QB = reinterpret_cast<double*>(dsm);  // [UR_CB][U_THREADS]
+  double* EXs = QB + UR_CB * U_THREADS;           // [span]
+  double* ERs = EXs + span;                       // [span]
+  double* CK = ERs + span;                        // [ceil(K / UR_CB)][U_THREADS]
+  const long long stride = (long long)gridDim.x * U_THREADS;
+  UScr scr{p.scratch, dsm, stride, (long long)blockIdx.x * U_THREADS + tid, U_THREADS, tid};
+  const long long BL = p.B * L;
+  const float tau2 = p.mp.tau2;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row = tile / ntx;
+    const long long t0 = (tile - row * ntx) * U_THREADS;
+    const long long t = t0 + tid;
+    const long long kend = min(L, t0 + span);
+    float g = t < L ? p.cot[row * L + t] : 0.f;
+    if (!__syncthreads_or(g != 0.f)) continue;
+    float F;
+    if (!ul_frame(p, row, t0, kend, F, red)) {
+      until_bwd_tile<M_LSE, false, U_CB_G>(p, row, t0, nullptr, scr);
+      __syncthreads();
+      continue;
+    }
+    const DetRow gl = det_row(p.dacc, p.dacc + BL, p.dscale, row, L, false);
+    const DetRow gr = det_row(p.dacc + 2 * BL, p.dacc + 3 * BL, p.dscale, row, L, false);
+    if (t < L && t + p.b > L - 1) {  // overrun output: the whole cotangent to the pad source
+      if (p.pad_last && g != 0.f) {
+        float pl, pr;
+        ul_pads(p, row, pl, pr);
+        (pl <= pr ? gl : gr).add(L - 1, g);
+      }
+      g = 0.f;
+    }
+    for (int c = tid; c < span; c += U_THREADS) {
+      const long long j = t0 + c;
+      double ex = 0.0, E = 0.0;
+      if (j < L) {
+        ex = ex2d(fmaf(-tau2, expr_eval<M_LSE>(p.left, row, j, p.mp), -F));
+        E = ex2d(fmaf(-tau2, expr_eval<M_LSE>(p.right, row, j, p.mp), -F));
+      }
+      EXs[c] = ex;
+      ERs[c] = E;
+    }
+    __syncthreads();
+    // pass 1: A, checkpoints of S (before each block's first column)
+    double A = 0.0;
+    if (g != 0.f) {
+      double S = 0.0;
+      for (int i = 0; i < p.a; ++i) S += EXs[tid + i];
+      for (int k = 0; k < K; ++k) {
+        const int c = tid + p.a + k;
+        if (k % UR_CB == 0) CK[(k / UR_CB) * U_THREADS + tid] = S;
+        S += EXs[c];
+        A += __drcp_rn(S + ERs[c]);
+      }
+    }
+    const double cA = (g != 0.f) ? (double)g / A : 0.0;
+    // pass 2: descending blocks
+    Systolic accL, accR;
+    accL.reset();
+    accR.reset();
+    accL.pad_last = accR.pad_last = p.pad_last;
+    const long long wbase = t0 + (tid & ~31) + p.a;  // lane i, step k -> element wbase + k + i
+    double R = 0.0;
+    for (int cb = (K + UR_CB - 1) / UR_CB - 1; cb >= 0; --cb) {
+      const int k_lo = cb * UR_CB, k_hi = min(k_lo + UR_CB, K);
+      if (cA != 0.0) {
+        double S = CK[cb * U_THREADS + tid];
+        for (int k = k_lo; k < k_hi; ++k) {
+          const int c = tid + p.a + k;
+          S += EXs[c];
+          QB[(k - k_lo) * U_THREADS + tid] = __drcp_rn(S + ERs[c]);
+        }
+      }
+      for (int k = k_hi - 1; k >= k_lo; --k) {
+        float vr = 0.f, vl = 0.f;
+        if (cA != 0.0) {
+          const int c = tid + p.a + k;
+          const double q = QB[(k - k_lo) * U_THREADS + tid];
+          const double q2 = q * q;
+          R += q2;
+          vr = (float)(cA * ERs[c] * q2);
+          if (k > 0) vl = (float)(cA * EXs[c] * R);  // k = 0 (s = u) joins the a-prefix below
+        }
+        accR.step(vr, wbase, k, gr, L);
+        accL.step(vl, wbase, k, gl, L);
+      }
+    }
+    accR.flush(gr, L);
+    accL.flush(gl, L);
+    // l_j for j in [t, u]: every window column, sum_{s >= u} D_s^-2 = R
+    for (int i = 0; i <= p.a; ++i) {
+      const float vl = (cA != 0.0) ? (float)(cA * EXs[tid + i] * R) : 0.f;
+      accL.step(vl, wbase - p.a, i, gl, L);
+    }
+    accL.flush(gl, L);
+    __syncthreads();  // before the next tile's staging
+  }
+}
+
 // 32 values per lane -> lane i holds the warp's sum of value i
 // column sums of a warp's 32 x 32 block through a padded shared transpose (row
 // stride 36 floats: conflict-free 128-bit row stores and column loads); lane i
@@ -1419,7 +1542,9 @@ size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int
   p.untimed = untimed;
   p.fill = fill;
   if (mode == M_HARD) return 0;  // one source per output: no checkpoints
-  if (bwd_uses_smem(p)) return 0;
+  // the reciprocal-form timed LSE backward falls back per tile to the per-pair tile
+  // function with its checkpoints in the global slab
+  if (bwd_uses_smem(p) && !(mode == M_LSE && ul_timed(p))) return 0;
   const long long stride = (long long)until_sm_count() * U_PERSIST_PER_SM * U_THREADS;
   const long long nck = (untimed ? L : K) / U_CB_G + 1;
   return (size_t)(nck * 3) * stride * 4;
@@ -1547,7 +1672,18 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if ((e = det_begin(MODE, p, st)) != cudaSuccess) return e;
   const int ntx = (int)((p.L + U_THREADS - 1) / U_THREADS);
   const size_t ul_smem = (size_t)U_CB_G * 2 * U_THREADS * 4 + (size_t)(ntx * 4 + 4) * sizeof(double);
-  if (MODE == M_LSE && p.untimed && !p.fill && p.scratch != nullptr && ul_smem <= kUSmemMax) {
+  const size_t ur_sm = ur_smem(p);
+  if (MODE == M_LSE && ul_timed(p) && p.scratch != nullptr && ur_sm <= 100 * 1024) {
+    if ((e = set_smem_u(k_until_rcp_lse_bwd_timed, ur_sm)) != cudaSuccess) return e;
+    const long long ntiles = (long long)ntx * p.B;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_until_rcp_lse_bwd_timed, U_THREADS, ur_sm) !=
+            cudaSuccess || occ <= 0)
+      occ = 1;
+    long long grid = (long long)until_sm_count() * min(occ, U_PERSIST_PER_SM);
+    if (grid > ntiles) grid = ntiles;
+    k_until_rcp_lse_bwd_timed<<<(unsigned)grid, U_THREADS, ur_sm, st>>>(p, ntx, ntiles);
+  } else if (MODE == M_LSE && p.untimed && !p.fill && p.scratch != nullptr && ul_smem <= kUSmemMax) {
     if ((e = set_smem_u(k_until_unt_lse_bwd, ul_smem)) != cudaSuccess) return e;
     const long long ntiles = (long long)ntx * p.B;
     int occ = 0;

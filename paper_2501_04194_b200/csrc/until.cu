@@ -1165,6 +1165,13 @@ __global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constan
 // (global-slab checkpoints; the grid is persistent for that slab).
 constexpr int UR_CB = 32;
 __host__ __device__ __forceinline__ int ur_span(int b) { return U_THREADS + b; }
+// 1 / x for x in the frame's normal fp64 range: the MUFU seed plus one Newton step
+// (~2^-44 relative; the correctly rounded __drcp_rn costs a multi-step sequence)
+__device__ __forceinline__ double ur_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
 static size_t ur_smem(const UParams& p) {
   const size_t qb = (size_t)UR_CB * U_THREADS * 8;  // also the fallback's block buffer
   const size_t st = (size_t)2 * ur_span(p.b) * 8;
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(U_THREADS) k_until_rcp_lse_bwd_timed(const __g
         const int c = tid + p.a + k;
         if (k % UR_CB == 0) CK[(k / UR_CB) * U_THREADS + tid] = S;
         S += EXs[c];
-        A += __drcp_rn(S + ERs[c]);
+        A += ur_rcp(S + ERs[c]);
       }
     }
     const double cA = (g != 0.f) ? (double)g / A : 0.0;
@@ -1247,7 +1254,7 @@ __global__ void __launch_bounds__(U_THREADS) k_until_rcp_lse_bwd_timed(const __g
         for (int k = k_lo; k < k_hi; ++k) {
           const int c = tid + p.a + k;
           S += EXs[c];
-          QB[(k - k_lo) * U_THREADS + tid] = __drcp_rn(S + ERs[c]);
+          QB[(k - k_lo) * U_THREADS + tid] = ur_rcp(S + ERs[c]);
         }
       }
       for (int k = k_hi - 1; k >= k_lo; --k) {

@@ -1534,10 +1534,10 @@ static int until_sm_count() {
   return n;
 }
 
-// timed LSE Until forward in reciprocal form: windows long enough that one rcp per pair
-// beats the incremental per-pair ex2 / lg2.  (A timed reciprocal backward measured slower
-// than the per-output one — 40.1 vs 33.9 ms at C5 U[0,100]: the own-chunk exact fp64 pass
-// and the window-masked chunk columns dominate at K = 101 — so the backward stays there.)
+// timed LSE Until in reciprocal form: windows long enough that one rcp per pair beats the
+// incremental per-pair ex2 / lg2 (forward: the staged chunk kernel; backward: one thread
+// per output, k_until_rcp_lse_bwd_timed — the staged chunk form of the backward measured
+// 40.1 ms at C5 U[0,100] against 18.3 ms for the per-output one)
 static bool ul_timed(const UParams& p) { return !p.untimed && !p.fill && p.K >= 16 && p.L < (1LL << 30); }
 
 size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K) {

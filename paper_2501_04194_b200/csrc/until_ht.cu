@@ -78,26 +78,35 @@ __device__ __forceinline__ float4 hs_pack(const HS& s) {
 __device__ __forceinline__ HS hs_unpack(const float4 v) {
   return HS{v.x, v.y, __float_as_int(v.z), __float_as_int(v.w)};
 }
+// mb[bk]: the state of the MB whole blocks bk+1 .. bk+MB (MB = (K-1)/32 - 1 when >= 3):
+// a window then costs suffix + mb + at most one more whole block + prefix — O(1)
+// combines per output for any K instead of O(K/32)
 struct HTArr {
   float2* lr;
-  float4 *sf, *pf;
+  float4 *sf, *pf, *mb;
+  int MB;
   __device__ __forceinline__ HS suf(int i) const { return hs_unpack(sf[ht_pad(i)]); }
   __device__ __forceinline__ HS pre(int i) const { return hs_unpack(pf[ht_pad(i)]); }
   __device__ __forceinline__ float2 at(int i) const { return lr[ht_pad(i)]; }
 };
 
 __host__ __device__ __forceinline__ int ht_padded(int NS) { return ((NS + 31) >> 5) * 33; }
+// 32-bit words of the staged arrays: mb (nb float4), then sf / pf (float4) and lr (float2)
+__host__ __device__ __forceinline__ int ht_words(int NS) { return ((NS + 31) >> 5) * 4 + ht_padded(NS) * 10; }
 
-__device__ __forceinline__ HTArr ht_carve(float* base, int NS) {
+__device__ __forceinline__ HTArr ht_carve(float* base, int NS, int K) {
   const int NP = ht_padded(NS);
   HTArr A;
-  A.sf = reinterpret_cast<float4*>(base);
+  A.mb = reinterpret_cast<float4*>(base);
+  A.sf = A.mb + ((NS + 31) >> 5);
   A.pf = A.sf + NP;
   A.lr = reinterpret_cast<float2*>(A.pf + NP);
+  const int mb = (K - 1) / 32 - 1;
+  A.MB = mb >= 3 ? mb : 0;  // (at K ~ 100 the one combine saved per output does not pay)
   return A;
 }
 
-size_t ht_smem_bytes(int NS) { return (size_t)ht_padded(NS) * 40; }
+size_t ht_smem_bytes(int NS) { return (size_t)ht_words(NS) * 4; }
 
 // stage the children over [base, base + NS) (coalesced), then walk every 32-block
 // serially: one lane per block for the prefix states and one for the suffix states.
@@ -197,6 +206,14 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
     }
   }
   __syncthreads();
+  if (A.MB > 0) {  // the MB-block aggregates (only read where bk + MB < nb)
+    for (int bk = threadIdx.x; bk + A.MB < nb; bk += HT_T) {
+      HS s = A.pre((bk + 1) * 32 + 31);
+      for (int j = 2; j <= A.MB; ++j) s = hs_comb(s, A.pre((bk + j) * 32 + 31));
+      A.mb[bk] = hs_pack(s);
+    }
+    __syncthreads();
+  }
 }
 
 // state of the staged range [i0, i1] (inclusive, relative indices)
@@ -212,7 +229,12 @@ __device__ __forceinline__ HS ht_range(const HTArr& A, int i0, int i1, int base)
     return s;
   }
   HS s = A.suf(i0);
-  for (int bk = b0 + 1; bk < b1; ++bk) s = hs_comb(s, A.pre(bk * 32 + 31));
+  int bk = b0 + 1;
+  if (A.MB > 0 && b1 - b0 - 1 >= A.MB) {
+    s = hs_comb(s, hs_unpack(A.mb[b0]));
+    bk += A.MB;
+  }
+  for (; bk < b1; ++bk) s = hs_comb(s, A.pre(bk * 32 + 31));
   return hs_comb(s, A.pre(i1));
 }
 
@@ -273,7 +295,7 @@ __global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant_
   const int L = (int)p.L;
   const int NS = ht_ns(p.b), NT = NS - p.b;
   const int t0 = blockIdx.x * NT;
-  const HTArr A = ht_carve(htsm, NS);
+  const HTArr A = ht_carve(htsm, NS, p.K);
   ht_prepare(p, row, t0, NS, A);
   float* outr = p.out + row * L;
   const int tend = min(t0 + NT, L);
@@ -303,8 +325,8 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
   const int NS = ht_ns(2 * p.b), NT = NS - 2 * p.b;
   const int t0 = blockIdx.x * NT;
   const int base = t0 - p.b;
-  const HTArr A = ht_carve(htsm, NS);
-  unsigned long long* accL = reinterpret_cast<unsigned long long*>(htsm + ht_padded(NS) * 10);
+  const HTArr A = ht_carve(htsm, NS, p.K);
+  unsigned long long* accL = reinterpret_cast<unsigned long long*>(htsm + ht_words(NS));
   unsigned long long* accR = accL + NT;
   for (int i = threadIdx.x; i < NT; i += HT_T) accL[i] = accR[i] = 0ull;
   const float* cot = p.cot + row * L;

@@ -292,6 +292,21 @@ struct ChildEval {
   // fast kinds only (kind != 0): the load and the leaf transform apart, so a caller can
   // issue a batch of loads before the first use
   __device__ __forceinline__ float raw(long long j) const { return __ldg(p + j * es); }
+  // 32-bit index forms (rows shorter than 2^31 samples, strides below 2^31): one 32-bit
+  // multiply and a widening add per access instead of 64-bit arithmetic
+  __device__ __forceinline__ float raw(int j) const { return __ldg(p + j * (int)es); }
+  template <int MODE>
+  __device__ __forceinline__ void grad(int j, float g, const ModeP& mp) const {
+    if (kind == 0) {
+      expr_vjp<MODE>(*e, row, j, g, mp);
+      return;
+    }
+    if (gp == nullptr) return;
+    const float v = kind == 1 ? g * s_out : g * s_out * s_in;
+    float* q = gp + j * (int)ges;
+    if (gst) *q = v;
+    else *q += v;
+  }
   __device__ __forceinline__ float apply(float x) const {
     return kind == 1 ? s_out * x : s_out * __fadd_rn(s_in * x, c);
   }

@@ -674,22 +674,23 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_fwd(cons
   __shared__ float Ls[UH_T * UH_S];
   __shared__ float Rs[UH_T * UH_S];
   __shared__ Clamp cb[UH_T / 32];
-  const long long row = LB ? blockIdx.y : blockIdx.x, L = p.L;
-  const int nch = (int)((L + UH_CH - 1) / UH_CH);
+  const long long row = LB ? blockIdx.y : blockIdx.x;
+  const int L = (int)p.L;  // < 2^31 (launcher)
+  const int nch = (L + UH_CH - 1) / UH_CH;
   const int tid = threadIdx.x;
   const ChildEval cl(p.left, row), cr(p.right, row);
   unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
   float seq = -INFINITY;  // sequential shape: the value entering the current chunk
   for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
-  const long long c0 = (long long)(nch - 1 - s) * UH_CH;  // scan order: from the row end
+  const int c0 = (nch - 1 - s) * UH_CH;  // scan order: from the row end
   {  // all of the thread's loads in flight before the first store
     float lv[UH_E], rv[UH_E];
     if (cl.kind != 0 && cr.kind != 0) {
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {
-        const long long t = c0 + tid + e * UH_T;
-        const long long tc = t < L ? t : L - 1;
+        const int t = c0 + tid + e * UH_T;
+        const int tc = t < L ? t : L - 1;
         lv[e] = cl.raw(tc);
         rv[e] = cr.raw(tc);
       }
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_fwd(cons
     } else {
 #pragma unroll
       for (int e = 0; e < UH_E; ++e) {
-        const long long t = c0 + tid + e * UH_T;
+        const int t = c0 + tid + e * UH_T;
         lv[e] = t < L ? cl.value<MODE>(t, p.mp) : 0.f;
         rv[e] = t < L ? cr.value<MODE>(t, p.mp) : 0.f;
       }
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_fwd(cons
   __syncthreads();
   if (!LB) seq = Ls[0];
   for (int k = tid; k < UH_CH; k += UH_T) {
-    long long t = c0 + k;
+    const int t = c0 + k;
     if (t < L) p.out[row * L + t] = Ls[uhpos(k)];
   }
   __syncthreads();
@@ -779,8 +780,9 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
   __shared__ float Ls[UH_T * UH_S], Rs[UH_T * UH_S], Os[UH_T * UH_S], Gs[UH_T * UH_S];
   __shared__ double wsum[UH_T / 32];
   __shared__ int wflag[UH_T / 32];
-  const long long row = LB ? blockIdx.y : blockIdx.x, L = p.L;
-  const int nch = (int)((L + UH_CH - 1) / UH_CH);
+  const long long row = LB ? blockIdx.y : blockIdx.x;
+  const int L = (int)p.L;  // < 2^31 (launcher)
+  const int nch = (L + UH_CH - 1) / UH_CH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* outr = p.out_in + row * L;
   const float* cot = p.cot + row * L;
@@ -788,15 +790,15 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
   unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
   double seq = 0.0;  // sequential shape: cotangent accumulated since the last terminator
   for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
-  const long long c0 = (long long)s * UH_CH;
+  const int c0 = s * UH_CH;
   {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
     float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
     const bool fast = cl.kind != 0 && cr.kind != 0;
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      const long long t = c0 + tid + e * UH_T;
-      const long long tc = t < L ? t : L - 1;
-      const long long to = t + 1 < L ? t + 1 : L - 1;
+      const int t = c0 + tid + e * UH_T;
+      const int tc = t < L ? t : L - 1;
+      const int to = t + 1 < L ? t + 1 : L - 1;
       if (fast) {
         lv[e] = cl.raw(tc);
         rv[e] = cr.raw(tc);
@@ -806,7 +808,7 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
     }
 #pragma unroll
     for (int e = 0; e < UH_E; ++e) {
-      const long long t = c0 + tid + e * UH_T;
+      const int t = c0 + tid + e * UH_T;
       const bool in = t < L;
       if (fast) {
         lv[e] = in ? cl.apply(lv[e]) : 0.f;
@@ -834,7 +836,7 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
   int anyterm = 0;
 #pragma unroll
   for (int e = 0; e < UH_E; ++e) {
-    const long long t = c0 + tid * UH_E + e;
+    const int t = c0 + tid * UH_E + e;
     const int q = tid * UH_S + e;
     term[e] = 0;
     g[e] = 0.f;
@@ -924,7 +926,7 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
   __syncthreads();
   // coalesced child VJPs (left first: first-writer order)
   for (int k = tid; k < UH_CH; k += UH_T) {
-    const long long t = c0 + k;
+    const int t = c0 + k;
     if (t >= L) break;
     const int q = uhpos(k);
     cl.grad<MODE>(t, Ls[q], p.mp);
@@ -1627,6 +1629,7 @@ template <int MODE>
 static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
   if (MODE == M_HARD && until_ht_applicable(p)) return launch_until_ht_fwd(p, st);  // O(T), until_ht.cu
   if (p.untimed && MODE == M_HARD && !p.fill) {
+    if (p.L >= (1LL << 31)) return cudaErrorNotSupported;  // 32-bit time indices
     if (uh_use_lb(p)) {
       const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
       cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);
@@ -1660,6 +1663,7 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
 template <int MODE>
 static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if (p.untimed && MODE == M_HARD && !p.fill) {
+    if (p.L >= (1LL << 31)) return cudaErrorNotSupported;  // 32-bit time indices
     if (uh_use_lb(p)) {
       const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
       cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);

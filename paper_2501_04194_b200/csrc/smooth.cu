@@ -125,13 +125,16 @@ __global__ void __launch_bounds__(S_T) k_smooth_fwd(const __grid_constant__ SPar
           const float4* U4 = reinterpret_cast<const float4*>(U);
           const float4* W4 = reinterpret_cast<const float4*>(LW);
           float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
+          // (b of one step is a of the next: one LDS.128 of U per 16 FMAs)
+          float4 a = kb < ke ? U4[o + (kb >> 2)] : make_float4(0.f, 0.f, 0.f, 0.f);
           for (int k = kb; k < ke; k += 4) {
             const float4 w = W4[k >> 2];
-            const float4 a = U4[o + (k >> 2)], b = U4[o + (k >> 2) + 1];
+            const float4 b = U4[o + (k >> 2) + 1];
             r0 = fmaf(w.x, a.x, fmaf(w.y, a.y, fmaf(w.z, a.z, fmaf(w.w, a.w, r0))));
             r1 = fmaf(w.x, a.y, fmaf(w.y, a.z, fmaf(w.z, a.w, fmaf(w.w, b.x, r1))));
             r2 = fmaf(w.x, a.z, fmaf(w.y, a.w, fmaf(w.z, b.x, fmaf(w.w, b.y, r2))));
             r3 = fmaf(w.x, a.w, fmaf(w.y, b.x, fmaf(w.z, b.y, fmaf(w.w, b.z, r3))));
+            a = b;
           }
           __syncthreads();  // LW is reused as the cross-group reduction buffer
           LW[g * S_T + 4 * o] = r0;
@@ -367,13 +370,16 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_child(const __grid_constant_
           const float4* A4 = reinterpret_cast<const float4*>(Gt);
           const float4* W4 = reinterpret_cast<const float4*>(LW);
           float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
+          // carried: b of one step is a of the next
+          float4 a = kb < ke ? A4[o + (kb >> 2)] : make_float4(0.f, 0.f, 0.f, 0.f);
           for (int k = kb; k < ke; k += 4) {
             const float4 w = W4[k >> 2];
-            const float4 a = A4[o + (k >> 2)], b = A4[o + (k >> 2) + 1];
+            const float4 b = A4[o + (k >> 2) + 1];
             r0 = fmaf(w.x, a.x, fmaf(w.y, a.y, fmaf(w.z, a.z, fmaf(w.w, a.w, r0))));
             r1 = fmaf(w.x, a.y, fmaf(w.y, a.z, fmaf(w.z, a.w, fmaf(w.w, b.x, r1))));
             r2 = fmaf(w.x, a.z, fmaf(w.y, a.w, fmaf(w.z, b.x, fmaf(w.w, b.y, r2))));
             r3 = fmaf(w.x, a.w, fmaf(w.y, b.x, fmaf(w.z, b.y, fmaf(w.w, b.z, r3))));
+            a = b;
           }
           __syncthreads();  // LW becomes the cross-group reduction buffer
           LW[g * S_T + 4 * o] = r0;
@@ -597,13 +603,15 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
             const float4* G4 = reinterpret_cast<const float4*>(Gt);
             const float4* E4 = reinterpret_cast<const float4*>(U);
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            float4 x = E4[kq >> 2];  // carried: y of one step is x of the next
             for (int q = 0; q < nt; q += 4) {
               const float4 g = G4[q >> 2];
-              const float4 x = E4[(q + kq) >> 2], y = E4[((q + kq) >> 2) + 1];
+              const float4 y = E4[((q + kq) >> 2) + 1];
               a0 = fmaf(g.x, x.x, fmaf(g.y, x.y, fmaf(g.z, x.z, fmaf(g.w, x.w, a0))));
               a1 = fmaf(g.x, x.y, fmaf(g.y, x.z, fmaf(g.z, x.w, fmaf(g.w, y.x, a1))));
               a2 = fmaf(g.x, x.z, fmaf(g.y, x.w, fmaf(g.z, y.x, fmaf(g.w, y.y, a2))));
               a3 = fmaf(g.x, x.w, fmaf(g.y, y.x, fmaf(g.z, y.y, fmaf(g.w, y.z, a3))));
+              x = y;
             }
             // w_i d out / d w_i convention (k_smooth_abc divides by 2^{lw2_i})
             accf[0] += (double)a0 * exp2(cexp + (double)lwf[0]);

@@ -130,10 +130,11 @@ struct PwLeaf {
     c = L.c;
     s_out = L.s_out;
   }
-  __device__ __forceinline__ float value(long long j) const {
-    const float x = __ldg(p + j * es);
-    return src ? s_out * x : s_out * __fadd_rn(s_in * x, c);
-  }
+  __device__ __forceinline__ float value(long long j) const { return apply(raw(j)); }
+  // the load and the transform apart: a thread issues all its loads before the first store
+  // (the output may alias nothing the compiler can prove, so it would not hoist them)
+  __device__ __forceinline__ float raw(long long j) const { return __ldg(p + j * es); }
+  __device__ __forceinline__ float apply(float x) const { return src ? s_out * x : s_out * __fadd_rn(s_in * x, c); }
   __device__ __forceinline__ void grad(long long j, float g) const {
     if (gp == nullptr || (g == 0.f && !gst)) return;
     const float v = src ? g * s_out : g * s_out * s_in;
@@ -151,12 +152,20 @@ __global__ void __launch_bounds__(PW_T) k_pointwise2_fwd(const __grid_constant__
   for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
     const PwLeaf a(e, e.leaf[e.step[0].a], row), b(e, e.leaf[e.step[1].a], row);
     float* out = p.out + row * L;
+    float xa[PW_E], xb[PW_E];
+#pragma unroll
+    for (int k = 0; k < PW_E; ++k) {
+      const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
+      const int tc = t < L ? t : L - 1;
+      xa[k] = a.raw(tc);
+      xb[k] = b.raw(tc);
+    }
 #pragma unroll
     for (int k = 0; k < PW_E; ++k) {
       const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
       if (t < L) {
         float w1, w2;
-        out[t] = pair_red<MODE>(a.value(t), b.value(t), sg, p.mp, w1, w2);
+        out[t] = pair_red<MODE>(a.apply(xa[k]), b.apply(xb[k]), sg, p.mp, w1, w2);
       }
     }
   }
@@ -171,13 +180,22 @@ __global__ void __launch_bounds__(PW_T) k_pointwise2_vjp(const __grid_constant__
   for (long long row = blockIdx.y; row < p.B; row += gridDim.y) {
     const PwLeaf a(e, e.leaf[e.step[0].a], row), b(e, e.leaf[e.step[1].a], row);
     const float* gr = g + row * L;
+    float xa[PW_E], xb[PW_E], xg[PW_E];
+#pragma unroll
+    for (int k = 0; k < PW_E; ++k) {
+      const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
+      const int tc = t < L ? t : L - 1;
+      xa[k] = a.raw(tc);
+      xb[k] = b.raw(tc);
+      xg[k] = gr[tc];
+    }
 #pragma unroll
     for (int k = 0; k < PW_E; ++k) {
       const int t = blockIdx.x * PW_N + k * PW_T + threadIdx.x;
       if (t < L) {
         float w1, w2;
-        pair_red<MODE>(a.value(t), b.value(t), sg, p.mp, w1, w2);
-        const float gv = gr[t];
+        pair_red<MODE>(a.apply(xa[k]), b.apply(xb[k]), sg, p.mp, w1, w2);
+        const float gv = xg[k];
         b.grad(t, 0.f + gv * w2);  // expr_vjp order (the later step first) and its 0 + adj
         a.grad(t, 0.f + gv * w1);
       }

@@ -23,12 +23,20 @@ namespace stlg {
 constexpr int UN_SEQ = 8, UN_LB = 2;
 static_assert(RC<UN_LB>::N == LB_MIN_TILE, "look-back slots are sized for 1024-sample tiles");
 
-// scan bounds of this CTA: every tile of the row (sequential) or tile blockIdx.x (look-back)
+// scan bounds of this CTA: every tile of the row (sequential, row = blockIdx.x) or the one
+// tile of its look-back ticket (row-major over B x ntiles)
 template <bool LB>
-__device__ __forceinline__ void unt_span(int ntiles, long long& row, int& s0, int& s1) {
-  row = LB ? blockIdx.y : blockIdx.x;
-  s0 = LB ? (int)blockIdx.x : 0;
-  s1 = LB ? (int)blockIdx.x + 1 : ntiles;
+__device__ __forceinline__ void unt_span(const FGParams& p, int ntiles, long long& row, int& s0, int& s1) {
+  if (LB) {
+    const int tk = lb_ticket(p.lb);
+    row = tk / ntiles;
+    s0 = tk - (int)row * ntiles;
+    s1 = s0 + 1;
+  } else {
+    row = blockIdx.x;
+    s0 = 0;
+    s1 = ntiles;
+  }
 }
 
 template <int RK, int MODE, int EK, int NW, bool LB>
@@ -41,13 +49,13 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_fwd(const __grid_
   const int ntiles = (L + N - 1) / N;
   long long row;
   int s0, s1;
-  unt_span<LB>(ntiles, row, s0, s1);
+  unt_span<LB>(p, ntiles, row, s0, s1);
   const float tau2 = p.mp.tau2, itau2 = p.mp.inv_tau2, sg = p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ev<MODE, EK> ev(p.child, row, p.mp);
   float* outr = p.out + row * L;
   const RSt id = rident<RK>();
-  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
+  unsigned* slots = LB ? p.lb + LB_WORDS + (size_t)row * ntiles * LB_WORDS : nullptr;
   RSt seq = id;  // sequential shape: fold of every sample after the current tile
   for (int s = s0; s < s1; ++s) {
     const int c0 = (ntiles - 1 - s) * N;  // scan order: from the row end
@@ -164,7 +172,7 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_lse(const __g
   const int ntiles = (L + N - 1) / N;
   long long row;
   int s0, s1;
-  unt_span<LB>(ntiles, row, s0, s1);
+  unt_span<LB>(p, ntiles, row, s0, s1);
   const float tau2 = p.mp.tau2, sg = p.sg, nsg = -p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_lse(const __g
   Ev<M_LSE, EK> ev(p.child, row, p.mp);
   const RSt id = rident<RK_GLSE>();
   const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
-  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
+  unsigned* slots = LB ? p.lb + LB_WORDS + (size_t)row * ntiles * LB_WORDS : nullptr;
   RSt seq = id;  // sequential shape: fold of every output before the current tile
   for (int s = s0; s < s1; ++s) {
     const int c0 = s * N;  // scan order: from the row start
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_hard(const __
   const int ntiles = (L + N - 1) / N;
   long long row;
   int s0, s1;
-  unt_span<LB>(ntiles, row, s0, s1);
+  unt_span<LB>(p, ntiles, row, s0, s1);
   const float sg = p.sg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
@@ -316,8 +324,8 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_hard(const __
   const HRun idr{-1, -1, 0.0, 1};
   const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
   // look-back: arg-max aggregates in slot row 0, run aggregates in slot row 1
-  unsigned* slots = LB ? p.lb + (size_t)row * ntiles * LB_WORDS : nullptr;
-  unsigned* rslots = LB ? slots + (size_t)gridDim.y * ntiles * LB_WORDS : nullptr;
+  unsigned* slots = LB ? p.lb + LB_WORDS + (size_t)row * ntiles * LB_WORDS : nullptr;
+  unsigned* rslots = LB ? slots + (size_t)p.B * ntiles * LB_WORDS : nullptr;
   RSt mseq = idm;  // sequential shape: (max, first arg-max) of every position after the tile
   HRun rseq = idr; //                   run state of every position after the tile
   for (int s = s0; s < s1; ++s) {
@@ -496,8 +504,8 @@ static bool unt_use_lb(const FGParams& p) {
   return p.lb != nullptr && p.B < 2 * 148 && p.L >= 4 * LB_MIN_TILE;
 }
 static cudaError_t unt_lb_reset(const FGParams& p, int rows_of_slots, cudaStream_t st) {
-  const long long ntiles = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
-  return cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * ntiles * rows_of_slots), st);
+  const long long ntiles = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;  // (+ the ticket slot)
+  return cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * ntiles * rows_of_slots + 1), st);
 }
 
 // register-blocked untimed forward (hard / LSE without masked_fill); false: not handled
@@ -506,7 +514,7 @@ bool launch_unt_fwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   const int ek = expr_kind(p.child);
   if (unt_use_lb(p)) {
     using C = RC<UN_LB>;
-    const dim3 grid((unsigned)((p.L + C::N - 1) / C::N), (unsigned)p.B);
+    const dim3 grid((unsigned)(((p.L + C::N - 1) / C::N) * p.B));  // tickets, row-major
     if ((err = unt_lb_reset(p, 1, st)) != cudaSuccess) return true;
     if (mode == M_HARD) {
       UNT_DISPATCH_EK(ek, (k_unt_fwd<RK_HARDV, M_HARD, EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))
@@ -533,7 +541,7 @@ bool launch_unt_bwd(int mode, FGParams& p, cudaStream_t st, cudaError_t& err) {
   const int ek = expr_kind(p.child);
   if (unt_use_lb(p)) {
     using C = RC<UN_LB>;
-    const dim3 grid((unsigned)((p.L + C::N - 1) / C::N), (unsigned)p.B);
+    const dim3 grid((unsigned)(((p.L + C::N - 1) / C::N) * p.B));  // tickets, row-major
     if ((err = unt_lb_reset(p, mode == M_HARD ? 2 : 1, st)) != cudaSuccess) return true;
     if (mode == M_HARD) {
       UNT_DISPATCH_EK(ek, (k_unt_bwd_hard<EK, UN_LB, true><<<grid, C::T, 0, st>>>(p)))

@@ -103,8 +103,8 @@ cudaError_t launch_fg_untimed_bwd(int mode, FGParams& p, cudaStream_t st);
 size_t until_bwd_scratch_bytes(int mode, int untimed, int fill, long long L, int b, int K);
 // look-back slots of the multi-CTA untimed scans (lookback.cuh): tiles of >= 1024 samples
 constexpr int LB_MIN_TILE = 1024;
-inline size_t lb_slot_bytes(long long B, long long L) {
-  return (size_t)B * (size_t)((L + LB_MIN_TILE - 1) / LB_MIN_TILE) * 32;
+inline size_t lb_slot_bytes(long long B, long long L) {  // + the ticket counter's slot
+  return (size_t)B * (size_t)((L + LB_MIN_TILE - 1) / LB_MIN_TILE) * 32 + 32;
 }
 cudaError_t launch_mining_grid(int mode, const float* x, long long n, int L, long long rs, const double* a,
                                const double* b, long long npairs, double c, double eps, float tau,

@@ -1,19 +1,29 @@
 // lookback.cuh — deterministic carries for row scans split over CTAs (SURVEY §2's
 // "single-pass suffix scan, decoupled look-back across time tiles").
 //
-// A row of n tiles is scanned by n CTAs.  The CTA with scan index s (blockIdx.x; the
-// tiles it depends on have smaller indices, so they were dispatched before it and are
-// resident or finished) stages and scans its own tile, publishes the tile aggregate, and
+// A row of n tiles is scanned by n CTAs.  Each CTA draws its (row, scan index s) from a
+// ticket counter (an atomic in the slot region), so every tile it depends on belongs to a
+// CTA that has already started — forward progress does not rest on the hardware's block
+// dispatch order.  It stages and scans its own tile, publishes the tile aggregate, and
 // then folds the published aggregates of tiles 0 .. s-1 in that fixed order.  There is no
 // inclusive-prefix shortcut: the carry is the same expression the sequential one-CTA walk
 // evaluated, so its bits do not depend on which tiles happened to finish first (the fp64
 // run sums and LSE carries stay reproducible).  One 32-byte slot per (row, tile): word 0
-// the flag (zeroed by the launcher before every launch), words 1..7 the payload.
+// the flag (zeroed by the launcher before every launch), words 1..7 the payload.  Slot
+// region layout: [ticket counter slot][row-major tile slots].
 #pragma once
 
 namespace stlg {
 
 constexpr int LB_WORDS = 8;
+
+// this CTA's ticket (0, 1, 2, ... in the order CTAs start), broadcast to every thread
+__device__ __forceinline__ int lb_ticket(unsigned* counter) {
+  __shared__ int tk;
+  if (threadIdx.x == 0) tk = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  return tk;
+}
 
 __device__ __forceinline__ void lb_store_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -674,15 +674,16 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_fwd(cons
   __shared__ float Ls[UH_T * UH_S];
   __shared__ float Rs[UH_T * UH_S];
   __shared__ Clamp cb[UH_T / 32];
-  const long long row = LB ? blockIdx.y : blockIdx.x;
   const int L = (int)p.L;  // < 2^31 (launcher)
   const int nch = (L + UH_CH - 1) / UH_CH;
+  const int tk = LB ? lb_ticket(p.lb) : 0;  // look-back shape: (row, chunk) from a ticket
+  const long long row = LB ? tk / nch : blockIdx.x;
   const int tid = threadIdx.x;
   const ChildEval cl(p.left, row), cr(p.right, row);
-  unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
+  unsigned* slots = LB ? p.lb + LB_WORDS + (size_t)row * nch * LB_WORDS : nullptr;
   // f_{L-1}(-inf) = A_{L-1}: the recurrence starts uniformly from -inf
   float seq = -INFINITY;  // sequential shape: the value entering the current chunk
-  for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
+  for (int s = LB ? tk - (int)row * nch : 0; s < (LB ? tk - (int)row * nch + 1 : nch); ++s) {
   const int c0 = (nch - 1 - s) * UH_CH;  // scan order: from the row end
   {  // all of the thread's loads in flight before the first store
     float lv[UH_E], rv[UH_E];
@@ -780,16 +781,17 @@ __global__ void __launch_bounds__(LB ? UH_LB : UH_SEQ) k_until_unt_hard_bwd(cons
   __shared__ float Ls[UH_T * UH_S], Rs[UH_T * UH_S], Os[UH_T * UH_S], Gs[UH_T * UH_S];
   __shared__ double wsum[UH_T / 32];
   __shared__ int wflag[UH_T / 32];
-  const long long row = LB ? blockIdx.y : blockIdx.x;
   const int L = (int)p.L;  // < 2^31 (launcher)
   const int nch = (L + UH_CH - 1) / UH_CH;
+  const int tk = LB ? lb_ticket(p.lb) : 0;  // look-back shape: (row, chunk) from a ticket
+  const long long row = LB ? tk / nch : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* outr = p.out_in + row * L;
   const float* cot = p.cot + row * L;
   const ChildEval cl(p.left, row), cr(p.right, row);
-  unsigned* slots = LB ? p.lb + (size_t)row * nch * LB_WORDS : nullptr;
+  unsigned* slots = LB ? p.lb + LB_WORDS + (size_t)row * nch * LB_WORDS : nullptr;
   double seq = 0.0;  // sequential shape: cotangent accumulated since the last terminator
-  for (int s = LB ? (int)blockIdx.x : 0; s < (LB ? (int)blockIdx.x + 1 : nch); ++s) {
+  for (int s = LB ? tk - (int)row * nch : 0; s < (LB ? tk - (int)row * nch + 1 : nch); ++s) {
   const int c0 = s * UH_CH;
   {  // coalesced staging of l, r, out[t + 1] and the cotangent, all loads in flight first
     float lv[UH_E], rv[UH_E], ov[UH_E], gv[UH_E];
@@ -1631,10 +1633,10 @@ static cudaError_t until_fwd_mode(UParams& p, cudaStream_t st) {
   if (p.untimed && MODE == M_HARD && !p.fill) {
     if (p.L >= (1LL << 31)) return cudaErrorNotSupported;  // 32-bit time indices
     if (uh_use_lb(p)) {
-      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
-      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);
+      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;  // (+ the ticket slot)
+      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch + 1), st);
       if (e != cudaSuccess) return e;
-      k_until_unt_hard_fwd<MODE, true><<<dim3((unsigned)nch, (unsigned)p.B), UH_LB, 0, st>>>(p);
+      k_until_unt_hard_fwd<MODE, true><<<(unsigned)(nch * p.B), UH_LB, 0, st>>>(p);
     } else {
       k_until_unt_hard_fwd<MODE, false><<<(unsigned)p.B, UH_SEQ, 0, st>>>(p);
     }
@@ -1665,10 +1667,10 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   if (p.untimed && MODE == M_HARD && !p.fill) {
     if (p.L >= (1LL << 31)) return cudaErrorNotSupported;  // 32-bit time indices
     if (uh_use_lb(p)) {
-      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;
-      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch), st);
+      const long long nch = (p.L + LB_MIN_TILE - 1) / LB_MIN_TILE;  // (+ the ticket slot)
+      cudaError_t e = cudaMemsetAsync(p.lb, 0, sizeof(unsigned) * LB_WORDS * (size_t)(p.B * nch + 1), st);
       if (e != cudaSuccess) return e;
-      k_until_unt_hard_bwd<MODE, true><<<dim3((unsigned)nch, (unsigned)p.B), UH_LB, 0, st>>>(p);
+      k_until_unt_hard_bwd<MODE, true><<<(unsigned)(nch * p.B), UH_LB, 0, st>>>(p);
     } else {
       k_until_unt_hard_bwd<MODE, false><<<(unsigned)p.B, UH_SEQ, 0, st>>>(p);
     }

@@ -479,6 +479,15 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_pad(const __grid_constant__ 
 // 1e-300 tail weights and overflows fp32; k_smooth_abc divides by the same 2^{lw2_i})
 // (zero where w_i == 0: the reference masks those entries before exp, tape.py:372)
 // ---------------------------------------------------------------------------
+// 2^x in fp64 for the d/dw factors: exact power of two times ex2 of the fraction (~2^-22
+// relative, the precision of the fp32 partial sums it scales) instead of the fp64 exp2
+// routine
+__device__ __forceinline__ double sm_ex2d(double x) {
+  if (!(x > -1022.0)) return 0.0;
+  const double n = floor(fmin(x, 1023.0));
+  return (double)ex2f((float)(x - n)) * __hiloint2double(((int)n + 1023) << 20, 0);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SParams p) {
   __shared__ __align__(16) float U[S_T + S_CH];
@@ -612,10 +621,10 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
               a3 = fmaf(g.x, x.w, fmaf(g.y, y.x, fmaf(g.z, y.y, fmaf(g.w, y.z, a3))));
             }
             // w_i d out / d w_i convention (k_smooth_abc divides by 2^{lw2_i})
-            accf[0] += (double)a0 * exp2(cexp + (double)lwf[0]);
-            accf[1] += (double)a1 * exp2(cexp + (double)lwf[1]);
-            accf[2] += (double)a2 * exp2(cexp + (double)lwf[2]);
-            accf[3] += (double)a3 * exp2(cexp + (double)lwf[3]);
+            accf[0] += (double)a0 * sm_ex2d(cexp + (double)lwf[0]);
+            accf[1] += (double)a1 * sm_ex2d(cexp + (double)lwf[1]);
+            accf[2] += (double)a2 * sm_ex2d(cexp + (double)lwf[2]);
+            accf[3] += (double)a3 * sm_ex2d(cexp + (double)lwf[3]);
           }
           done = true;
         }

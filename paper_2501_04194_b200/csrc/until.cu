@@ -972,6 +972,13 @@ struct UlStage {
   int fmin[4];
 };
 
+// 1 / x for x in the frames' normal fp64 range: the MUFU seed plus one Newton step
+// (~2^-44 relative; a correctly rounded fp64 division or __drcp_rn is a long sequence)
+__device__ __forceinline__ double ur_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
 __device__ __forceinline__ int ilogb_d(double x) { return (int)((__double2hiint(x) >> 20) & 0x7ff) - 1023; }
 __device__ __forceinline__ double pow2d(int e) { return __hiloint2double((e + 1023) << 20, 0); }
 __device__ __forceinline__ float pow2f(int e) {
@@ -1130,7 +1137,7 @@ __global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constan
         for (int j = lane; j < n; ++j) {
           s += S.ex[c * UL_C + j];
           const long long col = c0 + j;
-          if (!TIMED || (col >= u && col <= v)) A += 1.0 / (s + S.E[c * UL_C + j]);
+          if (!TIMED || (col >= u && col <= v)) A += ur_rcp(s + S.E[c * UL_C + j]);
         }
         base = s;
       } else if (!diag || c > w) {
@@ -1169,13 +1176,7 @@ __global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constan
 // (global-slab checkpoints; the grid is persistent for that slab).
 constexpr int UR_CB = 32;
 __host__ __device__ __forceinline__ int ur_span(int b) { return U_THREADS + b; }
-// 1 / x for x in the frame's normal fp64 range: the MUFU seed plus one Newton step
-// (~2^-44 relative; the correctly rounded __drcp_rn costs a multi-step sequence)
-__device__ __forceinline__ double ur_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  return fma(r, fma(-x, r, 1.0), r);
-}
+
 static size_t ur_smem(const UParams& p) {
   const size_t qb = (size_t)UR_CB * U_THREADS * 8;  // also the fallback's block buffer
   const size_t st = (size_t)2 * ur_span(p.b) * 8;
@@ -1418,7 +1419,7 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
           double s = 0.0;
           for (int j = lane; j < n; ++j) {
             s += S.ex[c * UL_C + j];
-            A += 1.0 / (s + S.E[c * UL_C + j]);
+            A += ur_rcp(s + S.E[c * UL_C + j]);
           }
           sown = s;
           base = s;
@@ -1458,7 +1459,8 @@ __global__ void __launch_bounds__(UL_T, UL_MINB) k_until_unt_lse_bwd(const __gri
               double sk = 0.0;
               for (int j = lane; j <= k; ++j) sk += S.ex[c * UL_C + j];
               const double D = sk + S.E[c * UL_C + k];
-              const double w2 = 1.0 / (D * D);
+              const double qd = ur_rcp(D);
+              const double w2 = qd * qd;
               Rt += w2;
               pv = (float)(cA * S.E[c * UL_C + k] * w2);
               qv = (float)(cA * S.ex[c * UL_C + k] * Rt);

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_cav_fwd(const __gri
 // backward, LSE (gather form over outputs t; RK_GLSE)
 // ---------------------------------------------------------------------------
 template <int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + 1) k_cav_bwd_lse(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];
@@ -343,7 +343,6 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const
   __shared__ float padsum_sh;
   float* P0 = rsm;
   float* P1 = rsm + C::NP;
-  float* P2 = rsm + 2 * C::NP;  // staged low words of M
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
   const int L = (int)p.L;
@@ -378,8 +377,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const
 #pragma unroll
         for (int k = 0; k < CAV_LB; ++k) {
           P0[so + (h + k) * SS] = nsg * mv[k];
-          P1[so + (h + k) * SS] = gv[k];
-          P2[so + (h + k) * SS] = lv[k];
+          // the low word of M folded into the weight: g 2^{-tau2 sg lo} (|tau2 lo| << 1)
+          P1[so + (h + k) * SS] = lp ? gv[k] * ex2f(nt2sg * lv[k]) : gv[k];
         }
       }
     } else {
@@ -400,8 +399,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const
           const int t = tt + (h + k) * T;
           const bool v = t >= 0 && t < nvalid;
           P0[so + (h + k) * SS] = v ? nsg * mv[k] : -FLT_MAX;
-          P1[so + (h + k) * SS] = v ? gv[k] : 0.f;
-          P2[so + (h + k) * SS] = v ? lv[k] : 0.f;
+          P1[so + (h + k) * SS] = v ? (lor ? gv[k] * ex2f(nt2sg * lv[k]) : gv[k]) : 0.f;
         }
       }
     }
@@ -418,22 +416,19 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const
   }
   __syncthreads();
   RSt x[RG_EPT];
-  float lw[RG_EPT];
 #pragma unroll
   for (int k = 0; k < RG_EPT; ++k) {
     const int qq = tid * (RG_EPT + 1) + k;
     x[k] = RSt{P0[qq], P1[qq]};
-    lw[k] = P2[qq];
   }
   const bool full = tid * RG_EPT + RG_EPT <= J;
   float f;
   const bool wide = fs_frame(x, true, tau2, f);
   if (!__syncthreads_or(wide)) {
-    // E = g 2^{tau2 (e - lo - f)} (one ex2; the low word shifts the exponent)
+    // E = g' 2^{tau2 (e - f)}, g' = g 2^{-tau2 sg lo} from the staging
     float E[RG_EPT];
 #pragma unroll
-    for (int k = 0; k < RG_EPT; ++k)
-      E[k] = x[k].s != 0.f ? x[k].s * ex2f(fmaf(tau2, x[k].m - f, nt2sg * lw[k])) : 0.f;
+    for (int k = 0; k < RG_EPT; ++k) E[k] = x[k].s != 0.f ? x[k].s * ex2f(tau2 * (x[k].m - f)) : 0.f;
     fs_scans(E, f, P0, T0, T1);
     __syncthreads();
     RSt A0, A1;
@@ -448,8 +443,6 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_lse(const
     if (full) fs_windows<true>(E, c0, c1, d, c, 0, J, P0, fin);
     else fs_windows<false>(E, c0, c1, d, c, 0, J, P0, fin);
   } else {
-#pragma unroll
-    for (int k = 0; k < RG_EPT; ++k) x[k].s = x[k].s != 0.f ? x[k].s * ex2f(nt2sg * lw[k]) : 0.f;
     cav_scans<RK_GLSE>(x, tau2, P0, P1, T0, T1);
     __syncthreads();
     RSt A0, A1;

@@ -71,7 +71,7 @@ cudaError_t bwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
   } else {
     const int J = C::N - p.K + 1;
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
-    const size_t smem = (size_t)(cav ? 3 : 2) * C::NP * 4;
+    const size_t smem = (size_t)2 * C::NP * 4;
     if (cav) {
       REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_lse<EK, NW>, grid, C::T, smem, p, st))
     } else {

@@ -624,7 +624,7 @@ __device__ __forceinline__ RunSeg run_shfl_up(RunSeg v, int o) {
 }
 
 template <int EK, int NW, bool IDX>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + (IDX ? 1 : 0)) k_cav_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   constexpr int NOKEY = 0x7fffffff;  // windows past the tile: g = 0, key above every element
@@ -635,7 +635,9 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
   __shared__ float padsum_sh;
   float* P0 = rsm;
   float* P1 = rsm + C::NP;
-  float* G = rsm + 2 * C::NP;
+  // IDX: no scans reuse P0 / P1 after the keys and cotangents reach registers, so the
+  // run totals take P1's space (two arrays: one more resident CTA per SM)
+  float* G = IDX ? rsm + C::NP : rsm + 2 * C::NP;
   const int K = p.K;
   const int d = (K - 1) >> 4, c = (K - 1) & 15;
   const int L = (int)p.L;
@@ -750,6 +752,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_cav_bwd_hard(cons
       g[k] = P1[q0 + k];
     }
   }
+  if constexpr (IDX) __syncthreads();  // every P1 read done before G (its space) is written
   {
     const int q0 = tid * (RG_EPT + 1);
 #pragma unroll

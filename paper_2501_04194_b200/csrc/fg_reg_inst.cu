@@ -56,8 +56,8 @@ cudaError_t bwd_nw(int mode, int ek, FGParams& p, cudaStream_t st) {
     dim3 grid((unsigned)((p.L + J - 1) / J), (unsigned)p.B);
     const size_t smem = (size_t)3 * C::NP * 4;
     if (cav) {
-      if (p.aux_in != nullptr) {  // the forward's arg-max: no recomputation
-        REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW, true>, grid, C::T, smem, p, st))
+      if (p.aux_in != nullptr) {  // the forward's arg-max: no recomputation (two arrays)
+        REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW, true>, grid, C::T, 2 * C::NP * 4, p, st))
       } else {
         REG_DISPATCH_EK(ek, e = reg_launch(k_cav_bwd_hard<EK, NW, false>, grid, C::T, smem, p, st))
       }

@@ -72,8 +72,9 @@ struct SParams {
 
 // rows per CTA of the d/dw pass; each CTA writes one partial row of d out / d w_i and a
 // second pass sums the partials in a fixed order (deterministic d(a, b, c))
-constexpr int SMOOTH_RP = 4;
-inline long long smooth_dw_parts(long long B) { return (B + SMOOTH_RP - 1) / SMOOTH_RP; }
+// d/dw pass: one CTA (and one fp64 partial row) per ceil(B / parts) rows, parts = one
+// wave of resident CTAs (148 SMs x 4) so the pass has no partial second wave
+inline long long smooth_dw_parts(long long B) { return B < 592 ? B : 592; }
 
 // timed softmax F / G in fp64 (fg_soft64.cu): applicability, forward, fused backward
 bool sx_applicable(const FGParams& p);

@@ -24,7 +24,6 @@ namespace stlg {
 
 constexpr int S_T = 256;    // outputs (or child elements) per CTA
 constexpr int S_CH = 1024;  // window offsets staged per chunk
-constexpr int S_RP = SMOOTH_RP;  // rows per CTA in the d/dw pass (kernels.cuh)
 
 // ---------------------------------------------------------------------------
 // forward
@@ -500,8 +499,9 @@ __global__ void __launch_bounds__(S_T) k_smooth_bwd_w(const __grid_constant__ SP
   const int L = (int)p.L;
   const int K = p.i_hi - p.i_lo + 1;
   const float sg = p.sg, tau2 = p.mp.tau2, itau = 1.f / p.mp.tau;
-  const long long r0 = (long long)blockIdx.x * S_RP;
-  const long long r1 = min(r0 + S_RP, p.B);
+  const long long rp = (p.B + gridDim.x - 1) / gridDim.x;  // rows per CTA (smooth_dw_parts)
+  const long long r0 = (long long)blockIdx.x * rp;
+  const long long r1 = min(r0 + rp, p.B);
   for (int k0 = 0; k0 < K; k0 += S_CH) {
     const int kc = min(S_CH, K - k0);
     // each thread owns offsets i = i_lo + k0 + k, k = threadIdx.x + S_T * c

@@ -40,7 +40,7 @@ __device__ __forceinline__ void unt_span(const FGParams& p, int ntiles, long lon
 }
 
 template <int RK, int MODE, int EK, int NW, bool LB>
-__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_fwd(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 4) k_unt_fwd(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
   __shared__ float P[NP];
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_fwd(const __grid_
 // — an inclusive prefix scan over the outputs of the (e_t = -M_t, g_t) elements
 // (RK_GLSE), scan order from the row start, then the fused child VJP over the tile.
 template <int EK, int NW, bool LB>
-__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_lse(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 3) k_unt_bwd_lse(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
   __shared__ float B0[NP], B1[NP];
@@ -304,7 +304,7 @@ __device__ __forceinline__ HRun hrun_shfl_down(HRun v, int o) {
 }
 
 template <int EK, int NW, bool LB>
-__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 2) k_unt_bwd_hard(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 3) k_unt_bwd_hard(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS, NP = C::NP;
   __shared__ float U[NP];  // child values (max space), then the arg-max keys

@@ -1174,14 +1174,15 @@ __global__ void __launch_bounds__(UL_T) k_until_rcp_lse_fwd(const __grid_constan
 // contributions scatter warp-systolically into the reproducible int64 accumulators.
 // Tiles whose values span more than UL_RANGE log2 units run the per-pair tile function
 // (global-slab checkpoints; the grid is persistent for that slab).
-constexpr int UR_CB = 32;
+constexpr int UR_CB = 16;
 __host__ __device__ __forceinline__ int ur_span(int b) { return U_THREADS + b; }
 
 static size_t ur_smem(const UParams& p) {
-  const size_t qb = (size_t)UR_CB * U_THREADS * 8;  // also the fallback's block buffer
+  const size_t qb = (size_t)UR_CB * U_THREADS * 8;
   const size_t st = (size_t)2 * ur_span(p.b) * 8;
   const size_t ck = (size_t)((p.K + UR_CB - 1) / UR_CB) * U_THREADS * 8;
-  return qb + st + ck;
+  const size_t fallback = (size_t)U_CB_G * 2 * U_THREADS * 4;  // the per-pair tiles' block buffer
+  return max(qb + st + ck, fallback);
 }
 
 __global__ void __launch_bounds__(U_THREADS) k_until_rcp_lse_bwd_timed(const __grid_constant__ UParams p, int ntx,
@@ -1190,7 +1191,8 @@ __global__ void __launch_bounds__(U_THREADS) k_until_rcp_lse_bwd_timed(const __g
   __shared__ float red[8];
   const long long L = p.L;
   const int K = p.K, tid = threadIdx.x, span = ur_span(p.b);
-  double* QB = reinterpret_cast<double*>(dsm);  // [UR_CB][U_THREADS]
+  double* QB = reinterpret_cast<double*>(dsm);  // [UR_CB][U_THREADS] (the fallback's block buffer
+                                                //  overlays the start of the region)
   double* EXs = QB + UR_CB * U_THREADS;           // [span]
   double* ERs = EXs + span;                       // [span]
   double* CK = ERs + span;                        // [ceil(K / UR_CB)][U_THREADS]

@@ -247,7 +247,7 @@ __device__ __forceinline__ void rsuffix_windows(const RSt (&x)[RG_EPT], unsigned
 // forward (hard: RK_HARD, LSE: RK_LSE)
 // ---------------------------------------------------------------------------
 template <int RK, int MODE, int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB) k_reg_fwd(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 1) k_reg_fwd(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];

@@ -313,3 +313,47 @@ def test_lse_timed_until_reciprocal_sweep(cuda, a, K, L, pad):
     assert rel_err(tr, ref_tr) <= TOL
     for k in ("x", "y"):
         assert rel_err(g[k], ref_g[k]) <= TOL, k
+
+
+@pytest.mark.parametrize("mode", [P.Hard(), P.LogSumExp(5.0)], ids=["hard", "lse"])
+@pytest.mark.parametrize("child", ["norm_pair", "compound"])
+def test_untimed_lookback_child_kinds(cuda, mode, child):
+    """The look-back shape (small batch, long rows) with the other child evaluators: a
+    NormPred over an interleaved [B, T, 2] tensor (EK_PAIR) and a compound child (an And of
+    predicates, materialised by its own pointwise entry); sampled rows vs the oracle."""
+    import torch
+    rng = np.random.default_rng(90 + (child == "compound"))
+    B, T = 6, 9000
+    dev = torch.device("cuda", 0)
+    if child == "norm_pair":
+        pxy = np.asarray(np.cumsum(rng.normal(0, 0.05, (B, T, 2)), axis=1), dtype=np.float32)
+        t = torch.tensor(pxy, device=dev).requires_grad_(True)
+        chans = {"px": t[..., 0], "py": t[..., 1]}
+        f = P.Eventually(P.NormPred(("px", "py"), "<", 0.5))
+        arrays = {"px": pxy[..., 0], "py": pxy[..., 1]}
+        leaves = [t]
+    else:
+        x = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+        y = np.asarray(rng.normal(0, 1, (B, T)), dtype=np.float32)
+        tx = torch.tensor(x, device=dev).requires_grad_(True)
+        ty = torch.tensor(y, device=dev).requires_grad_(True)
+        chans = {"x": tx, "y": ty}
+        f = P.Always(P.And(P.Pred("x", ">", -0.5), P.Pred("y", "<", 0.8)))
+        arrays = {"x": x, "y": y}
+        leaves = [tx, ty]
+    cfg = P.SemanticsConfig(mode=mode)
+    out = P.trace(f, chans, cfg)
+    cot = torch.tensor(np.asarray(rng.uniform(0.5, 1.5, (B, T)), dtype=np.float32), device=dev)
+    grads = torch.autograd.grad(out, leaves, cot)
+    tr = out.detach().double().cpu().numpy()
+    if child == "norm_pair":
+        g = grads[0].double().cpu().numpy()
+        gk = {"px": g[..., 0], "py": g[..., 1]}
+    else:
+        gk = {"x": grads[0].double().cpu().numpy(), "y": grads[1].double().cpu().numpy()}
+    for r in (0, 5):
+        rows = {k: v[r:r + 1].astype(np.float64) for k, v in arrays.items()}
+        ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, rows, cfg, cot[r:r + 1].double().cpu().numpy())
+        assert rel_err(tr[r:r + 1], ref_tr) <= TOL
+        for k in arrays:
+            assert rel_err(gk[k][r:r + 1], ref_g[k]) <= TOL, k

@@ -261,7 +261,7 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
 // forward (hard: RK_HARD, LSE: RK_LSE)
 // ---------------------------------------------------------------------------
 template <int RK, int MODE, int EK, int NW>
-__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 1) k_cav_fwd(const __grid_constant__ FGParams p) {
+__global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 2) k_cav_fwd(const __grid_constant__ FGParams p) {
   using C = RC<NW>;
   constexpr int T = C::T, N = C::N, SS = C::SS;
   extern __shared__ float rsm[];

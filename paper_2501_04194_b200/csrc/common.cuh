@@ -91,6 +91,20 @@ __device__ __forceinline__ float ld_na(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
+// Low word of the double-float LSE trace (M = hi + lo, |lo| <= ulp(hi) / 2), kept as a
+// bf16 plane in the first half of the row's aux words: 2 B per sample instead of 4 in the
+// forward's write and the backward's read.  Rounding lo to 8 bits moves M by at most
+// 2^-9 |lo| <= 2^-10 ulp(hi), far below the fp32 rounding the low word corrects.
+__device__ __forceinline__ unsigned short lo_pack(float v) {
+  unsigned u = __float_as_uint(v);  // finite, |v| tiny: round to nearest even cannot overflow
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (unsigned short)(u >> 16);
+}
+__device__ __forceinline__ float lo_ld(const unsigned short* p) {
+  unsigned short h;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(h) : "l"(p));
+  return __uint_as_float((unsigned)h << 16);
+}
 __device__ __forceinline__ float2 ld_na2(const float2* p) {
   float2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));

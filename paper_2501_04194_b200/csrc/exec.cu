@@ -13,7 +13,10 @@
 // stlg_forward runs the entries in order; stlg_backward runs them in reverse,
 // each consuming the cotangent of its own output (user cotangent for the
 // root, else its slot's accumulated cotangent) — the schedule equivalent of
-// tape.backward's reverse topological walk (tape.py:114-134).
+// tape.backward's reverse topological walk (tape.py:114-134).  Independent
+// sub-formulas under the root (no shared slot, channel or smooth binding, e.g.
+// the two operands of C3's And) run on two streams with their own scratch:
+// most of these kernels are latency-bound and leave the GPU half idle alone.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -75,6 +78,8 @@ struct stlg_plan {
   stlg_cfg cfg;
   int n_ch = 0, n_smooth = 0, n_slots = 0, n_aux = 0, n_tables = 0;
   int root_temporal = 0;
+  int n_lanes = 1;         // 2: entries before the last split into two independent lanes
+  std::vector<int> lane;   // per entry: 0 (caller's stream) or 1 (side stream); last entry 0
   std::vector<Entry> entries;
   std::vector<int> ch_touched;  // channel referenced by some leaf (else zero-filled on overwrite)
 };
@@ -226,6 +231,72 @@ void mark_first_writers(stlg_plan* plan) {
   plan->ch_touched.assign(plan->n_ch, 0);
   for (auto& kv : touched)
     if (kv.first < plan->n_ch) plan->ch_touched[kv.first] = 1;
+}
+
+// Lanes: the entries before the last one (the root, which joins everything) fall into
+// connected components under "reads the other's slot", "touches the same channel" and
+// "shares a smooth binding" — components share no buffer the backward writes (channel
+// gradients, slot cotangents, d(a,b,c)), so they may run concurrently.  Two or more
+// components are dealt to two lanes, heaviest first (an Until entry counts 4).
+void assign_lanes(stlg_plan* plan) {
+  const int n = (int)plan->entries.size();
+  plan->lane.assign(n, 0);
+  plan->n_lanes = 1;
+  if (n < 3) return;
+  std::vector<int> par(n - 1);
+  for (int i = 0; i < n - 1; ++i) par[i] = i;
+  auto find = [&](int x) {
+    while (par[x] != x) x = par[x] = par[par[x]];
+    return x;
+  };
+  auto unite = [&](int a, int b) { par[find(a)] = find(b); };
+  std::vector<int> producer(plan->n_slots, -1);
+  for (int i = 0; i < n - 1; ++i)
+    if (plan->entries[i].out_slot >= 0) producer[plan->entries[i].out_slot] = i;
+  std::map<int, int> ch_user, smooth_user;
+  auto touch = [&](int i, int src) {
+    if (src < plan->n_ch) {
+      auto it = ch_user.find(src);
+      if (it == ch_user.end()) ch_user[src] = i;
+      else unite(i, it->second);
+    } else if (src - plan->n_ch < plan->n_slots && producer[src - plan->n_ch] >= 0) {
+      unite(i, producer[src - plan->n_ch]);
+    }
+  };
+  auto visit = [&](int i, const HExpr& ex) {
+    for (const HLeaf& lf : ex.leaf) {
+      if (lf.kind == LEAF_CONST) continue;
+      touch(i, lf.src);
+      if (lf.kind == LEAF_NORM) touch(i, lf.src2);
+    }
+  };
+  for (int i = 0; i < n - 1; ++i) {
+    const Entry& e = plan->entries[i];
+    visit(i, e.e1);
+    if (e.kind == E_UNTIL) visit(i, e.e2);
+    if (e.kind == E_FG_SMOOTH) {
+      auto it = smooth_user.find(e.smooth_slot);
+      if (it == smooth_user.end()) smooth_user[e.smooth_slot] = i;
+      else unite(i, it->second);
+    }
+  }
+  std::map<int, int> cost;  // component root -> weight
+  for (int i = 0; i < n - 1; ++i) cost[find(i)] += plan->entries[i].kind == E_UNTIL ? 4 : 1;
+  if (cost.size() < 2) return;
+  std::vector<std::pair<int, int>> comps;  // (weight, root)
+  for (auto& kv : cost) comps.push_back({kv.second, kv.first});
+  std::sort(comps.begin(), comps.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+    return x.first != y.first ? x.first > y.first : x.second < y.second;
+  });
+  int load[2] = {0, 0};
+  std::map<int, int> lane_of;
+  for (auto& c : comps) {
+    const int l = load[1] < load[0] ? 1 : 0;
+    lane_of[c.second] = l;
+    load[l] += c.first;
+  }
+  for (int i = 0; i < n - 1; ++i) plan->lane[i] = lane_of[find(i)];
+  plan->n_lanes = 2;
 }
 
 int validate_nodes(const stlg_node* nodes, int n, int n_ch, int n_smooth) {
@@ -513,6 +584,7 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     plan->entries.push_back(e);
   }
   mark_first_writers(plan);
+  assign_lanes(plan);
   *out_plan = plan;
   return STLG_OK;
 }
@@ -561,6 +633,13 @@ static size_t det_bytes(const stlg_plan* plan, long long B, long long T) {
   return align256(sizeof(unsigned long long) * 4 * (size_t)B * (size_t)T) + align256(sizeof(int) * (size_t)B);
 }
 
+// per-lane backward scratch: [scratch 3BT | dw64 (+ partials) | dacc, dscale | 256 | Until
+// slab | look-back slots (2 rows)]; lane 1 (plans with independent sub-formulas) gets a copy
+static size_t bwd_lane_bytes(const stlg_plan* plan, long long B, long long T) {
+  return align256(sizeof(float) * 3 * (size_t)B * (size_t)T) + dw_bytes(plan, B, T) + det_bytes(plan, B, T) +
+         256 + until_slab_bytes(plan, T) + align256(2 * lb_slot_bytes(B, T));
+}
+
 int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fwd_bytes,
                          size_t* bwd_bytes) {
   if (!plan) return fail(STLG_E_INVALID, "null plan");
@@ -568,16 +647,16 @@ int stlg_workspace_bytes(const stlg_plan* plan, int64_t B, int64_t T, size_t* fw
   long long BT = (long long)B * T;
   size_t sb, ab;
   fwd_layout(plan, BT, &sb, &ab);
-  if (fwd_bytes) *fwd_bytes = sb + ab + tables_bytes(plan, T) + align256(lb_slot_bytes(B, T)) + 256;
+  if (fwd_bytes)
+    *fwd_bytes = sb + ab + tables_bytes(plan, T) + plan->n_lanes * align256(lb_slot_bytes(B, T)) + 256;
   if (bwd_bytes)
-    *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) +
-                 align256(sizeof(float) * 3 * (size_t)BT) + dw_bytes(plan, B, T) +
-                 det_bytes(plan, B, T) + until_slab_bytes(plan, T) + align256(2 * lb_slot_bytes(B, T)) + 1024;
+    *bwd_bytes = align256(sizeof(float) * (size_t)plan->n_slots * BT) + plan->n_lanes * bwd_lane_bytes(plan, B, T) +
+                 1024;
   return STLG_OK;
 }
 
 static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws, size_t fwd_bytes,
-                      void* bwd_ws, size_t bwd_bytes, Bufs& bf) {
+                      void* bwd_ws, size_t bwd_bytes, Bufs& bf, int lane = 0) {
   long long BT = (long long)B * T;
   size_t need_f, need_b;
   stlg_workspace_bytes(plan, B, T, &need_f, &need_b);
@@ -589,7 +668,7 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
   bf.slots = (float*)base;
   bf.aux = (float*)(base + sb);
   bf.tables = (float*)(base + sb + ab);
-  bf.lb = (unsigned*)(base + sb + ab + tables_bytes(plan, T));
+  bf.lb = (unsigned*)(base + sb + ab + tables_bytes(plan, T) + lane * align256(lb_slot_bytes(B, T)));
   bf.gslots = nullptr;
   bf.scratch = nullptr;
   bf.uslab = nullptr;
@@ -600,7 +679,8 @@ static int setup_bufs(const stlg_plan* plan, int64_t B, int64_t T, void* fwd_ws,
     if (bwd_bytes < need_b) return fail(STLG_E_INVALID, "backward workspace too small");
     uintptr_t bb = ((uintptr_t)bwd_ws + 255) & ~(uintptr_t)255;
     bf.gslots = (float*)bb;
-    bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT));
+    bf.scratch = (float*)(bb + align256(sizeof(float) * (size_t)plan->n_slots * BT) +
+                          lane * bwd_lane_bytes(plan, B, T));
     bf.dw64 = (double*)((uintptr_t)bf.scratch + align256(sizeof(float) * 3 * (size_t)BT));
     bf.dwpart = bf.dw64 + align256(sizeof(double) * (size_t)T) / sizeof(double);
     uintptr_t dp = (uintptr_t)bf.dw64 + dw_bytes(plan, B, T);
@@ -708,6 +788,41 @@ static int run_smooth(const stlg_plan* plan, const Entry& e, const stlg_channel*
   return STLG_OK;
 }
 
+// Side stream + fork / join events for two-lane plans: one set per host thread and
+// device (autograd runs the backward on its own thread), created on first use outside
+// stream capture (a capturing call without them runs its lanes in order on the caller's
+// stream).  Under capture the fork / join records pull the side stream into the graph.
+struct Fork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+};
+static Fork* fork_for(cudaStream_t st) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  thread_local std::map<int, Fork> forks;
+  Fork& f = forks[dev];
+  if (f.side == nullptr) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      f = Fork{};
+      return nullptr;
+    }
+  }
+  return &f;
+}
+static cudaError_t fork_begin(const Fork* f, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(f->ev_fork, st);
+  return e == cudaSuccess ? cudaStreamWaitEvent(f->side, f->ev_fork, 0) : e;
+}
+static cudaError_t fork_end(const Fork* f, cudaStream_t st) {
+  cudaError_t e = cudaEventRecord(f->ev_join, f->side);
+  return e == cudaSuccess ? cudaStreamWaitEvent(st, f->ev_join, 0) : e;
+}
+
 int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B, int64_t T,
                  const stlg_smooth* smooth_params, float* trace_out, void* fwd_ws,
                  size_t fwd_ws_bytes, void* stream) {
@@ -716,12 +831,21 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
   if (B > 65535) return fail(STLG_E_SHAPE, "batch rows per call must be <= 65535");
   if (plan->n_ch > 0 && !channels) return fail(STLG_E_INVALID, "null channels");
   if (plan->n_slots + plan->n_aux > 0 && !fwd_ws) return fail(STLG_E_INVALID, "null workspace");
-  Bufs bf{};
-  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, nullptr, 0, bf);
+  Bufs bfl[2]{};
+  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, nullptr, 0, bfl[0]);
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
+  if (plan->n_lanes > 1 && (rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, nullptr, 0, bfl[1], 1))) return rc;
+  cudaStream_t st0 = (cudaStream_t)stream;
+  const Fork* fk = plan->n_lanes > 1 ? fork_for(st0) : nullptr;
+  if (fk && (rc = cuda_status(fork_begin(fk, st0), "fork"))) return rc;
   const int mode = plan->cfg.mode;
-  for (const Entry& e : plan->entries) {
+  const int n_entries = (int)plan->entries.size();
+  for (int ei = 0; ei < n_entries; ++ei) {
+    const Entry& e = plan->entries[ei];
+    const int ln = plan->lane[ei];
+    const Bufs& bf = bfl[ln];
+    cudaStream_t st = (fk && ln == 1) ? fk->side : st0;
+    if (fk && ei == n_entries - 1 && (rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
     float* out = e.out_slot < 0 ? trace_out : bf.slot(e.out_slot);
     cudaError_t ce = cudaSuccess;
     if (e.kind == E_POINTWISE || e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) {
@@ -773,20 +897,29 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
   if (B <= 0 || T <= 0) return fail(STLG_E_SHAPE, "empty signal batch");
   if (B > 65535) return fail(STLG_E_SHAPE, "batch rows per call must be <= 65535");
   if (!bwd_ws) return fail(STLG_E_INVALID, "null backward workspace");
-  Bufs bf{};
-  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, bwd_ws, bwd_ws_bytes, bf);
+  Bufs bfl[2]{};
+  int rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, bwd_ws, bwd_ws_bytes, bfl[0]);
   if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
+  if (plan->n_lanes > 1 &&
+      (rc = setup_bufs(plan, B, T, fwd_ws, fwd_ws_bytes, bwd_ws, bwd_ws_bytes, bfl[1], 1)))
+    return rc;
+  cudaStream_t st0 = (cudaStream_t)stream;
   const int mode = plan->cfg.mode;
   for (int c = 0; c < plan->n_ch && d_channels; ++c) {
     const stlg_grad& g = d_channels[c];
     if (g.ptr && !g.accumulate && !plan->ch_touched[c]) {
-      cudaError_t ce = launch_fill_strided(g.ptr, B, T, g.row_stride, g.elem_stride, 0.f, st);
+      cudaError_t ce = launch_fill_strided(g.ptr, B, T, g.row_stride, g.elem_stride, 0.f, st0);
       if ((rc = cuda_status(ce, "zero-fill"))) return rc;
     }
   }
-  for (auto it = plan->entries.rbegin(); it != plan->entries.rend(); ++it) {
-    const Entry& e = *it;
+  const Fork* fk = plan->n_lanes > 1 ? fork_for(st0) : nullptr;
+  const int n_entries = (int)plan->entries.size();
+  for (int ei = n_entries - 1; ei >= 0; --ei) {
+    const Entry& e = plan->entries[ei];
+    const int ln = plan->lane[ei];
+    const Bufs& bf = bfl[ln];
+    cudaStream_t st = (fk && ln == 1) ? fk->side : st0;
+    if (fk && ei == n_entries - 2 && (rc = cuda_status(fork_begin(fk, st0), "fork"))) return rc;
     const float* g = e.out_slot < 0 ? cot : bf.gslot(e.out_slot);
     const float* out_in = e.out_slot < 0 ? trace : bf.slot(e.out_slot);
     cudaError_t ce = cudaSuccess;
@@ -834,6 +967,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
     }
     if ((rc = cuda_status(ce, "backward launch"))) return rc;
   }
+  if (fk && (rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
   return STLG_OK;
 }
 

@@ -239,14 +239,19 @@ __device__ __forceinline__ void cav_fwd_core(const FGParams& p, long long row, i
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
-    if (auxr != nullptr) {  // LSE: low word of the double-float trace; softmax: window LSE;
-                            // hard: arg-max offset (uint16 plane in the row's aux words)
+    if (auxr != nullptr) {  // LSE: low word of the double-float trace (bf16 plane); softmax:
+                            // window LSE; hard: arg-max offset (uint16 plane in the row's aux words)
       const float* src1 = P1 + rpad(tid + K - 1);
       if (RK == RK_HARDI) {
         unsigned short* ap = reinterpret_cast<unsigned short*>(auxr) + t0 + tid;
 #pragma unroll
         for (int k = 0; k < RG_EPT; ++k)
           if (tid + k * T < tend) ap[k * T] = (unsigned short)__float_as_int(src1[k * SS]);
+      } else if (RK == RK_LSE) {
+        unsigned short* ap = reinterpret_cast<unsigned short*>(auxr) + t0 + tid;
+#pragma unroll
+        for (int k = 0; k < RG_EPT; ++k)
+          if (tid + k * T < tend) ap[k * T] = lo_pack(src1[k * SS]);
       } else {
         float* ap = auxr + t0 + tid;
 #pragma unroll
@@ -290,6 +295,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 2) k_cav_fwd(const _
     for (int i = tid; i < tend; i += T) {
       outr[t0 + i] = __fadd_rn(padv, czero);
       if (auxr && RK == RK_HARDI) reinterpret_cast<unsigned short*>(auxr)[t0 + i] = 0xffff;
+      else if (auxr && RK == RK_LSE) reinterpret_cast<unsigned short*>(auxr)[t0 + i] = 0;
       else if (auxr) auxr[t0 + i] = 0.f;
     }
     return;
@@ -355,7 +361,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + 1) k_cav_bwd_lse(c
   const float nsg = -sg, nt2sg = -tau2 * sg;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
-  const float* lor = p.aux_in ? p.aux_in + row * L : nullptr;  // low word of M (double-float)
+  const unsigned short* lor =  // low word of M (double-float, bf16 plane)
+      p.aux_in ? reinterpret_cast<const unsigned short*>(p.aux_in + row * L) : nullptr;
   const int tid = threadIdx.x;
   // phase 1: e_t = -M_t (max space), g_t, lo_t; (-FLT_MAX, 0, 0) outside [0, nvalid)
   {
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + 1) k_cav_bwd_lse(c
     if (tb >= 0 && tb + N <= nvalid) {
       const float* cp = cot + tt;
       const float* mp = outr + tt;
-      const float* lp = lor ? lor + tt : nullptr;
+      const unsigned short* lp = lor ? lor + tt : nullptr;
 #pragma unroll
       for (int h = 0; h < RG_EPT; h += CAV_LB) {
         float gv[CAV_LB], mv[CAV_LB], lv[CAV_LB];
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + 1) k_cav_bwd_lse(c
         for (int k = 0; k < CAV_LB; ++k) {
           gv[k] = ld_na(cp + (h + k) * T);
           mv[k] = ld_na(mp + (h + k) * T);
-          lv[k] = lp ? ld_na(lp + (h + k) * T) : 0.f;
+          lv[k] = lp ? lo_ld(lp + (h + k) * T) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < CAV_LB; ++k) {
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B + 1) k_cav_bwd_lse(c
           const int tc = t < 0 ? 0 : (t > thi ? thi : t);  // clamped loads: no branches
           gv[k] = ld_na(cot + tc);
           mv[k] = ld_na(outr + tc);
-          lv[k] = lor ? ld_na(lor + tc) : 0.f;
+          lv[k] = lor ? lo_ld(lor + tc) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < CAV_LB; ++k) {

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 1) k_reg_fwd(const _
   if (t0 >= nvalid) {  // every output of the tile overruns
     for (int i = tid; i < tend; i += T) outr[t0 + i] = __fadd_rn(padv, czero);
     if (RK == RK_LSE && p.aux != nullptr)
-      for (int i = tid; i < tend; i += T) p.aux[row * L + t0 + i] = 0.f;
+      for (int i = tid; i < tend; i += T) reinterpret_cast<unsigned short*>(p.aux + row * L)[t0 + i] = 0;
     return;
   }
   // phase 1: coalesced loads, child values -> P0 (transpose buffer)
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB + 1) k_reg_fwd(const _
 #pragma unroll
     for (int k = 0; k < RG_EPT; ++k)
       if (tid + k * T < tend) op[k * T] = src[k * SS];
-    if (RK == RK_LSE && p.aux != nullptr) {  // low word of the double-float trace
+    if (RK == RK_LSE && p.aux != nullptr) {  // low word of the double-float trace (bf16 plane)
       const float* src1 = P1 + rpad(tid + K - 1);
-      float* ap = p.aux + row * L + t0 + tid;
+      unsigned short* ap = reinterpret_cast<unsigned short*>(p.aux + row * L) + t0 + tid;
 #pragma unroll
       for (int k = 0; k < RG_EPT; ++k)
-        if (tid + k * T < tend) ap[k * T] = src1[k * SS];
+        if (tid + k * T < tend) ap[k * T] = lo_pack(src1[k * SS]);
     }
   }
 }
@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_lse(const
   const float tau2 = p.mp.tau2, sg = p.sg;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
-  const float* lor = p.aux_in ? p.aux_in + row * L : nullptr;  // low word of M (double-float)
+  const unsigned short* lor =  // low word of M (double-float, bf16 plane)
+      p.aux_in ? reinterpret_cast<const unsigned short*>(p.aux_in + row * L) : nullptr;
   const int tid = threadIdx.x;
   // phase 1: elements (-M_t, g_t) for t in [tb, tb + N); identity outside [0, nvalid)
   {
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_lse(const
         for (int k = 0; k < 8; ++k) {
           gv[k] = ld_na(cot + tt + (h + k) * T);
           mv[k] = ld_na(outr + tt + (h + k) * T);
-          lv[k] = lor ? ld_na(lor + tt + (h + k) * T) : 0.f;
+          lv[k] = lor ? lo_ld(lor + tt + (h + k) * T) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_lse(const
           const bool v = t >= 0 && t < nvalid;
           gv[k] = v ? ld_na(cot + t) : 0.f;
           mv[k] = v ? ld_na(outr + t) : 0.f;
-          lv[k] = (v && lor) ? ld_na(lor + t) : 0.f;
+          lv[k] = (v && lor) ? lo_ld(lor + t) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

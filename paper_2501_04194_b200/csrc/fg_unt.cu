@@ -149,10 +149,10 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 4) k_unt_fwd(const __grid_
 #pragma unroll
       for (int k = 0; k < RG_EPT; ++k) P[q0 + k] = lo[k];
       __syncthreads();
-      float* ap = p.aux + row * L + c0 + tid;
+      unsigned short* ap = reinterpret_cast<unsigned short*>(p.aux + row * L) + c0 + tid;  // bf16 plane
 #pragma unroll
       for (int k = 0; k < RG_EPT; ++k)
-        if (tid + k * T < nt) ap[k * T] = src[k * SS];
+        if (tid + k * T < nt) ap[k * T] = lo_pack(src[k * SS]);
     }
     __syncthreads();
   }
@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 3) k_unt_bwd_lse(const __g
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* cot = p.cot + row * L;
   const float* outr = p.out_in + row * L;
-  const float* lor = p.aux_in != nullptr ? p.aux_in + row * L : nullptr;  // trace low word
+  const unsigned short* lor =  // trace low word (bf16 plane)
+      p.aux_in != nullptr ? reinterpret_cast<const unsigned short*>(p.aux_in + row * L) : nullptr;
   Ev<M_LSE, EK> ev(p.child, row, p.mp);
   const RSt id = rident<RK_GLSE>();
   const int so = tid + (tid >> 4), q0 = tid * (RG_EPT + 1), i0 = tid * RG_EPT;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(RC<NW>::T, LB ? 8 : 3) k_unt_bwd_lse(const __g
         const int tc = t < L ? t : L - 1;
         gv[k] = ld_na(cot + tc);
         mv[k] = ld_na(outr + tc);
-        lv[k] = lor != nullptr ? ld_na(lor + tc) : 0.f;
+        lv[k] = lor != nullptr ? lo_ld(lor + tc) : 0.f;
       }
       // M = hi + lo: the low word rides in the weight, g 2^{-tau2 lo} (|tau2 lo| << 1)
 #pragma unroll

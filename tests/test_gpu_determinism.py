@@ -26,6 +26,12 @@ CASES = [
     ("F_smooth_soft", P.Eventually(P.Pred("x", ">", 0.0), SI), P.SoftMax(2.0)),
     ("nested_hard", P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 30))),
                           P.Until(P.Pred("y", "<", 1.0), P.Pred("x", ">", 0.0))), P.Hard()),
+    # independent operands (no shared channel): the executor runs them on two streams
+    ("lanes_hard", P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 30))),
+                         P.Until(P.Pred("y", "<", 1.0), P.Pred("z", ">", 0.0))), P.Hard()),
+    ("lanes_lse", P.Or(P.Or(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(2, 50)),
+                            P.Always(P.Pred("y", "<", 1.0))),
+                       P.Eventually(P.Pred("z", ">", 0.5))), P.LogSumExp(4.0)),
 ]
 
 
@@ -36,13 +42,15 @@ def test_backward_bitwise_reproducible(cuda, name, f, mode):
     B, T = 64, 1500
     x = torch.randn(B, T, device="cuda", generator=g)
     y = torch.randn(B, T, device="cuda", generator=g)
+    z = torch.randn(B, T, device="cuda", generator=g)
     if "hard" in name:  # ties, so the first-arg-max runs are long and cross tiles
-        x, y = torch.round(x * 2), torch.round(y * 2)
+        x, y, z = torch.round(x * 2), torch.round(y * 2), torch.round(z * 2)
     cot = torch.randn(B, T, device="cuda", generator=g)
     names = sorted(P.variables(f))
     runs = []
     for _ in range(2):
-        chans = {"x": x.clone().requires_grad_(True), "y": y.clone().requires_grad_(True)}
+        chans = {"x": x.clone().requires_grad_(True), "y": y.clone().requires_grad_(True),
+                 "z": z.clone().requires_grad_(True)}
         chans = {k: chans[k] for k in names}
         smooth = "smooth" in name
         abc = tuple(torch.tensor(v, dtype=torch.float64, device="cuda", requires_grad=True)

@@ -105,6 +105,31 @@ def test_random_formulas_vs_oracle(cuda, seed):
     _check(type(mode).__name__, tr, {k: g[k] for k in ref_g}, ref_tr, ref_g, cot)
 
 
+@pytest.mark.parametrize("seed", range(16))
+def test_independent_operands_vs_oracle(cuda, seed):
+    """Root And / Or over operands on disjoint channels: the executor deals them to two
+    streams with per-lane scratch (exec.cu assign_lanes); same results as the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    mode = MODES[seed % len(MODES)]
+    cfg = P.SemanticsConfig(mode=mode, top_value=100.0)
+    ops = [P.Eventually(_rand_formula(rng, 1, chans=("x",)), P.StepInterval(int(rng.integers(0, 5)), int(rng.integers(6, 60)))),
+           _rand_formula(rng, 2, chans=("y", "z")),
+           P.Always(_rand_formula(rng, 1, chans=("w",)))]
+    f = P.And(ops[0], ops[1]) if seed % 2 else P.Or(ops[0], ops[1])
+    if seed % 3 == 0:
+        f = P.And(f, ops[2]) if seed % 2 else P.Or(ops[2], f)
+    if not device_supports(f, cfg):
+        pytest.skip("operator not on the device path in this build")
+    B, L = 3, int(rng.integers(60, 400))
+    arrays = {c: np.asarray(rng.normal(0, 1.5, (B, L)), dtype=np.float32).astype(np.float64)
+              for c in ("x", "y", "z", "w")}
+    arrays = {c: arrays[c] for c in sorted(P.variables(f))}
+    cot = np.asarray(rng.normal(0, 1, (B, L)), dtype=np.float32).astype(np.float64)
+    ref_tr, ref_g, _ = stl_oracle.trace_and_grad(f, arrays, cfg, cot)
+    tr, g, _ = run_device(f, arrays, cfg, cot)
+    _check(type(mode).__name__, tr, {k: g[k] for k in ref_g}, ref_tr, ref_g, cot)
+
+
 # --- headline shapes: full size on device, rows sampled for the oracle ----------------
 
 def _walk(B, T, seed):

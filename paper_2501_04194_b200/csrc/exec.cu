@@ -562,6 +562,11 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
     if (cfg->mode == STLG_MODE_HARD && e.kind == E_FG_TIMED && !cfg->masked_fill &&
         e.b - e.a + 1 >= 17 && e.b - e.a + 1 <= 1024)
       e.aux_slot = plan->n_aux++;
+    // hard timed Until on the O(T) kernels: every output's gradient source (uint16 plane),
+    // so the backward routes cotangents without restaging the children or re-walking blocks
+    if (cfg->mode == STLG_MODE_HARD && e.kind == E_UNTIL && !e.untimed && !cfg->masked_fill &&
+        e.b <= 0x7fff)
+      e.aux_slot = plan->n_aux++;
     // softmax smooth intervals: [L_hi | M_lo | L_lo] (double-float window LSE and mean)
     if (cfg->mode == STLG_MODE_SOFTMAX && e.kind == E_FG_SMOOTH) plan->n_aux += 2;
     e.out_slot = (i == root) ? -1 : C.new_slot();
@@ -878,6 +883,7 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
       p.sent = (float)plan->cfg.sentinel;
       if (p.fill) p.canon = 0;  // no _replace_overrun in masked_fill mode (masking.py:261-274)
       p.mp = mode_params(plan->cfg);
+      p.src = e.aux_slot >= 0 ? reinterpret_cast<unsigned short*>(bf.auxp(e.aux_slot)) : nullptr;
       ce = launch_until_fwd(mode, p, st);
     } else {  // E_FG_SMOOTH
       if ((rc = run_smooth(plan, e, channels, nullptr, B, T, smooth_params, bf, out, nullptr,
@@ -959,6 +965,7 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
       p.dscale = bf.dscale;
       p.lb = bf.lb;
       p.mp = mode_params(plan->cfg);
+      p.src_in = e.aux_slot >= 0 ? reinterpret_cast<const unsigned short*>(bf.auxp(e.aux_slot)) : nullptr;
       ce = launch_until_bwd(mode, p, st);
     } else {  // E_FG_SMOOTH
       if ((rc = run_smooth(plan, e, channels, d_channels, B, T, smooth_params, bf, nullptr, out_in,

@@ -47,6 +47,8 @@ struct UParams {
   unsigned long long* dacc;  // backward: reproducible accumulators [4][B, L] (detacc.cuh)
   int* dscale;               // backward: per-row grid exponents [B]
   unsigned* lb;              // untimed hard: look-back slots [B][tiles][LB_WORDS] (lookback.cuh)
+  unsigned short* src;            // forward, hard timed (until_ht.cu): gradient source of every
+  const unsigned short* src_in;   // output as (offset from t) | 0x8000 right child; 0xffff overrun
   ModeP mp;
 };
 

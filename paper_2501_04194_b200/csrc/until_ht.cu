@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant_
   const HTArr A = ht_carve(htsm, NS, p.K);
   ht_prepare(p, row, t0, NS, A);
   float* outr = p.out + row * L;
+  unsigned short* srcr = p.src != nullptr ? p.src + row * L : nullptr;
   const int tend = min(t0 + NT, L);
   for (int t = t0 + (int)threadIdx.x; t < tend; t += HT_T) {
     float o;
@@ -305,7 +306,9 @@ __global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant_
       const int d = ht_source(p, t0, t, A);
       const float2 v = A.at((d & (HT_R - 1)) - t0);
       o = (d & HT_R) ? v.y : v.x;
+      if (srcr) srcr[t] = (unsigned short)(((d & (HT_R - 1)) - t) | ((d & HT_R) ? 0x8000 : 0));
     } else {  // overrun: hard min of the pad values, a tie keeps the left (reference.py:189)
+      if (srcr) srcr[t] = 0xffff;
       float pl = p.pad_value, pr = p.pad_value;
       if (p.pad_last) {
         pl = expr_eval<M_HARD>(p.left, row, L - 1, p.mp);
@@ -402,6 +405,79 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
   }
 }
 
+// Backward from the forward's stored sources (p.src_in): the CTA owning child elements
+// [t0, t0 + HS_NT) reads the cotangents and sources of the outputs [t0 - b, t0 + HS_NT) —
+// 6 B per output, no child staging, no block walks — and sums them in shared int64 fixed
+// point at a per-tile power-of-two scale (reproducible, as k_until_ht_bwd).
+constexpr int HS_NT = 2048;
+__global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant__ UParams p) {
+  __shared__ unsigned long long acc[2 * HS_NT];  // [left | right]
+  __shared__ float gred[HT_T / 32];
+  const long long row = blockIdx.y;
+  const int L = (int)p.L;
+  const int t0 = blockIdx.x * HS_NT;
+  const int tlo = max(t0 - p.b, 0), thi = min(t0 + HS_NT, L);
+  const float* cot = p.cot + row * L;
+  const unsigned short* src = p.src_in + row * L;
+  for (int i = threadIdx.x; i < 2 * HS_NT; i += HT_T) acc[i] = 0ull;
+  float gm = 0.f;
+  for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
+    const float ag = fabsf(cot[t]);
+    gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
+  }
+  for (int o = 16; o > 0; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+  if ((threadIdx.x & 31) == 0) gred[threadIdx.x >> 5] = gm;
+  __syncthreads();
+  gm = gred[0];
+  for (int w = 1; w < HT_T / 32; ++w) gm = fmaxf(gm, gred[w]);
+  int ge = 0;
+  frexp((double)gm * (double)(thi - tlo + 1), &ge);  // sum |g| < 2^ge
+  const double scale = ldexp(1.0, 62 - ge), inv = ldexp(1.0, ge - 62);
+  int padsrc = -1;  // overrun outputs: source of min(pad_l, pad_r) ('last' padding only)
+  if (p.pad_last && thi - 1 + p.b > L - 1) {
+    const float pl = expr_eval<M_HARD>(p.left, row, L - 1, p.mp);
+    const float pr = expr_eval<M_HARD>(p.right, row, L - 1, p.mp);
+    padsrc = (pl <= pr) ? (L - 1) : ((L - 1) | HT_R);
+  }
+  auto source = [&](int t) {
+    const unsigned s = src[t];
+    return s == 0xffffu ? padsrc : (int)(t + (s & 0x7fffu)) | ((s & 0x8000u) ? HT_R : 0);
+  };
+  const bool nonfinite = !(gm < INFINITY);  // inf / NaN cotangents: plain (ordered) sums
+  if (gm > 0.f && !nonfinite) {
+    for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
+      const float g = cot[t];
+      if (g == 0.f) continue;
+      const int d = source(t);
+      if (d < 0) continue;
+      const int j = (d & (HT_R - 1)) - t0;
+      if (j < 0 || j >= HS_NT) continue;
+      ht_add64(&acc[((d & HT_R) ? HS_NT : 0) + j], (unsigned long long)llrint((double)g * scale));
+    }
+  }
+  __syncthreads();
+  float* gl = p.gl + row * L;
+  float* gr = p.gr + row * L;
+  for (int j = t0 + (int)threadIdx.x; j < thi; j += HT_T) {
+    if (!nonfinite) {
+      gl[j] = (float)((double)(long long)acc[j - t0] * inv);
+      gr[j] = (float)((double)(long long)acc[HS_NT + j - t0] * inv);
+    } else {  // sequential over the candidate outputs in t order (rare: non-finite g)
+      float sl = 0.f, sr = 0.f;
+      for (int t = max(j - p.b, 0); t <= j; ++t) {
+        const float g = cot[t];
+        if (g == 0.f) continue;
+        const int d = source(t);
+        if (d < 0 || (d & (HT_R - 1)) != j) continue;
+        if (d & HT_R) sr += g;
+        else sl += g;
+      }
+      gl[j] = sl;
+      gr[j] = sr;
+    }
+  }
+}
+
 // true when the O(T) kernels apply (hard, timed, no masked_fill, staging fits)
 bool until_ht_applicable(const UParams& p) {
   if (p.untimed || p.fill || p.K < 1 || p.L >= (1LL << 29)) return false;
@@ -422,6 +498,12 @@ cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
 
 // writes every element of p.gl / p.gr (the caller runs the child VJPs)
 cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st) {
+  if (p.src_in != nullptr) {  // the forward stored every output's source
+    dim3 grid((unsigned)((p.L + HS_NT - 1) / HS_NT), (unsigned)p.B);
+    k_until_ht_bwd_src<<<grid, HT_T, 0, st>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
   const int NS = ht_ns(2 * p.b), NT = NS - 2 * p.b;
   const size_t smem = ht_smem_bytes(NS) + (size_t)NT * 16;
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

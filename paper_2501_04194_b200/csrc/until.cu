@@ -1683,6 +1683,7 @@ static cudaError_t until_bwd_mode(UParams& p, cudaStream_t st) {
   }
   cudaError_t e;
   if (MODE == M_HARD && until_ht_applicable(p)) {  // O(T), deterministic (until_ht.cu)
+    if (p.src_in != nullptr) return launch_until_ht_bwd(p, st);  // stored sources, fused child VJPs
     if ((e = launch_until_ht_bwd(p, st)) != cudaSuccess) return e;
   } else {
   if (p.dacc == nullptr || p.dscale == nullptr) return cudaErrorInvalidValue;

@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
 // Backward from the forward's stored sources (p.src_in): the CTA owning child elements
 // [t0, t0 + HS_NT) reads the cotangents and sources of the outputs [t0 - b, t0 + HS_NT) —
 // 6 B per output, no child staging, no block walks — and sums them in shared int64 fixed
-// point at a per-tile power-of-two scale (reproducible, as k_until_ht_bwd).
+// point at a per-tile power-of-two scale (reproducible, as k_until_ht_bwd), then runs the
+// children's VJPs on the owned elements (left first: first-writer order) — no gl / gr pass.
 constexpr int HS_NT = 2048;
 __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant__ UParams p) {
   __shared__ unsigned long long acc[2 * HS_NT];  // [left | right]
@@ -456,12 +457,11 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant
     }
   }
   __syncthreads();
-  float* gl = p.gl + row * L;
-  float* gr = p.gr + row * L;
+  const ChildEval cl(p.left, row), cr(p.right, row);
   for (int j = t0 + (int)threadIdx.x; j < thi; j += HT_T) {
     if (!nonfinite) {
-      gl[j] = (float)((double)(long long)acc[j - t0] * inv);
-      gr[j] = (float)((double)(long long)acc[HS_NT + j - t0] * inv);
+      cl.grad<M_HARD>(j, (float)((double)(long long)acc[j - t0] * inv), p.mp);
+      cr.grad<M_HARD>(j, (float)((double)(long long)acc[HS_NT + j - t0] * inv), p.mp);
     } else {  // sequential over the candidate outputs in t order (rare: non-finite g)
       float sl = 0.f, sr = 0.f;
       for (int t = max(j - p.b, 0); t <= j; ++t) {
@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant
         if (d & HT_R) sr += g;
         else sl += g;
       }
-      gl[j] = sl;
-      gr[j] = sr;
+      cl.grad<M_HARD>(j, sl, p.mp);
+      cr.grad<M_HARD>(j, sr, p.mp);
     }
   }
 }
@@ -496,7 +496,8 @@ cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// writes every element of p.gl / p.gr (the caller runs the child VJPs)
+// with p.src_in: runs the child VJPs itself; else writes every element of p.gl / p.gr
+// (the caller runs the child VJPs)
 cudaError_t launch_until_ht_bwd(UParams& p, cudaStream_t st) {
   if (p.src_in != nullptr) {  // the forward stored every output's source
     dim3 grid((unsigned)((p.L + HS_NT - 1) / HS_NT), (unsigned)p.B);

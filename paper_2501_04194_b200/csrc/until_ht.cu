@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(HT_T, 4) k_until_ht_bwd(const __grid_constant_
 // point at a per-tile power-of-two scale (reproducible, as k_until_ht_bwd), then runs the
 // children's VJPs on the owned elements (left first: first-writer order) — no gl / gr pass.
 constexpr int HS_NT = 2048;
+constexpr int HS_R = (HS_NT + HT_T) / HT_T;  // outputs per thread held in registers (b <= HT_T)
 __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant__ UParams p) {
   __shared__ unsigned long long acc[2 * HS_NT];  // [left | right]
   __shared__ float gred[HT_T / 32];
@@ -420,9 +421,23 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant
   const int tlo = max(t0 - p.b, 0), thi = min(t0 + HS_NT, L);
   const float* cot = p.cot + row * L;
   const unsigned short* src = p.src_in + row * L;
+  // the first HS_R HT_T outputs: one batch of loads into registers; the rest (b > HT_T) in a loop
+  float gv[HS_R];
+  unsigned short sv[HS_R];
+#pragma unroll
+  for (int k = 0; k < HS_R; ++k) {
+    const int t = tlo + (int)threadIdx.x + k * HT_T;
+    gv[k] = t < thi ? cot[t] : 0.f;
+    sv[k] = t < thi ? src[t] : (unsigned short)0xffffu;
+  }
   for (int i = threadIdx.x; i < 2 * HS_NT; i += HT_T) acc[i] = 0ull;
   float gm = 0.f;
-  for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
+#pragma unroll
+  for (int k = 0; k < HS_R; ++k) {
+    const float ag = fabsf(gv[k]);
+    gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
+  }
+  for (int t = tlo + (int)threadIdx.x + HS_R * HT_T; t < thi; t += HT_T) {
     const float ag = fabsf(cot[t]);
     gm = (ag == ag) ? fmaxf(gm, ag) : INFINITY;
   }
@@ -440,21 +455,24 @@ __global__ void __launch_bounds__(HT_T) k_until_ht_bwd_src(const __grid_constant
     const float pr = expr_eval<M_HARD>(p.right, row, L - 1, p.mp);
     padsrc = (pl <= pr) ? (L - 1) : ((L - 1) | HT_R);
   }
-  auto source = [&](int t) {
-    const unsigned s = src[t];
+  auto source_of = [&](int t, unsigned s) {
     return s == 0xffffu ? padsrc : (int)(t + (s & 0x7fffu)) | ((s & 0x8000u) ? HT_R : 0);
+  };
+  auto source = [&](int t) { return source_of(t, src[t]); };
+  auto route = [&](int t, float g, int d) {
+    if (g == 0.f || d < 0) return;
+    const int j = (d & (HT_R - 1)) - t0;
+    if (j < 0 || j >= HS_NT) return;
+    ht_add64(&acc[((d & HT_R) ? HS_NT : 0) + j], (unsigned long long)llrint((double)g * scale));
   };
   const bool nonfinite = !(gm < INFINITY);  // inf / NaN cotangents: plain (ordered) sums
   if (gm > 0.f && !nonfinite) {
-    for (int t = tlo + (int)threadIdx.x; t < thi; t += HT_T) {
-      const float g = cot[t];
-      if (g == 0.f) continue;
-      const int d = source(t);
-      if (d < 0) continue;
-      const int j = (d & (HT_R - 1)) - t0;
-      if (j < 0 || j >= HS_NT) continue;
-      ht_add64(&acc[((d & HT_R) ? HS_NT : 0) + j], (unsigned long long)llrint((double)g * scale));
+#pragma unroll
+    for (int k = 0; k < HS_R; ++k) {
+      const int t = tlo + (int)threadIdx.x + k * HT_T;
+      if (t < thi) route(t, gv[k], source_of(t, sv[k]));
     }
+    for (int t = tlo + (int)threadIdx.x + HS_R * HT_T; t < thi; t += HT_T) route(t, cot[t], source(t));
   }
   __syncthreads();
   const ChildEval cl(p.left, row), cr(p.right, row);

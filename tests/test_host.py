@@ -154,6 +154,21 @@ def test_compile_and_plan_info_without_gpu():
     assert fb >= 3 * 256 * 4000 * 4 and bb >= 3 * 256 * 4000 * 4
 
 
+def test_independent_operands_get_a_second_lane():
+    """exec.cu assign_lanes: operands under the root that share no channel, slot or smooth
+    binding run on two streams, each lane with its own scratch — visible through the C ABI
+    as one more lane block in both workspaces.  A shared channel keeps one lane."""
+    cfg = P.SemanticsConfig()
+    left = P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 200)))
+    two = P.compile_formula(P.And(left, P.Until(P.Pred("y", "<", 1.0), P.Pred("z", ">", 0.0))),
+                            ["x", "y", "z"], cfg)
+    one = P.compile_formula(P.And(left, P.Until(P.Pred("y", "<", 1.0), P.Pred("x", ">", 0.5))),
+                            ["x", "y", "z"], cfg)
+    B, T = 64, 5000
+    (f2, b2), (f1, b1) = two.workspace_bytes(B, T), one.workspace_bytes(B, T)
+    assert f2 > f1 and b2 - b1 >= 3 * B * T * 4
+
+
 def test_compile_errors_map_to_reference_exceptions():
     lib = _lib.load()
     arr = (_lib.StlgNode * 1)()

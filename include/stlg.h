@@ -32,6 +32,12 @@
  *     raised in Python before the call, at the reference's own sites.
  *   - Functions are reentrant; a plan is immutable after stlg_compile and may
  *     be used concurrently on different streams with different workspaces.
+ *   - Plans whose root joins independent operands (no shared channel, slot or
+ *     smooth binding) run one operand group on an internal side stream (one
+ *     per host thread and device), forked from `stream` and joined back into
+ *     it with events before the call returns: all work is ordered on `stream`
+ *     as before, and under stream capture the two groups become parallel
+ *     graph branches.  Their workspaces hold one more lane of scratch.
  */
 #ifndef STLG_H
 #define STLG_H

@@ -78,12 +78,13 @@ __device__ __forceinline__ float4 hs_pack(const HS& s) {
 __device__ __forceinline__ HS hs_unpack(const float4 v) {
   return HS{v.x, v.y, __float_as_int(v.z), __float_as_int(v.w)};
 }
-// mb[bk]: the state of the MB whole blocks bk+1 .. bk+MB (MB = (K-1)/32 - 1 when >= 3):
-// a window then costs suffix + mb + at most one more whole block + prefix — O(1)
-// combines per output for any K instead of O(K/32)
+// mb[bk]: the state of the MB whole blocks bk+1 .. bk+MB (MB = (K-1)/32 - 1 when >= 2),
+// mb1[bk] the same over MB + 1 blocks: a window of K samples spans MB or MB + 1 whole
+// blocks, so it costs suffix + mb / mb1 + prefix — two combines per output for any K
+// instead of O(K/32), and no loop
 struct HTArr {
   float2* lr;
-  float4 *sf, *pf, *mb;
+  float4 *sf, *pf, *mb, *mb1;
   int MB;
   __device__ __forceinline__ HS suf(int i) const { return hs_unpack(sf[ht_pad(i)]); }
   __device__ __forceinline__ HS pre(int i) const { return hs_unpack(pf[ht_pad(i)]); }
@@ -91,18 +92,19 @@ struct HTArr {
 };
 
 __host__ __device__ __forceinline__ int ht_padded(int NS) { return ((NS + 31) >> 5) * 33; }
-// 32-bit words of the staged arrays: mb (nb float4), then sf / pf (float4) and lr (float2)
-__host__ __device__ __forceinline__ int ht_words(int NS) { return ((NS + 31) >> 5) * 4 + ht_padded(NS) * 10; }
+// 32-bit words of the staged arrays: mb, mb1 (nb float4 each), then sf / pf (float4) and lr (float2)
+__host__ __device__ __forceinline__ int ht_words(int NS) { return ((NS + 31) >> 5) * 8 + ht_padded(NS) * 10; }
 
 __device__ __forceinline__ HTArr ht_carve(float* base, int NS, int K) {
   const int NP = ht_padded(NS);
   HTArr A;
   A.mb = reinterpret_cast<float4*>(base);
-  A.sf = A.mb + ((NS + 31) >> 5);
+  A.mb1 = A.mb + ((NS + 31) >> 5);
+  A.sf = A.mb1 + ((NS + 31) >> 5);
   A.pf = A.sf + NP;
   A.lr = reinterpret_cast<float2*>(A.pf + NP);
   const int mb = (K - 1) / 32 - 1;
-  A.MB = mb >= 3 ? mb : 0;  // (at K ~ 100 the one combine saved per output does not pay)
+  A.MB = mb >= 2 ? mb : 0;
   return A;
 }
 
@@ -206,11 +208,12 @@ __device__ void ht_prepare(const UParams& p, long long row, int base, int NS, co
     }
   }
   __syncthreads();
-  if (A.MB > 0) {  // the MB-block aggregates (only read where bk + MB < nb)
+  if (A.MB > 0) {  // the MB- and (MB+1)-block aggregates (only read where they exist)
     for (int bk = threadIdx.x; bk + A.MB < nb; bk += HT_T) {
       HS s = A.pre((bk + 1) * 32 + 31);
       for (int j = 2; j <= A.MB; ++j) s = hs_comb(s, A.pre((bk + j) * 32 + 31));
       A.mb[bk] = hs_pack(s);
+      if (bk + A.MB + 1 < nb) A.mb1[bk] = hs_pack(hs_comb(s, A.pre((bk + A.MB + 1) * 32 + 31)));
     }
     __syncthreads();
   }
@@ -229,8 +232,11 @@ __device__ __forceinline__ HS ht_range(const HTArr& A, int i0, int i1, int base)
     return s;
   }
   HS s = A.suf(i0);
+  const int m = b1 - b0 - 1;  // whole blocks between
+  if (A.MB > 0 && m == A.MB) return hs_comb(hs_comb(s, hs_unpack(A.mb[b0])), A.pre(i1));
+  if (A.MB > 0 && m == A.MB + 1) return hs_comb(hs_comb(s, hs_unpack(A.mb1[b0])), A.pre(i1));
   int bk = b0 + 1;
-  if (A.MB > 0 && b1 - b0 - 1 >= A.MB) {
+  if (A.MB > 0 && m >= A.MB) {
     s = hs_comb(s, hs_unpack(A.mb[b0]));
     bk += A.MB;
   }

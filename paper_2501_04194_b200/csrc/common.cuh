@@ -95,10 +95,10 @@ __device__ __forceinline__ float ld_na(const float* p) {
 // bf16 plane in the first half of the row's aux words: 2 B per sample instead of 4 in the
 // forward's write and the backward's read.  Rounding lo to 8 bits moves M by at most
 // 2^-9 |lo| <= 2^-10 ulp(hi), far below the fp32 rounding the low word corrects.
-__device__ __forceinline__ unsigned short lo_pack(float v) {
-  unsigned u = __float_as_uint(v);  // finite, |v| tiny: round to nearest even cannot overflow
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return (unsigned short)(u >> 16);
+__device__ __forceinline__ unsigned short lo_pack(float v) {  // round to nearest even, one F2F
+  unsigned short h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(v));
+  return h;
 }
 __device__ __forceinline__ float lo_ld(const unsigned short* p) {
   unsigned short h;

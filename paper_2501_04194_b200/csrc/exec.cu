@@ -845,12 +845,12 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
   if (fk && (rc = cuda_status(fork_begin(fk, st0), "fork"))) return rc;
   const int mode = plan->cfg.mode;
   const int n_entries = (int)plan->entries.size();
-  for (int ei = 0; ei < n_entries; ++ei) {
+  bool open = fk != nullptr;  // side-stream work not yet joined into st0
+  auto fwd_entry = [&](int ei) -> int {
     const Entry& e = plan->entries[ei];
     const int ln = plan->lane[ei];
     const Bufs& bf = bfl[ln];
     cudaStream_t st = (fk && ln == 1) ? fk->side : st0;
-    if (fk && ei == n_entries - 1 && (rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
     float* out = e.out_slot < 0 ? trace_out : bf.slot(e.out_slot);
     cudaError_t ce = cudaSuccess;
     if (e.kind == E_POINTWISE || e.kind == E_FG_TIMED || e.kind == E_FG_UNTIMED) {
@@ -891,6 +891,17 @@ int stlg_forward(const stlg_plan* plan, const stlg_channel* channels, int64_t B,
         return rc;
     }
     if ((rc = cuda_status(ce, "forward launch"))) return rc;
+    return STLG_OK;
+  };
+  for (int ei = 0; ei < n_entries; ++ei) {
+    if (open && ei == n_entries - 1) {
+      open = false;
+      if ((rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
+    }
+    if ((rc = fwd_entry(ei))) {
+      if (open) fork_end(fk, st0);  // best effort: nothing on the side stream outlives the call
+      return rc;
+    }
   }
   return STLG_OK;
 }
@@ -920,12 +931,12 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
   }
   const Fork* fk = plan->n_lanes > 1 ? fork_for(st0) : nullptr;
   const int n_entries = (int)plan->entries.size();
-  for (int ei = n_entries - 1; ei >= 0; --ei) {
+  bool open = false;  // side-stream work not yet joined into st0
+  auto bwd_entry = [&](int ei) -> int {
     const Entry& e = plan->entries[ei];
     const int ln = plan->lane[ei];
     const Bufs& bf = bfl[ln];
     cudaStream_t st = (fk && ln == 1) ? fk->side : st0;
-    if (fk && ei == n_entries - 2 && (rc = cuda_status(fork_begin(fk, st0), "fork"))) return rc;
     const float* g = e.out_slot < 0 ? cot : bf.gslot(e.out_slot);
     const float* out_in = e.out_slot < 0 ? trace : bf.slot(e.out_slot);
     cudaError_t ce = cudaSuccess;
@@ -973,8 +984,19 @@ int stlg_backward(const stlg_plan* plan, const stlg_channel* channels, int64_t B
         return rc;
     }
     if ((rc = cuda_status(ce, "backward launch"))) return rc;
+    return STLG_OK;
+  };
+  for (int ei = n_entries - 1; ei >= 0; --ei) {
+    if (fk && ei == n_entries - 2) {
+      if ((rc = cuda_status(fork_begin(fk, st0), "fork"))) return rc;
+      open = true;
+    }
+    if ((rc = bwd_entry(ei))) {
+      if (open) fork_end(fk, st0);  // best effort: nothing on the side stream outlives the call
+      return rc;
+    }
   }
-  if (fk && (rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
+  if (open && (rc = cuda_status(fork_end(fk, st0), "join"))) return rc;
   return STLG_OK;
 }
 

@@ -158,8 +158,10 @@ def compile_formula(f, channel_names, cfg) -> Compiled:
 # autograd
 # ---------------------------------------------------------------------------
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(dev):
+    """The current stream of the tensors' device (the library launches on the current
+    device, so callers hold `torch.cuda.device(dev)` around the call)."""
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
 # rows per library call: the kernels index rows on grid.y (stlg_forward rejects
@@ -179,12 +181,13 @@ class _TraceFn(torch.autograd.Function):
         out = torch.empty((B, T), dtype=torch.float32, device=dev)
         fws_list = []
         bb_list = []
-        for r0, r1 in _row_chunks(B):
-            fb, bb = comp.workspace_bytes(r1 - r0, T)
-            fws = torch.empty(fb, dtype=torch.uint8, device=dev)
-            comp.forward([c[r0:r1] for c in chans], params, out[r0:r1], fws, _stream())
-            fws_list.append(fws)
-            bb_list.append(bb)
+        with torch.cuda.device(dev):
+            for r0, r1 in _row_chunks(B):
+                fb, bb = comp.workspace_bytes(r1 - r0, T)
+                fws = torch.empty(fb, dtype=torch.uint8, device=dev)
+                comp.forward([c[r0:r1] for c in chans], params, out[r0:r1], fws, _stream(dev))
+                fws_list.append(fws)
+                bb_list.append(bb)
         ctx.comp = comp
         ctx.params = params
         ctx.bwd_bytes = bb_list
@@ -205,17 +208,18 @@ class _TraceFn(torch.autograd.Function):
         dch = [torch.empty((B, T), dtype=torch.float32, device=dev)
                if ctx.needs_input_grad[3 + i] else None for i in range(len(chans))]
         d_total = None
-        for (r0, r1), fws, bb in zip(_row_chunks(B), fws_list, ctx.bwd_bytes):
-            d_smooth = None
-            # the d/dw pass runs only when a bound (a, b, c) tensor asks for its gradient
-            if comp.n_smooth and ctx.needs_input_grad[2]:
-                d_smooth = torch.zeros(3 * comp.n_smooth, dtype=torch.float64, device=dev)
-            bws = torch.empty(bb, dtype=torch.uint8, device=dev)
-            comp.backward([c[r0:r1] for c in chans], ctx.params, out[r0:r1], g[r0:r1],
-                          [d[r0:r1] if d is not None else None for d in dch], d_smooth, fws, bws,
-                          _stream())
-            if d_smooth is not None:
-                d_total = d_smooth if d_total is None else d_total + d_smooth
+        with torch.cuda.device(dev):
+            for (r0, r1), fws, bb in zip(_row_chunks(B), fws_list, ctx.bwd_bytes):
+                d_smooth = None
+                # the d/dw pass runs only when a bound (a, b, c) tensor asks for its gradient
+                if comp.n_smooth and ctx.needs_input_grad[2]:
+                    d_smooth = torch.zeros(3 * comp.n_smooth, dtype=torch.float64, device=dev)
+                bws = torch.empty(bb, dtype=torch.uint8, device=dev)
+                comp.backward([c[r0:r1] for c in chans], ctx.params, out[r0:r1], g[r0:r1],
+                              [d[r0:r1] if d is not None else None for d in dch], d_smooth, fws, bws,
+                              _stream(dev))
+                if d_smooth is not None:
+                    d_total = d_smooth if d_total is None else d_total + d_smooth
         dabc = None
         if ctx.needs_input_grad[2] and d_total is not None:
             dabc = d_total.view(-1, 3).sum(0)

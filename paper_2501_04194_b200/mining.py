@@ -141,11 +141,12 @@ def _grid(x, a, b, sharp, eps, gamma, cfg, with_grad=False):
     mode, temp = _mode_code(cfg)
     loss = torch.empty(a.numel(), dtype=torch.float64, device=x.device)
     dl = torch.empty(2 * a.numel(), dtype=torch.float64, device=x.device) if with_grad else None
-    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    _lib.check(lib.stlg_mining_grid(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), a.data_ptr(),
-                                    b.data_ptr(), a.numel(), float(sharp), float(eps), mode, temp,
-                                    float(gamma), loss.data_ptr(),
-                                    dl.data_ptr() if dl is not None else None, stream))
+    with torch.cuda.device(x.device):
+        stream = ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+        _lib.check(lib.stlg_mining_grid(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), a.data_ptr(),
+                                        b.data_ptr(), a.numel(), float(sharp), float(eps), mode, temp,
+                                        float(gamma), loss.data_ptr(),
+                                        dl.data_ptr() if dl is not None else None, stream))
     return loss, (dl.view(-1, 2) if dl is not None else None)
 
 

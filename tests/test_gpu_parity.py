@@ -363,3 +363,63 @@ def test_smooth_interval_graph_capture(cuda):
     torch.cuda.synchronize()
     for a, b in zip(eager, cap):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("mode", [P.Hard(), P.LogSumExp(5.0)], ids=["hard", "lse5"])
+def test_two_lane_plan_graph_capture(cuda, mode):
+    """Independent operands run on a library side stream forked from / joined into the
+    caller's stream (exec.cu): inside a CUDA graph they become parallel branches.  Eager and
+    captured forward + backward (random cotangent) give the same bits, and the captured
+    graph replays correctly after the inputs change."""
+    import ctypes
+    import torch
+    from paper_2501_04194_b200.engine import compile_formula
+    B, T = 48, 3000
+    f = P.And(P.Always(P.Eventually(P.Pred("x", ">", 0.0), P.StepInterval(0, 60))),
+              P.Until(P.Pred("y", "<", 1.0), P.Pred("z", ">", 0.0), P.StepInterval(0, 90)))
+    comp = compile_formula(f, ["x", "y", "z"], P.SemanticsConfig(mode=mode))
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    ch = [torch.round(torch.randn(B, T, device="cuda", generator=gen) * 2) for _ in range(3)]
+    cot = torch.randn(B, T, device="cuda", generator=gen)
+    fb, bb = comp.workspace_bytes(B, T)
+    fws = torch.empty(fb, dtype=torch.uint8, device="cuda")
+    bws = torch.empty(bb, dtype=torch.uint8, device="cuda")
+
+    def run(out, d):
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        comp.forward(ch, [], out, fws, st)
+        comp.backward(ch, [], out, cot, d, None, fws, bws, st)
+
+    def fresh():
+        return torch.empty(B, T, device="cuda"), [torch.empty(B, T, device="cuda") for _ in range(3)]
+
+    eager = fresh()
+    run(*eager)
+    torch.cuda.synchronize()
+    cap = fresh()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run(*cap)  # warm-up on the capture stream (creates the side stream outside capture)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    cap[0].zero_()
+    for t in cap[1]:
+        t.zero_()
+    with torch.cuda.graph(g):
+        run(*cap)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(eager[0], cap[0])
+    for a, b in zip(eager[1], cap[1]):
+        assert torch.equal(a, b)
+    # new inputs in place: the replay follows them, as a fresh eager run does
+    for c in ch:
+        c.copy_(torch.round(torch.randn(B, T, device="cuda", generator=gen) * 2))
+    g.replay()
+    ref = fresh()
+    run(*ref)
+    torch.cuda.synchronize()
+    assert torch.equal(ref[0], cap[0])
+    for a, b in zip(ref[1], cap[1]):
+        assert torch.equal(a, b)

@@ -564,8 +564,9 @@ int stlg_compile(const stlg_node* nodes, int32_t n_nodes, int32_t n_channels, in
       e.aux_slot = plan->n_aux++;
     // hard timed Until on the O(T) kernels: every output's gradient source (uint16 plane),
     // so the backward routes cotangents without restaging the children or re-walking blocks
+    // (offsets <= b < 0x7fff: a right-child offset never reaches the 0xffff overrun mark)
     if (cfg->mode == STLG_MODE_HARD && e.kind == E_UNTIL && !e.untimed && !cfg->masked_fill &&
-        e.b <= 0x7fff)
+        e.b < 0x7fff)
       e.aux_slot = plan->n_aux++;
     // softmax smooth intervals: [L_hi | M_lo | L_lo] (double-float window LSE and mean)
     if (cfg->mode == STLG_MODE_SOFTMAX && e.kind == E_FG_SMOOTH) plan->n_aux += 2;

@@ -49,6 +49,7 @@ struct UParams {
   unsigned* lb;              // untimed hard: look-back slots [B][tiles][LB_WORDS] (lookback.cuh)
   unsigned short* src;            // forward, hard timed (until_ht.cu): gradient source of every
   const unsigned short* src_in;   // output as (offset from t) | 0x8000 right child; 0xffff overrun
+  int ht_nt, ht_ns;               // hard timed forward: outputs / staged positions per tile (host-set)
   ModeP mp;
 };
 

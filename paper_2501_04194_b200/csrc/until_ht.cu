@@ -26,6 +26,8 @@
 // cotangents in shared int64 fixed point at a per-tile power-of-two scale — integer
 // addition is associative, so the sums are reproducible bit for bit — then writes
 // every owned element once (no memset, no float atomics).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace stlg {
@@ -299,9 +301,10 @@ __global__ void __launch_bounds__(HT_T, 5) k_until_ht_fwd(const __grid_constant_
   extern __shared__ __align__(16) float htsm[];
   const long long row = blockIdx.y;
   const int L = (int)p.L;
-  const int NS = ht_ns(p.b), NT = NS - p.b;
+  // balanced tiles (launch_until_ht_fwd): NT outputs, NS <= ht_ns(b) staged positions
+  const int NT = p.ht_nt, NS = p.ht_ns;
   const int t0 = blockIdx.x * NT;
-  const HTArr A = ht_carve(htsm, NS, p.K);
+  const HTArr A = ht_carve(htsm, ht_ns(p.b), p.K);
   ht_prepare(p, row, t0, NS, A);
   float* outr = p.out + row * L;
   unsigned short* srcr = p.src != nullptr ? p.src + row * L : nullptr;
@@ -510,11 +513,16 @@ bool until_ht_applicable(const UParams& p) {
 }
 
 cudaError_t launch_until_ht_fwd(UParams& p, cudaStream_t st) {
-  const int NS = ht_ns(p.b), NT = NS - p.b;
+  // balanced tiles: the row's ceil(L / NTmax) tiles share its outputs evenly and each stages
+  // only its outputs + the b-halo (T = 1000 was one full tile plus a 76-output one)
+  const int NS = ht_ns(p.b), NTM = NS - p.b;
+  const long long ntl = (p.L + NTM - 1) / NTM;
+  p.ht_nt = (int)((p.L + ntl - 1) / ntl);
+  p.ht_ns = std::min(NS, (p.ht_nt + p.b + 31) & ~31);
   const size_t smem = ht_smem_bytes(NS);
   cudaError_t e = cudaFuncSetAttribute(k_until_ht_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((p.L + NT - 1) / NT), (unsigned)p.B);
+  dim3 grid((unsigned)ntl, (unsigned)p.B);
   k_until_ht_fwd<<<grid, HT_T, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();

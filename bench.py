@@ -56,7 +56,7 @@ def _config(n):
             "parallelism": f"batch-shard dp{n}" if n > 1 else "single",
             "cotangent": "ones (full-trace VJP)",
             "l2": "rotating 3 input/output sets (3 x 205 MB > 126 MB L2)",
-            "timing": "CUDA events around CUDA-graph replays of the fwd / bwd launches"}
+            "timing": "CUDA events around K replays of one CUDA graph per step (fwd + bwd launches); the fwd / bwd split from per-phase graph replays"}
 
 
 def _walk(B, T, seed):
@@ -610,9 +610,18 @@ def run_b200(args, rank, world):
         with torch.cuda.graph(gb):
             bwd(s)
         graphs.append((gf, gb))
+    # and one graph per set holding the whole step (fwd + bwd): the timed steps
+    steps_g = []
+    for s in range(NSET):
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            fwd(s)
+            bwd(s)
+        steps_g.append(g1)
     for i in range(max(args.warmup, 3)):
         graphs[i % NSET][0].replay()
         graphs[i % NSET][1].replay()
+        steps_g[i % NSET].replay()
     torch.cuda.synchronize()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
@@ -623,13 +632,16 @@ def run_b200(args, rank, world):
     with ClockSampler(local) as clk:
         start.record(stream)
         for i in range(args.steps):
+            steps_g[i % NSET].replay()
+        stop.record(stream)
+        # the fwd / bwd split (roofline of each kernel): the per-phase graphs, events between
+        for i in range(args.steps):
             gf, gb = graphs[i % NSET]
             evs[i][0].record(stream)
             gf.replay()
             evs[i][1].record(stream)
             gb.replay()
             evs[i][2].record(stream)
-        stop.record(stream)
         torch.cuda.synchronize()
         if clk.proc is not None and len(clk.lines) < 3:
             # the timed region is shorter than the sampling period: keep the GPU under the

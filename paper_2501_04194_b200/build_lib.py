@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libstlg.so")
 SOURCES = ["exec.cu", "fg.cu", "fg_reg_fwd.cu", "fg_unt.cu", "fg_soft64.cu", "until.cu", "until_ht.cu", "smooth.cu", "mining.cu"]
 # (object name, source, defines): fg_reg_inst.cu once per tile width and direction
 VARIANTS = [(f"fg_reg_{'b' if bwd else 'f'}{nw}", "fg_reg_inst.cu", [f"-DREG_NW={nw}", f"-DREG_BWD={bwd}"])
-            for bwd in (1, 0) for nw in (4, 5, 6, 7, 8)]
+            for bwd in (1, 0) for nw in (3, 4, 5, 6, 7, 8)]
 HEADERS = ["common.cuh", "kernels.cuh", "fg_reg.cuh", "fg_cav.cuh", "detacc.cuh", "lookback.cuh"]
 UNITS = [(os.path.splitext(s)[0], s, []) for s in SOURCES] + VARIANTS
 

@@ -617,10 +617,12 @@ __global__ void __launch_bounds__(RC<NW>::T, RC<NW>::MINB_B) k_reg_bwd_hard(cons
 // even with more staged overlap (C2: 0.041 vs 0.043 ms at NW = 7); backward widths
 // minimise the staged samples per row.
 inline int reg_pick_nw(long long L, int K, bool hard_bwd, bool fwd = false) {
-  if (fwd && 2048LL >= 4LL * K) return 4;
+  // short rows (L < 2048) may take 3-warp tiles (1536 samples) when those stage less
+  const int nw_min = L < 2048 ? 3 : 4;
+  if (fwd && 2048LL >= 4LL * K) return (nw_min == 3 && 1536LL >= 4LL * K && L <= 1536 - K + 1) ? 3 : 4;
   int best = -1;
   long long best_cost = 0;
-  for (int nw = 8; nw >= 4; --nw) {
+  for (int nw = 8; nw >= nw_min; --nw) {
     const long long N = 512LL * nw;
     if (N < 4LL * K) continue;
     const long long J = hard_bwd ? N - 2 * K + 2 : N - K + 1;
@@ -647,6 +649,7 @@ inline cudaError_t reg_launch(KernT k, dim3 grid, int threads, size_t smem, cons
 
 #define REG_DISPATCH_NW(NWV, ...)                 \
   switch (NWV) {                                  \
+    case 3: { constexpr int NW = 3; __VA_ARGS__; } break; \
     case 4: { constexpr int NW = 4; __VA_ARGS__; } break; \
     case 5: { constexpr int NW = 5; __VA_ARGS__; } break; \
     case 6: { constexpr int NW = 6; __VA_ARGS__; } break; \

@@ -8,7 +8,7 @@
 #include "fg_cav.cuh"
 
 #ifndef REG_NW
-#error "compile with -DREG_NW=4..8 -DREG_BWD=0|1 (build_lib.py)"
+#error "compile with -DREG_NW=3..8 -DREG_BWD=0|1 (build_lib.py)"
 #endif
 
 namespace stlg {
